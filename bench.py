@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""bench.py — the headline measurement (BASELINE.json metric on configs[1] = C2):
+1,048,576 fp32 32x32 matrices, i.i.d. N(0,1), seed 1, inverted per step by one
+gj_invert_batched call (outputs: inverse, log|det|, sign — exactly BASELINE's outputs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL process group for the barrier and
+the max-over-ranks timing only): batches shard with no data-path collective, every rank
+inverts its own full C2-sized batch (weak scaling; rank r > 0 draws from seed (1, r)).
+`--impl reference` times the CPU oracle (oracle/, long double, all host cores) on a
+bounded sample of the same workload.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "matrices inverted/s (batched n=32 fp32)"
+UNIT = "matrices/s"
+N = 32
+BATCH = 1048576
+BYTES_PER_MATRIX = N * N * 4 * 2 + 8 + 1           # A in, A^-1 out, logabsdet fp64, sign int8
+FLOPS_PER_MATRIX = 2 * N ** 3 - N ** 2              # SURVEY.md §8a (n steps x [n(n-1) FMA + n scalings])
+WORKLOAD = "C2: batch 1048576 x 32x32 fp32, N(0,1), seed 1 (BASELINE.json configs[1])"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=BATCH, help="items per GPU (default: the C2 config)")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=65536, help="oracle sample size (items)")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profile_traffic():
+    """dram read+write bytes per launch of the K1 kernel from the committed ncu --set full
+    capture (profiles/*_k1_traffic.json), or None."""
+    pdir = os.path.join(ROOT, "profiles")
+    best = None
+    if os.path.isdir(pdir):
+        for fn in sorted(os.listdir(pdir)):
+            if fn.endswith("_k1_traffic.json"):
+                with open(os.path.join(pdir, fn)) as f:
+                    d = json.load(f)
+                if d.get("workload_batch") == BATCH:
+                    best = d
+    return None if best is None else float(best["dram_bytes_per_launch"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), float(f[3]), f[5], f[6], f[7], f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0}
+        load = [r for r in rows if r[2] > 200.0] or rows
+        reasons = set()
+        for r in load:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[3:]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median([r[0] for r in load])), "sm_max_mhz": max(r[1] for r in load),
+                "reasons": sorted(reasons), "samples": len(load)}
+
+
+def cpu_baseline(sample: int):
+    """The oracle as it stands, on the host's cores, on the first `sample` items of C2."""
+    import oracle
+    import synth
+    A = synth.gen_c2(batch=sample)
+    nth = oracle.threads()
+    t0 = time.perf_counter()
+    oracle.invert_batched(A, tol=N * 2.0 ** -23, nthreads=nth)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": UNIT, "cores": nth, "kind": "oracle",
+            "sample": f"first {sample} items of C2 (seed 1), long-double [A|I] GJ, {dt:.2f} s wall"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    sample = min(args.cpu_sample, 16384)
+    A = synth.gen_c2(batch=sample)
+    nth = oracle.threads()
+    for _ in range(args.warmup):
+        oracle.invert_batched(A[: min(256, sample)], tol=N * 2.0 ** -23, nthreads=nth)
+    times = []
+    for _ in range(args.steps if args.steps <= 5 else 5):
+        t0 = time.perf_counter()
+        oracle.invert_batched(A, tol=N * 2.0 ** -23, nthreads=nth)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    val = sample / dt
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": len(times), "warmup": args.warmup, "ms_per_step": dt * 1e3 * BATCH / sample,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f80 (x87 long double)",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": BATCH * world, "n": N,
+                                             "parallelism": "cpu-openmp", "sample_items_per_step": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": nth, "kind": "oracle",
+                             "sample": f"first {sample} items of C2 per step (bounded sample)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import paper_1401_7962_b200 as gj
+    import synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    B = args.batch
+    # ---- synthetic input (host generation is outside every timed region)
+    if rank == 0:
+        A_host = synth.gen_c2(batch=B)
+    else:
+        A_host = np.empty((B, N, N), np.float32)
+        rng = np.random.default_rng([1, rank])
+        for s in range(0, B, synth.C2_CHUNK):
+            e = min(B, s + synth.C2_CHUNK)
+            A_host[s:e] = rng.standard_normal((e - s, N, N), dtype=np.float32)
+    A = torch.from_numpy(A_host).to(dev)
+    X = torch.empty_like(A)
+    lg = torch.empty((B,), dtype=torch.float64, device=dev)
+    sg = torch.empty((B,), dtype=torch.int8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    tol = N * 2.0 ** -23
+
+    def step():
+        st = gj.lib.gj_invert_batched(0, N, B, A.data_ptr(), X.data_ptr(), None, lg.data_ptr(), sg.data_ptr(),
+                                      None, None, tol, stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = [a.elapsed_time(b) for a, b in ev]
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * B / (ms_per_step / 1e3)
+    avg_launch_ms = float(np.mean(launch_ms))
+
+    # ---- end to end through the public API with HOST buffers (pinned), copies inside
+    e2e = None
+    if args.e2e_steps > 0:
+        del X
+        torch.cuda.empty_cache()
+        Ah = torch.from_numpy(A_host).pin_memory()
+        Xh = torch.empty_like(Ah).pin_memory()
+        lgh = torch.empty((B,), dtype=torch.float64).pin_memory()
+        sgh = torch.empty((B,), dtype=torch.int8).pin_memory()
+        gj.invert_batched_host(Ah, out=Xh, logabsdet=lgh, sign=sgh, tol=tol)  # warm-up
+        barrier()
+        ts = []
+        for _ in range(args.e2e_steps):
+            barrier()
+            t0 = time.perf_counter()
+            gj.invert_batched_host(Ah, out=Xh, logabsdet=lgh, sign=sgh, tol=tol)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = float(np.mean(ts))
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * B / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Ah.numel() * 4),
+               "d2h_bytes_per_step": int(Xh.numel() * 4 + B * 9), "ms_per_step": e2e_s * 1e3,
+               "api": "gj_invert_batched_host (pinned host buffers, chunked H2D/compute/D2H pipeline)"}
+
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        achieved = B * BYTES_PER_MATRIX / (avg_launch_ms / 1e3) / 1e9
+        traffic = profile_traffic()
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "gj_batched_warp_kernel<float,32,true> (K1)",
+                "algorithmic_bytes_per_launch": B * BYTES_PER_MATRIX, "peak_source": peak_src,
+                "fp32_flops_per_launch": B * FLOPS_PER_MATRIX,
+                "achieved_fp32_tflops": B * FLOPS_PER_MATRIX / (avg_launch_ms / 1e3) / 1e12}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "global_batch": B * world, "n": N, "per_gpu_batch": B,
+                           "parallelism": f"dp{world} (independent shards, no collective)",
+                           "l2": "inputs (4 GiB/GPU) larger than L2 (126 MB); no flush needed",
+                           "outputs": "inverse, logabsdet, sign"},
+                "roofline": roof, "gpu_launches": args.steps, "clocks": clk.summary(), "e2e": e2e}
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,139 @@
+/*
+ * gjinv.h — C-ABI of the B200-native Gauss–Jordan inversion library (libgjinv.so).
+ *
+ * The operation (arxiv 1401.7962, /root/reference/PAPER.md):
+ *   Gauss–Jordan diagonalisation of the augmented system [A | I] -> [I | A^-1]
+ *   (§2, Eqs. (1)-(2) L24-L28, row-operation form Eqs. (14)-(15) L61-L72, result
+ *   Eq. (12)), with the pivot chosen as the max-|a_ik| candidate of column k
+ *   (Obs. 3, L60; listing L151-L154), the swaps undone at the end ("depivotarea",
+ *   Obs. 3 L60, listing L179-L198, §4), a pivot below a stated zero threshold
+ *   flagging the matrix singular (Obs. 2, L59), and det A as the signed product of
+ *   the pivots (Eq. (13); §4).
+ *
+ * Readings of the paper that fix the contract (DESIGN.md §3 lists all of them):
+ *   - pivot candidates: rows not yet pivoted; ties -> smallest row index (G3);
+ *   - zero threshold: RELATIVE — item is singular at the first step k whose largest
+ *     candidate |a_rk| <= tol * max_ij |a_ij| (G1); tol = 0 flags exact zeros only;
+ *     tol < 0 selects GJ_TOL_DEFAULT = n * eps(dtype);
+ *   - det = (-1)^(#swaps) * prod(pivots) (G4 — Eq. (13) omits the swap sign);
+ *   - ipiv: LAPACK-style 1-based swap sequence: at step k (1-based) the pivot row is
+ *     the row then at position ipiv[k] of the physically-swapped matrix (the listing's
+ *     p[k] = j, L154; reading G13).  Equal to LAPACK getrf's ipiv.
+ *
+ * Conventions for every entry point
+ *   Ownership: the caller owns every buffer; the library never frees or keeps
+ *     pointers.  Device entry points take DEVICE pointers and enqueue all work on
+ *     `stream` (a cudaStream_t passed as void*, NULL = legacy default stream); they
+ *     return as soon as the work is enqueued; outputs are valid once the caller
+ *     synchronises that stream.  Host entry points (suffix _host) take HOST pointers
+ *     and are synchronous.
+ *   Layout: matrices are dense row-major, item b of a batch at offset b*n*n
+ *     elements (contiguous batch), base addresses 16-byte aligned for the fastest
+ *     path (any element-aligned address is accepted).
+ *   Errors: the returned gj_status reports argument / launch / CUDA errors known at
+ *     enqueue time.  Numerical singularity is per-item DATA in `info` and never
+ *     aborts a batch: info[b] = 0 if item b is regular, else the first failing step
+ *     k (1-based); for such items det = 0, sign = 0, logabsdet = -inf, and the
+ *     inverse and ipiv contents are unspecified.
+ *   Inputs containing NaN/Inf give unspecified results (not validated).
+ *   Optional outputs: any output pointer documented "or NULL" may be NULL and is
+ *     then not computed / written.
+ */
+#ifndef GJINV_H
+#define GJINV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { GJ_F32 = 0, GJ_F64 = 1 } gj_dtype;
+
+typedef enum {
+    GJ_OK = 0,
+    GJ_ERR_ARG = 1,          /* invalid argument (NULL required pointer, n < 1, batch < 0, ...)  */
+    GJ_ERR_UNSUPPORTED = 2,  /* (dtype, n) combination not supported by this entry point        */
+    GJ_ERR_WORKSPACE = 3,    /* workspace too small                                             */
+    GJ_ERR_CUDA = 4,         /* a CUDA runtime call or kernel launch failed                      */
+    GJ_ERR_NCCL = 5          /* an NCCL call failed (distributed entry points)                   */
+} gj_status;
+
+#define GJ_TOL_DEFAULT (-1.0)  /* => tol = n * eps(dtype), relative to max|a_ij| of each matrix */
+
+/* Largest n accepted by the batched (one matrix per warp / CTA) entry points. */
+#define GJ_BATCHED_MAX_N 64
+
+/*
+ * gj_invert_batched — invert `batch` independent n x n matrices (1 <= n <= 64).
+ *   dt         GJ_F32 or GJ_F64: element type of A, Ainv and det; the arithmetic is
+ *              done in this type (logabsdet is accumulated in fp64 for both).
+ *   n, batch   matrix order and item count (batch = 0 is a no-op).
+ *   A          [batch][n][n] input, read only.
+ *   Ainv       [batch][n][n] output A^-1 (Eq. (12)), may equal A (in place), or NULL
+ *              (determinant-only run).
+ *   ipiv       [batch][n] int32 1-based swap sequence, or NULL.
+ *   logabsdet  [batch] fp64 log|det A| = sum_k log|p_k|, or NULL.
+ *   sign       [batch] int8 in {-1, 0, +1}, or NULL.
+ *   det        [batch] det A in dtype `dt` (may overflow to +-inf), or NULL.
+ *   info       [batch] int32 singular flag (see above), or NULL.
+ *   tol        relative zero threshold; < 0 selects GJ_TOL_DEFAULT.
+ *   stream     cudaStream_t.
+ * Returns GJ_OK, GJ_ERR_ARG, GJ_ERR_UNSUPPORTED (n > 64) or GJ_ERR_CUDA.
+ */
+gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
+                            int32_t* ipiv, double* logabsdet, int8_t* sign, void* det,
+                            int32_t* info, double tol, void* stream);
+
+/*
+ * gj_det — determinants only (Eq. (13); §4 "without laborious extra computation"):
+ * the same elimination as gj_invert_batched without storing A^-1.
+ * Arguments as gj_invert_batched; `workspace`/`workspace_bytes` are used for n > 64
+ * (batch must then be 1; size from gj_workspace_size(dt, n, 1, 2)), else may be NULL/0.
+ */
+gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logabsdet,
+                 int8_t* sign, void* det, int32_t* ipiv, int32_t* info, double tol,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * gj_invert — one n x n matrix, any n >= 1 (n <= 64 uses the batched kernels; larger n
+ * the blocked Gauss–Jordan: panel factorisation + FP64 tensor-core trailing updates,
+ * the aggregated form of Eqs. (14)-(15)).
+ *   A, lda       input (row stride lda >= n elements), read only.
+ *   Ainv, ldainv output (row stride ldainv >= n); may equal A when lda == ldainv.
+ *   ipiv, logabsdet, sign, info  as gj_invert_batched with batch = 1 (each may be NULL).
+ *   workspace    device buffer of at least gj_workspace_size(dt, n, 1, 1) bytes (may be
+ *                NULL when that size is 0).
+ */
+gj_status gj_invert(gj_dtype dt, int n, const void* A, int64_t lda, void* Ainv, int64_t ldainv,
+                    int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Workspace bytes for entry 0 = gj_invert_batched (always 0), 1 = gj_invert, 2 = gj_det. */
+size_t gj_workspace_size(gj_dtype dt, int n, int64_t batch, int entry);
+
+/*
+ * gj_invert_batched_host — gj_invert_batched on HOST buffers (synchronous).  The library
+ * allocates device staging buffers for `chunk` items at a time (chunk <= 0: automatic)
+ * and pipelines host->device copy, inversion and device->host copy of consecutive
+ * chunks on its own streams.  Pinned (page-locked) host buffers give overlapped copies;
+ * pageable buffers work but copy synchronously.  Ainv must not alias A.
+ * Returns as gj_invert_batched; all device memory it allocated is freed before return.
+ */
+gj_status gj_invert_batched_host(gj_dtype dt, int n, int64_t batch, const void* A_host,
+                                 void* Ainv_host, int32_t* ipiv_host, double* logabsdet_host,
+                                 int8_t* sign_host, void* det_host, int32_t* info_host,
+                                 double tol, int64_t chunk);
+
+/* Static description of a status code. */
+const char* gj_status_string(gj_status s);
+
+/* Library version, e.g. "gjinv 0.1.0 sm_100a". */
+const char* gj_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GJINV_H */

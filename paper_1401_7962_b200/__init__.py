@@ -1,0 +1,194 @@
+"""paper_1401_7962_b200 — B200-native Gauss–Jordan inversion (arxiv 1401.7962).
+
+Thin Python binding over the C-ABI library ``libgjinv.so`` (``include/gjinv.h``).
+Argument marshalling only: torch supplies device memory and the current CUDA stream;
+every step of the method runs in the library's sm_100a kernels.  There is no CPU
+fallback: if the library cannot be loaded, importing this package raises.
+
+Entry points mirror the C names: :func:`invert_batched`, :func:`invert`, :func:`det`,
+:func:`invert_batched_host`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from collections import namedtuple
+from typing import Optional
+
+from ._build import LIB as _LIB_PATH
+
+__all__ = ["invert_batched", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
+           "TOL_DEFAULT", "Result"]
+
+TOL_DEFAULT = -1.0
+GJ_F32, GJ_F64 = 0, 1
+
+
+class GJError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"libgjinv.so not built at {_LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(_LIB_PATH)
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.gj_invert_batched.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, dbl, vp]
+    L.gj_invert_batched.restype = i32
+    L.gj_det.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
+    L.gj_det.restype = i32
+    L.gj_invert.argtypes = [i32, i32, vp, i64, vp, i64, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
+    L.gj_invert.restype = i32
+    L.gj_workspace_size.argtypes = [i32, i32, i64, i32]
+    L.gj_workspace_size.restype = ctypes.c_size_t
+    L.gj_invert_batched_host.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, dbl, i64]
+    L.gj_invert_batched_host.restype = i32
+    L.gj_status_string.argtypes = [i32]
+    L.gj_status_string.restype = ctypes.c_char_p
+    L.gj_version.restype = ctypes.c_char_p
+    return L
+
+
+lib = _load()
+library_path = _LIB_PATH
+
+Result = namedtuple("Result", ["inverse", "logabsdet", "sign", "det", "ipiv", "info"])
+
+
+def _check(st: int):
+    if st != 0:
+        raise GJError(lib.gj_status_string(st).decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dt(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return GJ_F32
+    if t.dtype == torch.float64:
+        return GJ_F64
+    raise TypeError(f"unsupported dtype {t.dtype} (float32 / float64)")
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def invert_batched(A, tol: Optional[float] = None, *, out=None, inverse: bool = True, ipiv: bool = True,
+                   logabsdet: bool = True, sign: bool = True, det: bool = True, info: bool = True,
+                   stream=None) -> Result:
+    """Invert a batch ``A`` ([B, n, n] or [n, n], float32/float64, CUDA, contiguous) with
+    ``gj_invert_batched``.  ``tol``: relative zero threshold (None → n·eps).  ``out`` may be
+    ``A`` itself for an in-place inversion.  Unrequested outputs are None."""
+    torch = _torch()
+    if not A.is_cuda:
+        raise ValueError("A must be a CUDA tensor (use invert_batched_host for host buffers)")
+    squeeze = A.dim() == 2
+    if squeeze:
+        A = A.unsqueeze(0)
+    if A.dim() != 3 or A.shape[1] != A.shape[2]:
+        raise ValueError("A must be [B, n, n]")
+    if not A.is_contiguous():
+        raise ValueError("A must be contiguous")
+    B, n = A.shape[0], A.shape[1]
+    dev = A.device
+    X = None
+    if inverse:
+        X = out if out is not None else torch.empty_like(A)
+    o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev) if ipiv else None
+    o_lg = torch.empty((B,), dtype=torch.float64, device=dev) if logabsdet else None
+    o_sg = torch.empty((B,), dtype=torch.int8, device=dev) if sign else None
+    o_det = torch.empty((B,), dtype=A.dtype, device=dev) if det else None
+    o_info = torch.empty((B,), dtype=torch.int32, device=dev) if info else None
+    with torch.cuda.device(dev):
+        st = lib.gj_invert_batched(_dt(A), n, B, A.data_ptr(), _ptr(X), _ptr(o_ipiv), _ptr(o_lg), _ptr(o_sg),
+                                   _ptr(o_det), _ptr(o_info), TOL_DEFAULT if tol is None else float(tol),
+                                   _stream_ptr(stream))
+    _check(st)
+    if squeeze:
+        sq = lambda t: None if t is None else t[0]
+        return Result(sq(X), sq(o_lg), sq(o_sg), sq(o_det), sq(o_ipiv), sq(o_info))
+    return Result(X, o_lg, o_sg, o_det, o_ipiv, o_info)
+
+
+def det(A, tol: Optional[float] = None, *, stream=None) -> Result:
+    """Determinants only (``gj_det``): logabsdet, sign, det, ipiv, info; inverse is None."""
+    torch = _torch()
+    squeeze = A.dim() == 2
+    if squeeze:
+        A = A.unsqueeze(0)
+    B, n = A.shape[0], A.shape[1]
+    dev = A.device
+    o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev)
+    o_lg = torch.empty((B,), dtype=torch.float64, device=dev)
+    o_sg = torch.empty((B,), dtype=torch.int8, device=dev)
+    o_det = torch.empty((B,), dtype=A.dtype, device=dev)
+    o_info = torch.empty((B,), dtype=torch.int32, device=dev)
+    ws_bytes = lib.gj_workspace_size(_dt(A), n, B, 2)
+    ws = torch.empty((max(ws_bytes, 1),), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        st = lib.gj_det(_dt(A), n, B, A.data_ptr(), o_lg.data_ptr(), o_sg.data_ptr(), o_det.data_ptr(),
+                        o_ipiv.data_ptr(), o_info.data_ptr(), TOL_DEFAULT if tol is None else float(tol),
+                        ws.data_ptr(), ws_bytes, _stream_ptr(stream))
+    _check(st)
+    if squeeze:
+        return Result(None, o_lg[0], o_sg[0], o_det[0], o_ipiv[0], o_info[0])
+    return Result(None, o_lg, o_sg, o_det, o_ipiv, o_info)
+
+
+def invert(A, tol: Optional[float] = None, *, out=None, stream=None) -> Result:
+    """One matrix of any order (``gj_invert``); strided rows are allowed."""
+    torch = _torch()
+    if A.dim() != 2 or A.shape[0] != A.shape[1] or A.stride(1) != 1:
+        raise ValueError("A must be [n, n] with unit column stride")
+    n = A.shape[0]
+    dev = A.device
+    X = out if out is not None else torch.empty((n, n), dtype=A.dtype, device=dev)
+    o_ipiv = torch.empty((n,), dtype=torch.int32, device=dev)
+    o_lg = torch.empty((1,), dtype=torch.float64, device=dev)
+    o_sg = torch.empty((1,), dtype=torch.int8, device=dev)
+    o_info = torch.empty((1,), dtype=torch.int32, device=dev)
+    ws_bytes = lib.gj_workspace_size(_dt(A), n, 1, 1)
+    ws = torch.empty((max(ws_bytes, 1),), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        st = lib.gj_invert(_dt(A), n, A.data_ptr(), A.stride(0), X.data_ptr(), X.stride(0), o_ipiv.data_ptr(),
+                           o_lg.data_ptr(), o_sg.data_ptr(), o_info.data_ptr(),
+                           TOL_DEFAULT if tol is None else float(tol), ws.data_ptr(), ws_bytes,
+                           _stream_ptr(stream))
+    _check(st)
+    return Result(X, o_lg[0], o_sg[0], None, o_ipiv, o_info[0])
+
+
+def invert_batched_host(A, tol: Optional[float] = None, *, out=None, ipiv=None, logabsdet=None, sign=None,
+                        det=None, info=None, chunk: int = 0):
+    """``gj_invert_batched_host`` on host (CPU) tensors/arrays; synchronous.  ``out`` and the
+    optional side outputs are caller-provided host buffers (pinned → overlapped copies)."""
+    def ptr(t):
+        if t is None:
+            return None
+        if hasattr(t, "data_ptr"):
+            return t.data_ptr()
+        return t.ctypes.data
+    torch = _torch()
+    if hasattr(A, "dtype") and A.dtype in (torch.float32, torch.float64):
+        dt = _dt(A)
+    else:
+        import numpy as np
+        dt = GJ_F32 if A.dtype == np.float32 else GJ_F64
+    B, n = A.shape[0], A.shape[1]
+    st = lib.gj_invert_batched_host(dt, n, B, ptr(A), ptr(out), ptr(ipiv), ptr(logabsdet), ptr(sign), ptr(det),
+                                    ptr(info), TOL_DEFAULT if tol is None else float(tol), int(chunk))
+    _check(st)
+    return out

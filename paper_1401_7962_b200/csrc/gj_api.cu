@@ -1,0 +1,159 @@
+// libgjinv C-ABI (include/gjinv.h): argument validation, dispatch on (dtype, n),
+// stream handling and the host-buffer pipeline.  No compute happens here: every step
+// of the method runs in the kernels of gj_batched.cu / gj_large.cu.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "gj_internal.h"
+
+namespace gj {
+
+int device_sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+static double resolve_tol(gj_dtype dt, int n, double tol) {
+  if (tol >= 0.0) return tol;
+  const double eps = dt == GJ_F32 ? 1.1920928955078125e-07 : 2.220446049250313e-16;
+  return n * eps;
+}
+
+static size_t esize(gj_dtype dt) { return dt == GJ_F32 ? 4 : 8; }
+
+}  // namespace gj
+
+using namespace gj;
+
+extern "C" {
+
+const char* gj_status_string(gj_status s) {
+  switch (s) {
+    case GJ_OK: return "GJ_OK";
+    case GJ_ERR_ARG: return "GJ_ERR_ARG: invalid argument";
+    case GJ_ERR_UNSUPPORTED: return "GJ_ERR_UNSUPPORTED: (dtype, n) not supported by this entry point";
+    case GJ_ERR_WORKSPACE: return "GJ_ERR_WORKSPACE: workspace too small";
+    case GJ_ERR_CUDA: return "GJ_ERR_CUDA: CUDA runtime / launch failure";
+    case GJ_ERR_NCCL: return "GJ_ERR_NCCL: NCCL failure";
+  }
+  return "unknown gj_status";
+}
+
+const char* gj_version(void) { return "gjinv 0.1.0 sm_100a"; }
+
+gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
+                            int32_t* ipiv, double* logabsdet, int8_t* sign, void* det,
+                            int32_t* info, double tol, void* stream) {
+  if (dt != GJ_F32 && dt != GJ_F64) return GJ_ERR_ARG;
+  if (n < 1 || batch < 0) return GJ_ERR_ARG;
+  if (batch == 0) return GJ_OK;
+  if (A == nullptr) return GJ_ERR_ARG;
+  if (n > 32) return GJ_ERR_UNSUPPORTED;
+  BatchedArgs a{n, batch, A, Ainv, ipiv, logabsdet, sign, det, info, resolve_tol(dt, n, tol)};
+  cudaError_t e = launch_batched(dt, a, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
+size_t gj_workspace_size(gj_dtype dt, int n, int64_t batch, int entry) {
+  (void)batch;
+  if (n < 1) return 0;
+  if (entry == 1 && n <= GJ_BATCHED_MAX_N) return (size_t)n * n * esize(dt);  // lda != n repack
+  return 0;
+}
+
+gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logabsdet,
+                 int8_t* sign, void* det, int32_t* ipiv, int32_t* info, double tol,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+  (void)workspace; (void)workspace_bytes;
+  if (n > GJ_BATCHED_MAX_N) return GJ_ERR_UNSUPPORTED;
+  return gj_invert_batched(dt, n, batch, A, nullptr, ipiv, logabsdet, sign, det, info, tol, stream);
+}
+
+gj_status gj_invert(gj_dtype dt, int n, const void* A, int64_t lda, void* Ainv, int64_t ldainv,
+                    int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (dt != GJ_F32 && dt != GJ_F64) return GJ_ERR_ARG;
+  if (n < 1 || A == nullptr || Ainv == nullptr || lda < n || ldainv < n) return GJ_ERR_ARG;
+  if (n > GJ_BATCHED_MAX_N) return GJ_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t es = esize(dt);
+  if (lda == n && ldainv == n)
+    return gj_invert_batched(dt, n, 1, A, Ainv, ipiv, logabsdet, sign, nullptr, info, tol, stream);
+  // strided: repack into the workspace, invert in place, unpack
+  if (workspace == nullptr || workspace_bytes < (size_t)n * n * es) return GJ_ERR_WORKSPACE;
+  if (cudaMemcpy2DAsync(workspace, n * es, A, lda * es, n * es, n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return GJ_ERR_CUDA;
+  gj_status st = gj_invert_batched(dt, n, 1, workspace, workspace, ipiv, logabsdet, sign, nullptr, info, tol, stream);
+  if (st != GJ_OK) return st;
+  if (cudaMemcpy2DAsync(Ainv, ldainv * es, workspace, n * es, n * es, n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return GJ_ERR_CUDA;
+  return GJ_OK;
+}
+
+gj_status gj_invert_batched_host(gj_dtype dt, int n, int64_t batch, const void* A_host,
+                                 void* Ainv_host, int32_t* ipiv_host, double* logabsdet_host,
+                                 int8_t* sign_host, void* det_host, int32_t* info_host,
+                                 double tol, int64_t chunk) {
+  if (dt != GJ_F32 && dt != GJ_F64) return GJ_ERR_ARG;
+  if (n < 1 || batch < 0 || A_host == nullptr) return GJ_ERR_ARG;
+  if (n > GJ_BATCHED_MAX_N) return GJ_ERR_UNSUPPORTED;
+  if (batch == 0) return GJ_OK;
+  if (Ainv_host == A_host) return GJ_ERR_ARG;
+  const size_t es = esize(dt);
+  const size_t mat = (size_t)n * n * es;
+  if (chunk <= 0) {
+    chunk = (int64_t)((64u << 20) / mat);
+    if (chunk < 1) chunk = 1;
+  }
+  if (chunk > batch) chunk = batch;
+  constexpr int NB = 3;  // buffers / streams in flight: H2D(c+1) | kernel(c) | D2H(c-1)
+  struct Buf {
+    cudaStream_t s = nullptr;
+    void* X = nullptr; int32_t* ipiv = nullptr; double* lg = nullptr;
+    int8_t* sg = nullptr; void* det = nullptr; int32_t* info = nullptr;
+  } b[NB];
+  gj_status st = GJ_OK;
+  auto ck = [&](cudaError_t e) { if (e != cudaSuccess && st == GJ_OK) st = GJ_ERR_CUDA; return e == cudaSuccess; };
+  for (int i = 0; i < NB && st == GJ_OK; ++i) {
+    ck(cudaStreamCreateWithFlags(&b[i].s, cudaStreamNonBlocking));
+    ck(cudaMalloc(&b[i].X, mat * chunk));
+    if (ipiv_host) ck(cudaMalloc(&b[i].ipiv, sizeof(int32_t) * n * chunk));
+    if (logabsdet_host) ck(cudaMalloc(&b[i].lg, sizeof(double) * chunk));
+    if (sign_host) ck(cudaMalloc(&b[i].sg, chunk));
+    if (det_host) ck(cudaMalloc(&b[i].det, es * chunk));
+    if (info_host) ck(cudaMalloc(&b[i].info, sizeof(int32_t) * chunk));
+  }
+  const char* Ah = static_cast<const char*>(A_host);
+  char* Xh = static_cast<char*>(Ainv_host);
+  for (int64_t c0 = 0, ci = 0; c0 < batch && st == GJ_OK; c0 += chunk, ++ci) {
+    Buf& B = b[ci % NB];
+    const int64_t m = (batch - c0) < chunk ? (batch - c0) : chunk;
+    ck(cudaMemcpyAsync(B.X, Ah + c0 * mat, m * mat, cudaMemcpyHostToDevice, B.s));
+    gj_status k = gj_invert_batched(dt, n, m, B.X, Xh ? B.X : nullptr, B.ipiv, B.lg, B.sg, B.det, B.info, tol, B.s);
+    if (k != GJ_OK && st == GJ_OK) st = k;
+    if (Xh) ck(cudaMemcpyAsync(Xh + c0 * mat, B.X, m * mat, cudaMemcpyDeviceToHost, B.s));
+    if (ipiv_host) ck(cudaMemcpyAsync(ipiv_host + c0 * n, B.ipiv, sizeof(int32_t) * n * m, cudaMemcpyDeviceToHost, B.s));
+    if (logabsdet_host) ck(cudaMemcpyAsync(logabsdet_host + c0, B.lg, sizeof(double) * m, cudaMemcpyDeviceToHost, B.s));
+    if (sign_host) ck(cudaMemcpyAsync(sign_host + c0, B.sg, m, cudaMemcpyDeviceToHost, B.s));
+    if (det_host) ck(cudaMemcpyAsync(static_cast<char*>(det_host) + c0 * es, B.det, es * m, cudaMemcpyDeviceToHost, B.s));
+    if (info_host) ck(cudaMemcpyAsync(info_host + c0, B.info, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, B.s));
+  }
+  for (int i = 0; i < NB; ++i) {
+    if (b[i].s) ck(cudaStreamSynchronize(b[i].s));
+    cudaFree(b[i].X); cudaFree(b[i].ipiv); cudaFree(b[i].lg); cudaFree(b[i].sg); cudaFree(b[i].det); cudaFree(b[i].info);
+    if (b[i].s) cudaStreamDestroy(b[i].s);
+  }
+  return st;
+}
+
+}  // extern "C"
