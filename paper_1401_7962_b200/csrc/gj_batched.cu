@@ -1,294 +1,67 @@
-// K1 — batched Gauss–Jordan inversion for n <= 32 on sm_100a: one matrix per group of
-// NP lanes (NP = next power of two >= n, so 32/NP matrices per warp), lane = matrix row,
-// the row held in registers for the whole elimination.
+// K1 — batched Gauss–Jordan inversion for n <= 32 on sm_100a.
 //
-// Per step k (§2, Eqs. (14)-(15), L61-L72; listing L150-L177), per group:
-//   a2  pivot search over the rows not yet pivoted: max |x_ik| via one redux.sync on the
-//       IEEE bit pattern of |x| (monotone for non-negative floats; fp64: high word, then
+// One matrix per group of NP lanes (NP = next power of two >= n; 32/NP matrices per
+// warp), lane i holds row i of the compact working array in registers for the whole
+// elimination.  Per step k (§2, Eqs. (14)-(15), L61-L72; listing L150-L177):
+//   a2  pivot search over the rows not yet pivoted: max |x_ik| by one redux.sync on the
+//       IEEE bit pattern of |x| (monotone for non-negative floats; fp64: high word then
 //       low word); among equal candidates the row at the smallest PHYSICAL position wins
-//       (second redux.sync min) — exactly the listing's first-maximum scan over the
+//       (second redux.sync, min) — exactly the listing's first-maximum scan over the
 //       physically swapped rows k..n (L151-L153, Obs. 3 L60; reading G3).
-//   a3  logical swap: rows never move; each lane tracks the physical position its row
-//       would have in the listing's swapped array, which yields LAPACK-style ipiv (the
-//       listing's p[k] = j, L154) and, at the end, the step at which the row was pivot.
-//   a4  pivot-row normalisation is DEFERRED: the pivot row is published un-normalised and
-//       keeps the scale 1/p; every other row uses f_i = x_ik * (1/p), which is exactly the
-//       multiplier of Eq. (15) (-a_ik^{k-1} times a_kj^k = a_kj^{k-1} / p).
-//   a5  x_ij -= f_i * x_rj for j != k (Eq. (15)), FFMA2 (fma.rn.f32x2) for fp32; compact
-//       storage: column k becomes the new D column (-f_i; 1 on the pivot row).
-//   a6  log|det| = sum log|p_k| (fp64), sign = (-1)^swaps * prod sign(p_k) (Eq. (13), G4).
-//   a7  un-permutation on store: Ainv[k][perm[k']] = (1/p_{perm[k]}) * X[perm[k]][k']
-//       (the listing's reverse-order column swaps L179-L198 as one gather/scatter).
-// I/O: for n = NP (powers of two) and 16-byte aligned buffers, each warp streams its 32
-// rows per task with TMA (cp.async.bulk.tensor, 128/64/32-byte swizzle so that every
-// lane's row read and the scatter are bank-conflict free) double-buffered against the
-// compute; the output is staged in the same buffer and written with a TMA store.
-// Other n use coalesced vector loads into a padded staging buffer.
+//   a3  logical swap: rows never move; each lane tracks the position its row would have
+//       in the listing's swapped array (swap k <-> q, L156-L162).  One lane records
+//       (p, q) per step in shared memory: ipiv, the swap parity, the singular flag and
+//       log|det| are all derived from that record after the loop.
+//   a4  pivot-row normalisation is DEFERRED: the pivot lane publishes its row
+//       un-normalised; every other row uses f_i = x_ik * (1/p), which is exactly the
+//       multiplier of Eq. (15) (-a_ik^{k-1} times a_kj^k = a_kj^{k-1}/p); each row is
+//       scaled by 1/p of its own pivot step once, at the store.
+//   a5  x_ij -= f_i x_rj (Eq. (15)) with FFMA2 (fma.rn.f32x2) for fp32; compact storage:
+//       column k becomes the new D column (-f_i, and 1 on the pivot row).
+//   The k loop is rolled, two steps per iteration, with the register file ROTATED: the
+//   pivot column of the first step of a pair is register 0, of the second register 1,
+//   and the second step writes its results two registers to the left (x'[j] = x[j+2] -
+//   f y[j+2]) appending the two new D columns at the end.  After NP steps register j
+//   holds compact column j.  (The loop body stays ~100 instructions per step pair: no
+//   I-cache pressure.)  n < NP runs padded with identity rows/columns: padded steps pick
+//   the padding rows and change nothing real.
+//   a6  log|det| = sum log|p_k| (fp64), sign = (-1)^swaps prod sign(p_k) (Eq. (13), G4).
+//   a7  un-permutation on store: Ainv[k][perm[k']] = (1/p_{perm[k]}) X[perm[k]][k'] (the
+//       listing's reverse-order column swaps, L179-L198, as one gather/scatter).
+// I/O: for n = NP and 16-byte aligned buffers each warp streams its 32 rows per task with
+// TMA (cp.async.bulk.tensor; 128/64/32-byte swizzle so every lane's row read and the
+// scatter are bank-conflict free), double-buffered against the compute; the output is
+// staged in the same buffer and written with a TMA store.  Other n use coalesced vector
+// loads into a padded staging buffer.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
 
 #include "gj_internal.h"
+#include "gj_ptx.cuh"
 
 namespace gj {
 namespace {
 
+using namespace ptx;
+
 constexpr int kWarpsPerBlock = 4;
 
-// ------------------------------------------------------------------ small PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// All lanes wait, then reconverge (the per-lane try_wait loop may exit at different
-// iterations; everything after it relies on a converged warp).
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-  __syncwarp();
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int r0, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(r0), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int c0, int r0, const void* src) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                   reinterpret_cast<uint64_t>(tm)),
-               "r"(c0), "r"(r0), "r"(smem_u32(src))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-
-// 1/p: MUFU approximation + one Newton step (branch-free, within 1 ulp; exact for powers
-// of two).  fp64 keeps the IEEE round-to-nearest reciprocal.
-__device__ __forceinline__ float rcp_rn(float p) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
-  const float e = fmaf(-p, r, 1.0f);
-  return fmaf(r, e, r);
-}
-__device__ __forceinline__ double rcp_rn(double p) { return __drcp_rn(p); }
-
-// Largest T <= t (t >= 0), so that |p| <= tau is decided exactly in T's precision.
-__device__ __forceinline__ float round_down_to(double t, float) { return __double2float_rd(t); }
-__device__ __forceinline__ double round_down_to(double t, double) { return t; }
-
-template <int NP>
-__device__ __forceinline__ double group_max(double v) {
-#pragma unroll
-  for (int o = NP / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-template <int NP>
-__device__ __forceinline__ double group_sum(double v) {
-#pragma unroll
-  for (int o = NP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// ------------------------------------------------------------------ a5: elimination
-// x[j] -= f * y[j] for j != K; fp32 pairs use FFMA2.
-__device__ __forceinline__ void ffma2(float& x0, float& x1, float nf, float y0, float y1) {
-  unsigned long long xv, yv, fv;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(xv) : "f"(x0), "f"(x1));
-  asm("mov.b64 %0, {%1,%2};" : "=l"(yv) : "f"(y0), "f"(y1));
-  asm("mov.b64 %0, {%1,%1};" : "=l"(fv) : "f"(nf));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(xv) : "l"(fv), "l"(yv));
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(x0), "=f"(x1) : "l"(xv));
-}
-
-template <int NP, int K>
-__device__ __forceinline__ void elim_pair(float (&x)[NP], const float (&y)[NP], float nf, int j) {
-  if (j != K && j + 1 != K) {
-    ffma2(x[j], x[j + 1], nf, y[j], y[j + 1]);
-  } else if (j == K) {
-    x[j + 1] = fmaf(nf, y[j + 1], x[j + 1]);
-  } else {
-    x[j] = fmaf(nf, y[j], x[j]);
-  }
-}
-// The pair holding column K+1 (the next step's pivot column) goes first so the next
-// pivot search can start while the rest of the update is still issuing.
-template <int NP, int K>
-__device__ __forceinline__ void eliminate(float (&x)[NP], const float (&y)[NP], float nf) {
-  constexpr int first = ((K + 1) % NP) & ~1;
-  elim_pair<NP, K>(x, y, nf, first);
-#pragma unroll
-  for (int j = 0; j + 1 < NP; j += 2)
-    if (j != first) elim_pair<NP, K>(x, y, nf, j);
-}
-template <int NP, int K>
-__device__ __forceinline__ void eliminate(double (&x)[NP], const double (&y)[NP], double nf) {
-  constexpr int first = (K + 1) % NP;
-  if (first != K) x[first] = fma(nf, y[first], x[first]);
-#pragma unroll
-  for (int j = 0; j < NP; ++j)
-    if (j != K && j != first) x[j] = fma(nf, y[j], x[j]);
-}
-
-// ------------------------------------------------------------------ configuration
-// R rows per lane (two rows share every pivot-row load and every publish/search
-// instruction), L = NP/R lanes per matrix, MPW matrices per warp, ROWS = 32*R rows
-// per warp task.
+// R rows per lane: two rows share every pivot-row load (halving the shared-memory
+// traffic of the broadcast, which bounds the fp32 n = 32 case); L = NP/R lanes per matrix.
 template <typename T, int NP>
 struct Cfg {
-  static constexpr int R = (NP >= 4 && NP * (int)sizeof(T) * 2 <= 256) ? 2 : 1;
-  static constexpr int L = NP / R;
-  static constexpr int MPW = 32 / L;
-  static constexpr int ROWS = MPW * NP;
+  static constexpr int R = (NP == 32 && sizeof(T) == 4) ? 2 : 1;
+  static constexpr int L = NP / R;      // lanes per matrix
+  static constexpr int MPW = 32 / L;    // matrices per warp
+  static constexpr int ROWS = MPW * NP; // rows per warp task
 };
 
-// ------------------------------------------------------------------ shared-memory layouts
-// TMA path: the warp's ROWS rows stored as REG regions of [ROWS rows][SPAN bytes], each
-// swizzled like CU_TENSOR_MAP_SWIZZLE_{SPAN}B (16-byte chunk index ^= address bits 7+).
-template <typename T, int NP>
-struct TmaLayout {
-  static constexpr int ROWS = Cfg<T, NP>::ROWS;
-  static constexpr int RB = NP * (int)sizeof(T);        // row bytes
-  static constexpr int SPAN = RB < 128 ? RB : 128;       // swizzle span
-  static constexpr int REG = RB / SPAN;                  // regions (TMA boxes) per row
-  static constexpr int BOX_COLS = SPAN / (int)sizeof(T);
-  static constexpr int BYTES = ROWS * RB;                // one stage buffer
-  static constexpr int SWZ_MASK = SPAN == 128 ? 7 : SPAN == 64 ? 3 : SPAN == 32 ? 1 : 0;
-  // used with RB >= 16 only (launch_np instantiates the TMA path for such rows)
-  // per-row part of the address: row*SPAN and the XOR applied to the in-span byte offset
-  __device__ static __forceinline__ uint32_t row_base(int row) { return (uint32_t)(row * SPAN); }
-  __device__ static __forceinline__ uint32_t row_xor(int row) {
-    return (((uint32_t)(row * SPAN) >> 7) & SWZ_MASK) << 4;
-  }
-  __device__ static __forceinline__ uint32_t off(uint32_t rb, uint32_t rx, int byte_in_row) {
-    return (uint32_t)((byte_in_row / SPAN) * ROWS * SPAN) + rb + (((uint32_t)(byte_in_row % SPAN)) ^ rx);
-  }
-};
-
-// Generic path: padded rows (pitch NP+1 elements), linear.
-template <typename T, int NP, bool TMA>
-struct Smem {
-  using C = Cfg<T, NP>;
-  static constexpr int PITCH = NP + 1;
-  static constexpr int STAGE_BYTES = TMA ? TmaLayout<T, NP>::BYTES : C::ROWS * PITCH * (int)sizeof(T);
-  static constexpr int NBUF = TMA ? 2 : 1;
-  static constexpr int STAGE_ALIGNED = (STAGE_BYTES + 1023) / 1024 * 1024;
-  static constexpr int PROW_BYTES = 2 * C::MPW * NP * (int)sizeof(T);
-  static constexpr int PERM_BYTES = C::MPW * NP * 4;
-  static constexpr int per_warp =
-      ((NBUF * STAGE_ALIGNED + PROW_BYTES + PERM_BYTES + 16 * NBUF) + 1023) / 1024 * 1024;
-};
-
-template <typename T, int NP, bool TMA>
-struct RowAddr {
-  uint32_t rb = 0, rx = 0;
-  __device__ __forceinline__ RowAddr() {}
-  __device__ __forceinline__ explicit RowAddr(int row) {
-    if constexpr (TMA) {
-      rb = TmaLayout<T, NP>::row_base(row);
-      rx = TmaLayout<T, NP>::row_xor(row);
-    } else {
-      rb = (uint32_t)(row * (NP + 1) * (int)sizeof(T));
-      rx = 0;
-    }
-  }
-  __device__ __forceinline__ uint32_t at(int col) const {
-    if constexpr (TMA) {
-      return TmaLayout<T, NP>::off(rb, rx, col * (int)sizeof(T));
-    } else {
-      return rb + (uint32_t)(col * (int)sizeof(T));
-    }
-  }
-};
-
-// Read a whole row (NP values) from the staging buffer.
-template <typename T, int NP, bool TMA>
-__device__ __forceinline__ void stage_ld_row(T (&x)[NP], const unsigned char* stage, int row) {
-  const RowAddr<T, NP, TMA> ra(row);
-  if constexpr (TMA) {
-    constexpr int V = 16 / sizeof(T);
-#pragma unroll
-    for (int j = 0; j < NP; j += V) {
-      const uint4 u = *reinterpret_cast<const uint4*>(stage + ra.at(j));
-      if constexpr (sizeof(T) == 4) {
-        x[j] = __uint_as_float(u.x); x[j + 1] = __uint_as_float(u.y);
-        x[j + 2] = __uint_as_float(u.z); x[j + 3] = __uint_as_float(u.w);
-      } else {
-        x[j] = __longlong_as_double((long long)(((unsigned long long)u.y << 32) | u.x));
-        x[j + 1] = __longlong_as_double((long long)(((unsigned long long)u.w << 32) | u.z));
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < NP; ++j) x[j] = *reinterpret_cast<const T*>(stage + ra.at(j));
-  }
-}
-
-template <typename T, int NP>
-__device__ __forceinline__ void st_row(T* dst, const T (&x)[NP]) {
-  if constexpr ((NP * sizeof(T)) % 16 == 0) {
-#pragma unroll
-    for (int j = 0; j < NP; j += 16 / (int)sizeof(T)) {
-      if constexpr (sizeof(T) == 4) {
-        *reinterpret_cast<float4*>(dst + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
-      } else {
-        *reinterpret_cast<double2*>(dst + j) = make_double2(x[j], x[j + 1]);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < NP; ++j) dst[j] = x[j];
-  }
-}
-template <typename T, int NP>
-__device__ __forceinline__ void ld_row(T (&y)[NP], const T* src) {
-  if constexpr ((NP * sizeof(T)) % 16 == 0) {
-#pragma unroll
-    for (int j = 0; j < NP; j += 16 / (int)sizeof(T)) {
-      if constexpr (sizeof(T) == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(src + j);
-        y[j] = v.x; y[j + 1] = v.y; y[j + 2] = v.z; y[j + 3] = v.w;
-      } else {
-        const double2 v = *reinterpret_cast<const double2*>(src + j);
-        y[j] = v.x; y[j + 1] = v.y;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < NP; ++j) y[j] = src[j];
-  }
-}
-
-struct TmaMaps {
-  CUtensorMap a, x;
-};
-
-// ------------------------------------------------------------------ a2: pivot search (R rows/lane)
-// Per-matrix (lane-group) reductions.  redux.sync is only fast with a warp-uniform
-// member mask, so with two matrices per warp each group runs a full-warp redux in which
-// the other group contributes the identity; with more groups a shuffle butterfly over
-// the group's L lanes is cheaper.
+// ------------------------------------------------------------------ group reductions
+// redux.sync is only fast with a warp-uniform member mask: one matrix per warp uses it
+// directly, two matrices run one full-warp redux per group (the other group contributes
+// the identity), more groups use a shuffle butterfly over the group's lanes.
 template <int MPW, int L>
 __device__ __forceinline__ uint32_t group_max_u32(uint32_t v, int g) {
   if constexpr (MPW == 1) {
@@ -317,39 +90,53 @@ __device__ __forceinline__ uint32_t group_min_u32(uint32_t v, int g) {
     return v;
   }
 }
+template <int L>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int L>
+__device__ __forceinline__ unsigned lane_group_mask(int lane) {
+  if constexpr (L == 32) {
+    return 0xffffffffu;
+  } else {
+    return ((1u << L) - 1u) << (lane & ~(L - 1));
+  }
+}
 
-// On return q = physical position of the pivot row (uniform over the group) and
-// is_piv[r] marks the slot holding it.
+// ------------------------------------------------------------------ a2: pivot search
+// Eligible rows carry kmask = all ones, pivoted rows kmask = 0.  On return q = the pivot
+// row's physical position (group-uniform) and is_piv[r] marks the slot holding it.
 template <int R, int MPW, int L>
-__device__ __forceinline__ void pivot_search(const float (&v)[R], const bool (&used)[R], const int (&pos)[R],
+__device__ __forceinline__ void pivot_search(const float (&v)[R], const uint32_t (&kmask)[R], const int (&pos)[R],
                                              int g, int& q, bool (&is_piv)[R]) {
   uint32_t key[R];
   uint32_t km = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    key[r] = used[r] ? 0u : (__float_as_uint(v[r]) & 0x7fffffffu);
+    key[r] = __float_as_uint(v[r]) & 0x7fffffffu & kmask[r];
     km = max(km, key[r]);
   }
   const uint32_t m = group_max_u32<MPW, L>(km, g);
   uint32_t pc = 0xffffu;
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (!used[r] && key[r] == m) pc = min(pc, (uint32_t)pos[r]);
+    if (key[r] == m && kmask[r] != 0u) pc = min(pc, (uint32_t)pos[r]);
   q = (int)group_min_u32<MPW, L>(pc, g);
 #pragma unroll
-  for (int r = 0; r < R; ++r) is_piv[r] = (pos[r] == q) && !used[r] && key[r] == m;
+  for (int r = 0; r < R; ++r) is_piv[r] = pos[r] == q;
 }
-
 template <int R, int MPW, int L>
-__device__ __forceinline__ void pivot_search(const double (&v)[R], const bool (&used)[R], const int (&pos)[R],
+__device__ __forceinline__ void pivot_search(const double (&v)[R], const uint32_t (&kmask)[R], const int (&pos)[R],
                                              int g, int& q, bool (&is_piv)[R]) {
   uint32_t hi[R], lo[R];
   uint32_t hm = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(v[r]) & 0x7fffffffffffffffull;
-    hi[r] = used[r] ? 0u : (uint32_t)(b >> 32);
-    lo[r] = used[r] ? 0u : (uint32_t)b;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[r]);
+    hi[r] = (uint32_t)(b >> 32) & 0x7fffffffu & kmask[r];
+    lo[r] = (uint32_t)b & kmask[r];
     hm = max(hm, hi[r]);
   }
   const uint32_t mh = group_max_u32<MPW, L>(hm, g);
@@ -361,40 +148,13 @@ __device__ __forceinline__ void pivot_search(const double (&v)[R], const bool (&
   uint32_t pc = 0xffffu;
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (!used[r] && hi[r] == mh && lo[r] == ml) pc = min(pc, (uint32_t)pos[r]);
+    if (hi[r] == mh && lo[r] == ml && kmask[r] != 0u) pc = min(pc, (uint32_t)pos[r]);
   q = (int)group_min_u32<MPW, L>(pc, g);
 #pragma unroll
-  for (int r = 0; r < R; ++r) is_piv[r] = (pos[r] == q) && !used[r] && hi[r] == mh && lo[r] == ml;
+  for (int r = 0; r < R; ++r) is_piv[r] = pos[r] == q;
 }
 
-// Predicated row store (no branch, so the unrolled steps stay one basic block).
-template <typename T, int NP>
-__device__ __forceinline__ void st_row_if(bool pred, T* dst, const T (&x)[NP]) {
-  if constexpr ((NP * sizeof(T)) % 16 == 0) {
-    const uint32_t a = smem_u32(dst);
-    const uint32_t p = pred ? 1u : 0u;
-#pragma unroll
-    for (int j = 0; j < NP; j += 16 / (int)sizeof(T)) {
-      if constexpr (sizeof(T) == 4) {
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.v4.f32 [%1], {%2, %3, %4, %5};\n}"
-                     ::"r"(p), "r"(a + 4u * j), "f"(x[j]), "f"(x[j + 1]), "f"(x[j + 2]), "f"(x[j + 3]) : "memory");
-      } else {
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.v2.f64 [%1], {%2, %3};\n}"
-                     ::"r"(p), "r"(a + 8u * j), "d"(x[j]), "d"(x[j + 1]) : "memory");
-      }
-    }
-  } else {
-    if (pred) st_row<T, NP>(dst, x);
-  }
-}
-
-// Rotated elimination update.  The k loop is rolled (two steps per iteration) and the
-// register file is kept ROTATED so that the pivot column of the first step of a pair is
-// always register 0 and of the second step register 1: the second step writes its
-// results two registers to the left (x'[j] = x[j+2] - f*y[j+2]) and appends the two new
-// D columns at the end.  After NP steps (NP even) the rotation is back to identity and
-// register j holds compact column j (the D column of step j).
-// fp32 pairs stay 8-byte aligned (rotation by 2), so FFMA2 is used throughout.
+// ------------------------------------------------------------------ a5: rotated update
 template <int NP>
 __device__ __forceinline__ void update_first(float (&x)[NP], const float (&y)[NP], float nf) {
   x[1] = fmaf(nf, y[1], x[1]);
@@ -428,13 +188,159 @@ __device__ __forceinline__ void update_second_rot(double (&x)[NP], const double 
   x[NP - 1] = dcol;
 }
 
-// One elimination step (a2-a5) at runtime step index k; the pivot column is register
-// PC (0 or 1); SECOND selects the rotating update.
+// ------------------------------------------------------------------ shared-memory layouts
+// TMA path: the warp's 32 rows stored as REG regions of [32 rows][SPAN bytes], each
+// swizzled like CU_TENSOR_MAP_SWIZZLE_{SPAN}B (16-byte chunk index ^= address bits 7+).
+template <typename T, int NP>
+struct TmaLayout {
+  static constexpr int ROWS = Cfg<T, NP>::ROWS;
+  static constexpr int RB = NP * (int)sizeof(T);   // row bytes (>= 16 on this path)
+  static constexpr int SPAN = RB < 128 ? RB : 128;  // swizzle span
+  static constexpr int REG = RB / SPAN;             // regions (TMA boxes) per row
+  static constexpr int BOX_COLS = SPAN / (int)sizeof(T);
+  static constexpr int BYTES = ROWS * RB;           // one stage buffer
+  static constexpr int SWZ_MASK = SPAN == 128 ? 7 : SPAN == 64 ? 3 : SPAN == 32 ? 1 : 0;
+};
+
+template <typename T, int NP, bool TMA>
+struct Smem {
+  static constexpr int ROWS = Cfg<T, NP>::ROWS;
+  static constexpr int STAGE_BYTES = TMA ? ROWS * NP * (int)sizeof(T) : ROWS * (NP + 1) * (int)sizeof(T);
+  static constexpr int NBUF = TMA ? 2 : 1;
+  static constexpr int STAGE_ALIGNED = (STAGE_BYTES + 1023) / 1024 * 1024;
+  static constexpr int PROW_BYTES = 2 * ROWS * (int)sizeof(T);   // two pivot-row buffers (all groups)
+  static constexpr int REC_BYTES = ROWS * 16;                     // per-step (p, q) record
+  static constexpr int PERM_BYTES = ROWS * 4;
+  static constexpr int per_warp =
+      ((NBUF * STAGE_ALIGNED + PROW_BYTES + REC_BYTES + PERM_BYTES + 16 * NBUF) + 1023) / 1024 * 1024;
+};
+
+// Address of (row, col) inside a staging buffer: per-row part (rb, rx) + column bytes.
+template <typename T, int NP, bool TMA>
+struct RowAddr {
+  uint32_t rb = 0, rx = 0;
+  __device__ __forceinline__ explicit RowAddr(int row) {
+    if constexpr (TMA) {
+      using TL = TmaLayout<T, NP>;
+      rb = (uint32_t)(row * TL::SPAN);
+      rx = ((rb >> 7) & TL::SWZ_MASK) << 4;
+    } else {
+      rb = (uint32_t)(row * (NP + 1) * (int)sizeof(T));
+    }
+  }
+  __device__ __forceinline__ uint32_t at_b(uint32_t cb) const {
+    if constexpr (TMA) {
+      using TL = TmaLayout<T, NP>;
+      if constexpr (TL::REG == 1) {
+        return rb + (cb ^ rx);
+      } else {
+        return (cb / TL::SPAN) * (TL::ROWS * TL::SPAN) + rb + ((cb % TL::SPAN) ^ rx);
+      }
+    } else {
+      return rb + cb;
+    }
+  }
+};
+
+template <typename T, int NP, bool TMA>
+__device__ __forceinline__ void stage_ld_row(T (&x)[NP], const unsigned char* stage, int row) {
+  const RowAddr<T, NP, TMA> ra(row);
+  if constexpr (TMA) {
+    constexpr int V = 16 / sizeof(T);
+#pragma unroll
+    for (int j = 0; j < NP; j += V) {
+      const uint4 u = *reinterpret_cast<const uint4*>(stage + ra.at_b(j * sizeof(T)));
+      if constexpr (sizeof(T) == 4) {
+        x[j] = __uint_as_float(u.x); x[j + 1] = __uint_as_float(u.y);
+        x[j + 2] = __uint_as_float(u.z); x[j + 3] = __uint_as_float(u.w);
+      } else {
+        x[j] = __longlong_as_double((long long)(((unsigned long long)u.y << 32) | u.x));
+        x[j + 1] = __longlong_as_double((long long)(((unsigned long long)u.w << 32) | u.z));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) x[j] = *reinterpret_cast<const T*>(stage + ra.at_b(j * sizeof(T)));
+  }
+}
+
+// Pivot-row publish (predicated, no branch) and broadcast read.
+template <typename T, int NP>
+__device__ __forceinline__ void st_row_if(bool pred, T* dst, const T (&x)[NP]) {
+  if constexpr ((NP * sizeof(T)) % 16 == 0) {
+    const uint32_t a = smem_u32(dst);
+#pragma unroll
+    for (int j = 0; j < NP; j += 16 / (int)sizeof(T)) {
+      if constexpr (sizeof(T) == 4) {
+        st_shared_v4_if(pred, a + 4u * j, x[j], x[j + 1], x[j + 2], x[j + 3]);
+      } else {
+        st_shared_v2_if(pred, a + 8u * j, x[j], x[j + 1]);
+      }
+    }
+  } else {
+    if (pred) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) dst[j] = x[j];
+    }
+  }
+}
+template <typename T, int NP>
+__device__ __forceinline__ void ld_row(T (&y)[NP], const T* src) {
+  if constexpr ((NP * sizeof(T)) % 16 == 0) {
+#pragma unroll
+    for (int j = 0; j < NP; j += 16 / (int)sizeof(T)) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(src + j);
+        y[j] = v.x; y[j + 1] = v.y; y[j + 2] = v.z; y[j + 3] = v.w;
+      } else {
+        const double2 v = *reinterpret_cast<const double2*>(src + j);
+        y[j] = v.x; y[j + 1] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) y[j] = src[j];
+  }
+}
+
+// Per-step record (p, q); one lane per group writes it.
+__device__ __forceinline__ void rec_store(unsigned char* rec, int idx, float p, int q) {
+  *reinterpret_cast<uint2*>(rec + 8 * idx) = make_uint2(__float_as_uint(p), (uint32_t)q);
+}
+__device__ __forceinline__ void rec_store(unsigned char* rec, int idx, double p, int q) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(p);
+  *reinterpret_cast<uint4*>(rec + 16 * idx) = make_uint4((uint32_t)b, (uint32_t)(b >> 32), (uint32_t)q, 0u);
+}
+__device__ __forceinline__ void rec_load(const unsigned char* rec, int idx, float& p, int& q) {
+  const uint2 u = *reinterpret_cast<const uint2*>(rec + 8 * idx);
+  p = __uint_as_float(u.x);
+  q = (int)u.y;
+}
+__device__ __forceinline__ void rec_load(const unsigned char* rec, int idx, double& p, int& q) {
+  const uint4 u = *reinterpret_cast<const uint4*>(rec + 16 * idx);
+  p = __longlong_as_double((long long)(((unsigned long long)u.y << 32) | u.x));
+  q = (int)u.z;
+}
+
+// log|p| in fp64.  For fp32 pivots the hardware log2 (rel. error ~2^-22 of log2|p|,
+// far below the fp32 pivots' own rounding) suffices; fp64 uses the full-precision log.
+__device__ __forceinline__ double log_abs(float p) {
+  // log2|p| = e + log2(m), m in [1, 2): exact (0) for powers of two
+  const uint32_t b = __float_as_uint(p) & 0x7fffffffu;
+  const int e = (int)(b >> 23) - 127;
+  const float m = __uint_as_float((b & 0x7fffffu) | 0x3f800000u);
+  return ((double)e + (double)__log2f(m)) * 0.6931471805599453;
+}
+__device__ __forceinline__ double log_abs(double p) { return log(fabs(p)); }
+
+struct TmaMaps {
+  CUtensorMap a, x;
+};
+
+// One elimination step (a2-a5) at runtime step index k; pivot column = register PC.
 template <typename T, int NP, int PC, bool SECOND>
-__device__ __forceinline__ void gj_step(int k, int n, T (&x)[Cfg<T, NP>::R][NP], T* prow_g,
-                                        bool (&used)[Cfg<T, NP>::R], int (&pos)[Cfg<T, NP>::R],
-                                        T (&myrp)[Cfg<T, NP>::R], int (&myipiv)[Cfg<T, NP>::R], int& info, T tau,
-                                        int li, int g) {
+__device__ __forceinline__ void gj_step(int k, T (&x)[Cfg<T, NP>::R][NP], T* prow_g, unsigned char* rec_g,
+                                        uint32_t (&kmask)[Cfg<T, NP>::R], int (&pos)[Cfg<T, NP>::R], int li, int g) {
   using C = Cfg<T, NP>;
   constexpr int R = C::R;
   T col[R];
@@ -442,14 +348,14 @@ __device__ __forceinline__ void gj_step(int k, int n, T (&x)[Cfg<T, NP>::R][NP],
   for (int r = 0; r < R; ++r) col[r] = x[r][PC];
   int q;
   bool is_piv[R];
-  pivot_search<R, C::MPW, C::L>(col, used, pos, g, q, is_piv);
-  // a3: listing's swap of rows k and q (L156-L162), tracked on positions only
+  pivot_search<R, C::MPW, C::L>(col, kmask, pos, g, q, is_piv);
+  // a3: the listing's swap of rows k and q (L156-L162), on positions only
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    if (li + r * C::L == k) myipiv[r] = q + 1;
     if (pos[r] == k) pos[r] = q;
+    if (is_piv[r]) pos[r] = k;
   }
-  // a4: publish the pivot row (one buffer per step of the pair: one __syncwarp per step)
+  // a4: publish the (un-normalised) pivot row; one buffer per step of the pair
   T* pr = prow_g + PC * C::MPW * NP;
 #pragma unroll
   for (int r = 0; r < R; ++r) st_row_if<T, NP>(is_piv[r], pr, x[r]);
@@ -457,16 +363,11 @@ __device__ __forceinline__ void gj_step(int k, int n, T (&x)[Cfg<T, NP>::R][NP],
   T y[NP];
   ld_row<T, NP>(y, pr);
   const T p = y[PC];
-  // Obs. 2: largest candidate at or below the zero threshold -> singular at step k+1
-  if (fabs(p) <= tau && info == 0 && k < n) info = k + 1;
-  const T rp = rcp_rn(p);
+  if (li == 0) rec_store(rec_g, k, p, q);
+  const T rp = rcp(p);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    if (is_piv[r]) {
-      pos[r] = k;
-      used[r] = true;
-      myrp[r] = rp;
-    }
+    kmask[r] = is_piv[r] ? 0u : kmask[r];
     // a5: Eq. (15) with the deferred pivot-row scale; column k becomes the D column
     const T nf = is_piv[r] ? T(0) : -(x[r][PC] * rp);
     const T dcol = is_piv[r] ? T(1) : nf;
@@ -479,22 +380,14 @@ __device__ __forceinline__ void gj_step(int k, int n, T (&x)[Cfg<T, NP>::R][NP],
   }
 }
 
-template <int L>
-__device__ __forceinline__ unsigned lane_group_mask(int lane) {
-  if constexpr (L == 32) {
-    return 0xffffffffu;
-  } else {
-    return ((1u << L) - 1u) << (lane & ~(L - 1));
-  }
-}
-
 template <typename T, int NP, bool TMA>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
   using C = Cfg<T, NP>;
   using S = Smem<T, NP, TMA>;
-  using TL = TmaLayout<T, (TMA ? NP : 4 * (int)(16 / sizeof(T)))>;   // only used when TMA
-  constexpr int R = C::R, L = C::L, MPW = C::MPW, ROWS = C::ROWS;
+  using TL = TmaLayout<T, (TMA ? NP : 16 / (int)sizeof(T))>;   // only used when TMA
+  constexpr int L = C::L, MPW = C::MPW, R = C::R, ROWS = C::ROWS;
+  constexpr int RECW = sizeof(T) == 4 ? 8 : 16;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -503,17 +396,20 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
   unsigned char* wbase = sbase + warp * S::per_warp;
   unsigned char* stage0 = wbase;
   T* prow = reinterpret_cast<T*>(wbase + S::NBUF * S::STAGE_ALIGNED);
-  int* permS = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(prow) + S::PROW_BYTES);
+  unsigned char* rec = reinterpret_cast<unsigned char*>(prow) + S::PROW_BYTES;
+  int* permS = reinterpret_cast<int*>(rec + S::REC_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(permS) + S::PERM_BYTES);
 
   const int n = TMA ? NP : a.n;
   const int nn = n * n;
   const int g = lane / L;        // matrix within the warp task
-  const int li = lane % L;       // slot r holds row li + r*L
+  const int li = lane % L;       // row within the matrix
   const unsigned gmask = lane_group_mask<L>(lane);
   const T* __restrict__ Ag = static_cast<const T*>(a.A);
   T* __restrict__ Xg = static_cast<T*>(a.Ainv);
-  T* prow_g = prow + g * NP;     // + (k&1)*MPW*NP selects the buffer
+  T* prow_g = prow + g * NP;
+  unsigned char* rec_g = rec + g * NP * RECW;   // one record of NP steps per matrix
+  int* perm_g = permS + g * NP;
 
   const int64_t ntasks = (a.batch + MPW - 1) / MPW;
   const int64_t wstride = (int64_t)gridDim.x * kWarpsPerBlock;
@@ -541,7 +437,7 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     const int valid_items = left < MPW ? (int)left : MPW;
     unsigned char* stage = stage0 + (TMA ? (it & 1) * S::STAGE_ALIGNED : 0);
 
-    // ---- a1: load ----
+    // ---- a1: load the task's rows into the staging buffer ----
     if constexpr (TMA) {
       const int64_t nxt = task + wstride;
       if (lane == 0 && nxt < ntasks) {
@@ -552,7 +448,7 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
         for (int rg = 0; rg < TL::REG; ++rg)
           tma_load_2d(ns + rg * ROWS * TL::SPAN, &tm.a, rg * TL::BOX_COLS, (int)(nxt * ROWS), &bars[(it + 1) & 1]);
       }
-      mbar_wait(&bars[it & 1], (it >> 1) & 1);
+      mbar_wait_warp(&bars[it & 1], (it >> 1) & 1);
     } else {
       const int tot = valid_items * nn;
       const int64_t gofs = item0 * nn;
@@ -570,7 +466,7 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
             const int m = e / nn;
             const int rem = e - m * nn;
             const int r = rem / n;
-            *reinterpret_cast<T*>(stage + RowAddr<T, NP, false>(m * NP + r).at(rem - r * n)) = v[u];
+            *reinterpret_cast<T*>(stage + RowAddr<T, NP, false>(m * NP + r).at_b((rem - r * n) * sizeof(T))) = v[u];
           }
         }
       }
@@ -586,84 +482,102 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
       stage_ld_row<T, NP, TMA>(x[r], stage, g * NP + row);
       if (!TMA || !item_ok) {
 #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          const bool rl = item_ok && real[r] && j < n;
-          if (!rl) x[r][j] = (row == j) ? T(1) : T(0);
-        }
+        for (int j = 0; j < NP; ++j)
+          if (!(item_ok && real[r] && j < n)) x[r][j] = (row == j) ? T(1) : T(0);
       }
     }
     __syncwarp();   // staging buffer fully read: free for the output scatter
 
-    // zero threshold tau = tol * max|a_ij| (Obs. 2, reading G1)
+    // zero threshold tau = tol * max|a_ij| (Obs. 2, reading G1); padding excluded
     T rowmax = T(0);
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int j = 0; j < NP; ++j)
         if (real[r] && j < n) rowmax = fmax(rowmax, fabs(x[r][j]));
-    const T tau = round_down_to(a.tol * group_max<L>((double)rowmax), T(0));
+    double smax;
+    if constexpr (sizeof(T) == 4) {
+      smax = (double)__uint_as_float(group_max_u32<MPW, L>(__float_as_uint(rowmax), g));
+    } else {
+      // exact max of non-negative doubles: high words, then low words among the winners
+      const unsigned long long b = (unsigned long long)__double_as_longlong(rowmax);
+      const uint32_t mh = group_max_u32<MPW, L>((uint32_t)(b >> 32), g);
+      const uint32_t ml = group_max_u32<MPW, L>((uint32_t)(b >> 32) == mh ? (uint32_t)b : 0u, g);
+      smax = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+    }
+    const T tau = round_down_to(a.tol * smax, T(0));
 
-    bool used[R];
-    int pos[R];      // physical position; after the loop = the step this row was pivot
-    T myrp[R];       // 1/p of that step (deferred normalisation scale)
-    int myipiv[R];
+    uint32_t kmask[R];
+    int pos[R];   // physical position; after the loop = the step this row was pivot
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      used[r] = false;      // padding rows only ever win the padded steps k >= n
+      kmask[r] = 0xffffffffu;
       pos[r] = li + r * L;
-      myrp[r] = T(1);
-      myipiv[r] = li + r * L + 1;
     }
-    int info = 0;
     // padded steps k >= n pick the (identity) padding rows and change nothing real
 #pragma unroll 1
     for (int k = 0; k < NP; k += 2) {
-      gj_step<T, NP, 0, false>(k, n, x, prow_g, used, pos, myrp, myipiv, info, tau, li, g);
-      gj_step<T, NP, 1, true>(k + 1, n, x, prow_g, used, pos, myrp, myipiv, info, tau, li, g);
+      gj_step<T, NP, 0, false>(k, x, prow_g, rec_g, kmask, pos, li, g);
+      gj_step<T, NP, 1, true>(k + 1, x, prow_g, rec_g, kmask, pos, li, g);
     }
+    __syncwarp();
 
-    // ---- a6: determinant (Eq. (13) with the swap sign, G4) ----
+    // ---- a6: det / ipiv / singular flag from the per-step record ----
+    T myrp[R];
+    unsigned failb = 0;
+    int nswap = 0, nneg = 0;
     double lgl = 0.0;
-    int nneg = 0, nswap = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if (real[r]) lgl -= log(fabs((double)myrp[r]));
-      nneg += __popc(__ballot_sync(0xffffffffu, real[r] && myrp[r] < T(0)) & gmask);
-      nswap += __popc(__ballot_sync(0xffffffffu, real[r] && myipiv[r] != li + r * L + 1) & gmask);
+      const int row = li + r * L;
+      T p_own, p_k;
+      int q_own, q_k;
+      rec_load(rec_g, pos[r], p_own, q_own);   // this row's own pivot step
+      rec_load(rec_g, row, p_k, q_k);          // step `row` of the record
+      (void)q_own;
+      myrp[r] = rcp(p_own);
+      const bool stepk = row < n;
+      // steps li + r*L: bit li of slot r's ballot; first failing step = lowest (r, li)
+      const unsigned fb = __ballot_sync(0xffffffffu, stepk && fabs(p_k) <= tau) & gmask;
+      if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * L + r * L);
+      nswap += __popc(__ballot_sync(0xffffffffu, stepk && q_k != row) & gmask);
+      nneg += __popc(__ballot_sync(0xffffffffu, stepk && p_k < T(0)) & gmask);
+      if (stepk) lgl += log_abs(p_k);
+      if (a.ipiv && item_ok && stepk) a.ipiv[(item0 + g) * n + row] = q_k + 1;
     }
+    const int info = (int)failb;   // first failing step, 1-based (0: regular)
     const double lg = group_sum<L>(lgl);
     const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
-    if (item_ok) {
+    if (item_ok && li == 0) {
       const int64_t item = item0 + g;
-      if (li == 0) {
-        if (a.info) a.info[item] = info;
-        if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
-        if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
-        if (a.det) static_cast<T*>(a.det)[item] = info ? T(0) : (T)(sgn * exp(lg));
-      }
-      if (a.ipiv) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (real[r]) a.ipiv[item * n + li + r * L] = myipiv[r];
-      }
+      if (a.info) a.info[item] = info;
+      if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
+      if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
+      if (a.det) static_cast<T*>(a.det)[item] = info ? T(0) : (T)(sgn * exp(lg));
     }
 
     // ---- a7 + a8: un-permuted store through the staging buffer ----
     if (Xg != nullptr) {
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (real[r]) permS[g * NP + pos[r]] = li + r * L;
+      for (int r = 0; r < R; ++r) perm_g[pos[r]] = (li + r * L) * (int)sizeof(T);   // output column (bytes)
       __syncwarp();
-      RowAddr<T, NP, TMA> dst[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) dst[r] = RowAddr<T, NP, TMA>(g * NP + pos[r]);
+      for (int r = 0; r < R; ++r) {
+        const RowAddr<T, NP, TMA> dst(g * NP + pos[r]);
+        if constexpr (NP >= 4) {
 #pragma unroll
-      for (int kp = 0; kp < NP; ++kp) {
-        if (kp < n) {
-          const int c = permS[g * NP + kp];
+          for (int kp = 0; kp < NP; kp += 4) {
+            const int4 cb = *reinterpret_cast<const int4*>(perm_g + kp);
+            const int cbs[4] = {cb.x, cb.y, cb.z, cb.w};
 #pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (real[r]) *reinterpret_cast<T*>(stage + dst[r].at(c)) = myrp[r] * x[r][kp];
+            for (int u = 0; u < 4; ++u)
+              if (real[r] && kp + u < n)
+                *reinterpret_cast<T*>(stage + dst.at_b((uint32_t)cbs[u])) = myrp[r] * x[r][kp + u];
+          }
+        } else {
+#pragma unroll
+          for (int kp = 0; kp < NP; ++kp)
+            if (real[r] && kp < n) *reinterpret_cast<T*>(stage + dst.at_b((uint32_t)perm_g[kp])) = myrp[r] * x[r][kp];
         }
       }
       if constexpr (TMA) {
@@ -683,7 +597,8 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
           const int m = e / nn;
           const int rem = e - m * nn;
           const int r = rem / n;
-          __stcs(Xg + gofs + e, *reinterpret_cast<const T*>(stage + RowAddr<T, NP, false>(m * NP + r).at(rem - r * n)));
+          __stcs(Xg + gofs + e,
+                 *reinterpret_cast<const T*>(stage + RowAddr<T, NP, false>(m * NP + r).at_b((rem - r * n) * sizeof(T))));
         }
       }
     }
@@ -695,42 +610,6 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
 }
 
 // ------------------------------------------------------------------ host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
-template <typename T, int NP>
-bool make_map(CUtensorMap* m, const void* base, int64_t batch) {
-  using TL = TmaLayout<T, NP>;
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)NP, (cuuint64_t)(batch * NP)};
-  cuuint64_t strides[1] = {(cuuint64_t)NP * sizeof(T)};
-  cuuint32_t box[2] = {(cuuint32_t)TL::BOX_COLS, (cuuint32_t)TL::ROWS};
-  cuuint32_t es[2] = {1u, 1u};
-  CUtensorMapSwizzle sw = TL::SPAN == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                          : TL::SPAN == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                          : TL::SPAN == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
-                                           : CU_TENSOR_MAP_SWIZZLE_NONE;
-  CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <typename T, int NP, bool TMA>
 cudaError_t launch_warp(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
   using S = Smem<T, NP, TMA>;
@@ -757,13 +636,18 @@ cudaError_t launch_warp(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t 
 template <typename T, int NP>
 cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
   TmaMaps maps;
-  const bool full = a.n == NP;
-  const bool aligned = (reinterpret_cast<uintptr_t>(a.A) % 16 == 0) &&
-                       (a.Ainv == nullptr || reinterpret_cast<uintptr_t>(a.Ainv) % 16 == 0);
-  const bool rows_ok = (NP * sizeof(T)) % 16 == 0 && a.batch * NP < (int64_t(1) << 31);
   if constexpr ((NP * sizeof(T)) % 16 == 0) {
-    if (full && aligned && rows_ok && make_map<T, NP>(&maps.a, a.A, a.batch) &&
-        (a.Ainv == nullptr || make_map<T, NP>(&maps.x, a.Ainv, a.batch))) {
+    using TL = TmaLayout<T, NP>;
+    const bool full = a.n == NP;
+    const bool aligned = (reinterpret_cast<uintptr_t>(a.A) % 16 == 0) &&
+                         (a.Ainv == nullptr || reinterpret_cast<uintptr_t>(a.Ainv) % 16 == 0);
+    const bool rows_ok = a.batch * NP < (int64_t(1) << 31);
+    const bool f64 = sizeof(T) == 8;
+    const uint64_t rows = (uint64_t)a.batch * NP;
+    const int swz = TL::SPAN >= 32 ? TL::SPAN : 0;
+    if (full && aligned && rows_ok &&
+        make_tma_map_2d(&maps.a, f64, a.A, NP, rows, NP * sizeof(T), TL::BOX_COLS, TL::ROWS, swz) &&
+        (a.Ainv == nullptr || make_tma_map_2d(&maps.x, f64, a.Ainv, NP, rows, NP * sizeof(T), TL::BOX_COLS, TL::ROWS, swz))) {
       if (a.Ainv == nullptr) maps.x = maps.a;
       return launch_warp<T, NP, true>(a, maps, s);
     }

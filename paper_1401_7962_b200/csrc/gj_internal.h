@@ -27,3 +27,13 @@ cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 int device_sm_count();
 
 }  // namespace gj
+
+#include <cuda.h>
+
+namespace gj {
+// Encode a 2-D tiled TMA descriptor (driver entry point fetched at run time, so the
+// library does not link libcuda).  swizzle_bytes in {0, 32, 64, 128}.  Returns false
+// if the driver entry point is unavailable or the encode fails.
+bool make_tma_map_2d(CUtensorMap* m, bool f64, const void* base, uint64_t cols, uint64_t rows,
+                     uint64_t row_stride_bytes, uint32_t box_cols, uint32_t box_rows, int swizzle_bytes);
+}  // namespace gj
