@@ -58,9 +58,10 @@ gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, vo
   if (n < 1 || batch < 0) return GJ_ERR_ARG;
   if (batch == 0) return GJ_OK;
   if (A == nullptr) return GJ_ERR_ARG;
-  if (n > 32) return GJ_ERR_UNSUPPORTED;
+  if (n > GJ_BATCHED_MAX_N) return GJ_ERR_UNSUPPORTED;
   BatchedArgs a{n, batch, A, Ainv, ipiv, logabsdet, sign, det, info, resolve_tol(dt, n, tol)};
-  cudaError_t e = launch_batched(dt, a, static_cast<cudaStream_t>(stream));
+  cudaError_t e = n <= 32 ? launch_batched(dt, a, static_cast<cudaStream_t>(stream))
+                          : launch_batched64(dt, a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 

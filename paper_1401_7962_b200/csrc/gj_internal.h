@@ -20,8 +20,10 @@ struct BatchedArgs {
   double tol;          // >= 0 (default already resolved)
 };
 
-// K1/K2 launchers (gj_batched.cu). Return cudaSuccess or the launch error.
+// K1 launcher, n <= 32 (gj_batched.cu); K2 launcher, 32 < n <= 64 (gj_batched64.cu).
+// Return cudaSuccess or the launch error.
 cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
+cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 
 // Number of SMs of the current device (cached per device).
 int device_sm_count();

@@ -58,7 +58,7 @@ def test_permutation_matrices_bit_exact(gj, torch, n, dtype):
     assert np.all(g["det"] == g["sign"])
 
 
-@pytest.mark.parametrize("n", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 32, 64])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_hadamard_bit_exact(gj, torch, n, dtype):
     """P6: every step an exact tie (tie-break G3 at every step), every value dyadic."""
@@ -116,8 +116,25 @@ def test_c2_prefix(gj, torch):
     assert np.all(res[reg] <= lim[reg])
 
 
+# ------------------------------------------------------------------ C3 (configs[2])
+def test_c3_prefix(gj, torch):
+    """C3 recipe (reading G15) at batch 8192 with 1% duplicated-row singular items, tol 1e-10:
+    flat fp64 tolerances (well-conditioned), exact singular-flag agreement (R7)."""
+    A, S = synth.gen_c3(batch=8192, return_singular=True)
+    g = run_gpu(gj, torch, A, tol=synth.C3_TOL)
+    ref = oracle.invert_batched(A, tol=synth.C3_TOL)
+    assert np.array_equal(np.nonzero(ref.info)[0], S)
+    assert np.array_equal(np.nonzero(g["info"])[0], S)
+    rep = compare(A, g, ref, np.float64, synth.C3_TOL, flat_only=True)
+    print(rep.summary())
+    assert_report(rep, flat_only=True)
+    reg = ref.info == 0
+    res = oracle.residual_batched(A[reg][:2000], g["inverse"][reg][:2000])
+    assert res.max() <= TOL_RES[np.float64]
+
+
 # ------------------------------------------------------------------ ragged shapes
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 9, 12, 13, 17, 24, 31, 32])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 9, 12, 13, 17, 24, 31, 32, 33, 40, 47, 63, 64])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_ragged_sizes(gj, torch, n, dtype):
     B = 517  # not a multiple of any group count: ragged tail
@@ -135,8 +152,9 @@ def test_empty_batch(gj, torch):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_in_place_equals_out_of_place(gj, torch, dtype):
-    A = synth.gen_normal_batch(300, 32, seed=5, dtype=dtype)
+@pytest.mark.parametrize("n", [32, 64])
+def test_in_place_equals_out_of_place(gj, torch, dtype, n):
+    A = synth.gen_normal_batch(300, n, seed=5, dtype=dtype)
     g1 = run_gpu(gj, torch, A)
     g2 = run_gpu(gj, torch, A, inplace=True)
     for k in ("inverse", "ipiv", "logabsdet", "sign", "info"):
