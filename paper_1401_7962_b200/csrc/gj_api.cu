@@ -68,15 +68,22 @@ gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, vo
 size_t gj_workspace_size(gj_dtype dt, int n, int64_t batch, int entry) {
   (void)batch;
   if (n < 1) return 0;
-  if (entry == 1 && n <= GJ_BATCHED_MAX_N) return (size_t)n * n * esize(dt);  // lda != n repack
+  if (n > GJ_BATCHED_MAX_N && (entry == 1 || entry == 2)) return dt == GJ_F64 ? large_workspace_size(n) : 0;
+  if (entry == 1) return (size_t)n * n * esize(dt);  // lda != n repack
   return 0;
 }
 
 gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logabsdet,
                  int8_t* sign, void* det, int32_t* ipiv, int32_t* info, double tol,
                  void* workspace, size_t workspace_bytes, void* stream) {
-  (void)workspace; (void)workspace_bytes;
-  if (n > GJ_BATCHED_MAX_N) return GJ_ERR_UNSUPPORTED;
+  if (n > GJ_BATCHED_MAX_N) {
+    if (dt != GJ_F64 || batch != 1 || A == nullptr) return batch == 0 ? GJ_OK : GJ_ERR_UNSUPPORTED;
+    if (workspace == nullptr || workspace_bytes < large_workspace_size(n)) return GJ_ERR_WORKSPACE;
+    cudaError_t e = invert_large_f64(n, static_cast<const double*>(A), n, nullptr, 0, ipiv, logabsdet, sign,
+                                     static_cast<double*>(det), info, resolve_tol(dt, n, tol), workspace,
+                                     static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+  }
   return gj_invert_batched(dt, n, batch, A, nullptr, ipiv, logabsdet, sign, det, info, tol, stream);
 }
 
@@ -85,9 +92,15 @@ gj_status gj_invert(gj_dtype dt, int n, const void* A, int64_t lda, void* Ainv, 
                     void* workspace, size_t workspace_bytes, void* stream) {
   if (dt != GJ_F32 && dt != GJ_F64) return GJ_ERR_ARG;
   if (n < 1 || A == nullptr || Ainv == nullptr || lda < n || ldainv < n) return GJ_ERR_ARG;
-  if (n > GJ_BATCHED_MAX_N) return GJ_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t es = esize(dt);
+  if (n > GJ_BATCHED_MAX_N) {
+    if (dt != GJ_F64) return GJ_ERR_UNSUPPORTED;   // large-n fp32 (TF32 tensor path) is NEXT f1
+    if (workspace == nullptr || workspace_bytes < large_workspace_size(n)) return GJ_ERR_WORKSPACE;
+    cudaError_t e = invert_large_f64(n, static_cast<const double*>(A), lda, static_cast<double*>(Ainv), ldainv, ipiv,
+                                     logabsdet, sign, nullptr, info, resolve_tol(dt, n, tol), workspace, s);
+    return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+  }
   if (lda == n && ldainv == n)
     return gj_invert_batched(dt, n, 1, A, Ainv, ipiv, logabsdet, sign, nullptr, info, tol, stream);
   // strided: repack into the workspace, invert in place, unpack

@@ -25,6 +25,12 @@ struct BatchedArgs {
 cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 
+// Large-n blocked path (gj_large.cu), fp64, one matrix; Ainv may be null (det only).
+size_t large_workspace_size(int n);
+cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, int64_t ldainv, int32_t* ipiv,
+                             double* logabsdet, int8_t* sign, double* det, int32_t* info, double tol, void* ws,
+                             cudaStream_t s);
+
 // Number of SMs of the current device (cached per device).
 int device_sm_count();
 

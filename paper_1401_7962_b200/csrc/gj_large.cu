@@ -1,0 +1,655 @@
+// Large-n blocked Gauss–Jordan (gj_invert for n > 64) on sm_100a — the aggregated form
+// of the per-step rank-1 updates of Eqs. (14)-(15):
+//
+//   for each panel P of b = 128 columns:
+//     for each leaf L of W columns inside P:
+//       K3  leaf factorisation: W pivot steps (a2-a5) over ALL n rows but only the W leaf
+//           columns, by one thread-block cluster (8 or 16 CTAs x 1024 threads; every
+//           thread holds its rows' W values in registers; per step a CTA argmax, a
+//           DSMEM exchange of the CTA winners and one cluster barrier);
+//       K4  update the panel columns right of L:  X[:,T] += (W_L - S_L) R_L
+//     K4  trailing update of all columns outside P:  X[:,~P] += (W_P - S_P) R_P
+//   K5  un-permutation: Ainv[k][j] = X[perm[k]][step(j)]       (listing L179-L198)
+//   K6  log|det|, sign, singular flag, ipiv from the per-step record (Eq. (13), Obs. 2)
+//
+// Here W_L is the leaf's compact D columns (normalised), R_L = X[pivot rows of L, T] taken
+// before the update, and S_L selects the pivot rows: for a pivot row the update REPLACES
+// the old values (X_s <- (W R)_s), for every other row it adds.  Derivation: the block's
+// row operation is E = I + (S - C) A11^-1 S^T and its compact D columns are
+// W = E S = S + (S - C) A11^-1, so E v = v + (W - S) v[S].
+//
+// K4 is an FP64 tensor-core GEMM: mma.sync.m16n8k16.f64 (SASS DMMA; tcgen05 has no f64
+// kind on sm_100a), 128x128 CTA tiles, 8 warps of 64x32, cp.async double-buffered
+// 16-deep K slabs.  Pivoting is logical (rows never move); ties go to the smallest
+// physical position of the listing's swapped array (reading G3), so ipiv equals
+// LAPACK getrf's.  n is padded to a multiple of 32 with an identity block.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "gj_internal.h"
+#include "gj_ptx.cuh"
+
+namespace gj {
+namespace large {
+
+using namespace ptx;
+
+// ============================================================================ small kernels
+__global__ void init_perm_kernel(int n, int* pos, int* pivstep) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    pos[i] = i;
+    pivstep[i] = -1;
+  }
+}
+
+// X (npad x npad, ld npad) = blockdiag(A, I)
+__global__ void copy_pad_kernel(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ X, int npad) {
+  const int64_t tot = (int64_t)npad * npad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / npad), j = (int)(e - (int64_t)i * npad);
+    X[e] = (i < n && j < n) ? A[(int64_t)i * lda + j] : (i == j ? 1.0 : 0.0);
+  }
+}
+
+// max |a_ij| as the bit pattern of a non-negative double (atomicMax on u64 is monotone)
+__global__ void absmax_kernel(const double* __restrict__ A, int64_t lda, int n, unsigned long long* out) {
+  double m = 0.0;
+  const int64_t tot = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+    m = fmax(m, fabs(A[(int64_t)i * lda + j]));
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong(m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+    b = ob > b ? ob : b;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, b);
+}
+
+// R[s][c] = X[rows[s]][c] for s < w, c in [c_lo, c_hi) (R has leading dimension npad;
+// c_lo, c_hi even)
+__global__ void gather_rows_kernel(const double* __restrict__ X, int npad, const int* __restrict__ rows, int w,
+                                   double* __restrict__ R, int c_lo, int c_hi) {
+  const int s = blockIdx.y;
+  if (s >= w) return;
+  const double2* src = reinterpret_cast<const double2*>(X + (int64_t)rows[s] * npad + c_lo);
+  double2* dst = reinterpret_cast<double2*>(R + (int64_t)s * npad + c_lo);
+  const int m = (c_hi - c_lo) / 2;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) dst[j] = src[j];
+}
+
+// Ainv[k][j] = X[perm[k]][pivstep[j]]  (k, j < n); perm[k] = row pivoted at step k
+__global__ void unpermute_kernel(const double* __restrict__ X, int npad, const int* __restrict__ rec_row,
+                                 const int* __restrict__ pivstep, int n, double* __restrict__ Y, int64_t ldy) {
+  const int k = blockIdx.y;
+  const double* src = X + (int64_t)rec_row[k] * npad;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    Y[(int64_t)k * ldy + j] = src[pivstep[j]];
+}
+
+// log|det|, sign, singular flag and ipiv from the per-step record (Eq. (13), Obs. 2, G4)
+__global__ void finalize_kernel(int n, const double* __restrict__ rec_p, const int* __restrict__ rec_q, double tol,
+                                const unsigned long long* smax_bits, int32_t* ipiv, double* logabsdet, int8_t* sign,
+                                double* det, int32_t* info) {
+  __shared__ double s_lg[32];
+  __shared__ int s_first[32], s_par[32];
+  const double tau = tol * __longlong_as_double((long long)*smax_bits);
+  double lg = 0.0;
+  int first = 0x7fffffff, par = 0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double p = rec_p[k];
+    const int q = rec_q[k];
+    if (ipiv) ipiv[k] = q + 1;
+    lg += log(fabs(p));
+    par ^= (q != k) ^ (p < 0.0);
+    if (fabs(p) <= tau && k < first) first = k;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lg += __shfl_xor_sync(0xffffffffu, lg, o);
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    par ^= __shfl_xor_sync(0xffffffffu, par, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s_lg[w] = lg; s_first[w] = first; s_par[w] = par; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double L = 0.0;
+    int F = 0x7fffffff, Pp = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { L += s_lg[i]; F = min(F, s_first[i]); Pp ^= s_par[i]; }
+    const int inf = F == 0x7fffffff ? 0 : F + 1;
+    if (info) *info = inf;
+    if (logabsdet) *logabsdet = inf ? -INFINITY : L;
+    if (sign) *sign = inf ? 0 : (Pp ? -1 : 1);
+    if (det) *det = inf ? 0.0 : (Pp ? -exp(L) : exp(L));
+  }
+}
+
+// ============================================================================ K3: leaf
+// Cluster helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_remote(uint32_t laddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(laddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_remote_v4(uint32_t raddr, uint4 v) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(raddr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+struct LeafArgs {
+  double* X;         // npad x npad, ld npad
+  int npad;          // padded order
+  int c0;            // first column (= first global step) of the leaf
+  int* pos;          // [npad] physical position of each row
+  int* pivstep;      // [npad] step at which the row was pivot, -1 if not yet
+  double* rec_p;     // [npad] pivot value per step
+  int* rec_q;        // [npad] pivot's physical position per step
+  int* rec_row;      // [npad] pivot row per step
+};
+
+constexpr int kLeafThreads = 512;
+
+// Candidate key: |p| as (hi, lo) words, position, row.
+struct Cand {
+  uint32_t hi, lo, pos, row;
+};
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {   // a strictly preferred to b
+  if (a.hi != b.hi) return a.hi > b.hi;
+  if (a.lo != b.lo) return a.lo > b.lo;
+  return a.pos < b.pos;
+}
+
+template <int W, int RPT>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
+  constexpr int EXW = W + 2;   // exchange entry: 2 doubles of key + W row values
+  extern __shared__ __align__(16) unsigned char smem[];
+  Cand* wslot = reinterpret_cast<Cand*>(smem);                              // [32]
+  Cand* ctawin = wslot + 32;                                                // [1]
+  double* rowbuf = reinterpret_cast<double*>(smem + 33 * sizeof(Cand) + 16 - (33 * sizeof(Cand)) % 16);  // [EXW]
+  double* exch = rowbuf + EXW;                                              // [2][CL][EXW]
+
+  const uint32_t rank = cluster_rank();
+  const uint32_t CL = cluster_size();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npad = a.npad, c0 = a.c0;
+
+  double x[RPT][W];
+  int pos[RPT], pst[RPT];
+  bool valid[RPT];
+  int rowid[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = (int)(rank * (kLeafThreads * RPT)) + i * kLeafThreads + tid;
+    rowid[i] = r;
+    valid[i] = r < npad;
+    if (valid[i]) {
+      const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)r * npad + c0);
+#pragma unroll
+      for (int j = 0; j < W; j += 2) {
+        const double2 v = src[j / 2];
+        x[i][j] = v.x;
+        x[i][j + 1] = v.y;
+      }
+      pos[i] = a.pos[r];
+      pst[i] = a.pivstep[r];
+    } else {
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[i][j] = 0.0;
+      pos[i] = 0x7fffffff;
+      pst[i] = 0;
+    }
+  }
+  double myrp[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) myrp[i] = 1.0;
+  cluster_sync_all();   // every CTA of the cluster is resident before any DSMEM store
+
+#pragma unroll
+  for (int kk = 0; kk < W; ++kk) {
+    const int kg = c0 + kk;
+    // ---- a2: candidates of this thread (rows not yet pivoted)
+    Cand best{0u, 0u, 0xffffffffu, 0u};
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if (valid[i] && pst[i] < 0) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(x[i][kk]) & 0x7fffffffffffffffull;
+        const Cand c{(uint32_t)(b >> 32), (uint32_t)b, (uint32_t)pos[i], (uint32_t)rowid[i]};
+        if (best.pos == 0xffffffffu || better(c, best)) best = c;
+      }
+    }
+    // warp winner
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, best.pos == 0xffffffffu ? 0u : best.hi);
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, (best.pos != 0xffffffffu && best.hi == mh) ? best.lo : 0u);
+    const uint32_t pw =
+        __reduce_min_sync(0xffffffffu, (best.pos != 0xffffffffu && best.hi == mh && best.lo == ml) ? best.pos : 0xffffffffu);
+    const uint32_t rw = __reduce_max_sync(0xffffffffu, (best.pos == pw && pw != 0xffffffffu) ? best.row : 0u);
+    if (lane == 0) wslot[warp] = Cand{mh, ml, pw, rw};
+    __syncthreads();
+    // CTA winner (warp 0)
+    if (warp == 0) {
+      const Cand c = lane < kLeafThreads / 32 ? wslot[lane] : Cand{0u, 0u, 0xffffffffu, 0u};
+      const bool has = c.pos != 0xffffffffu;
+      const uint32_t h = __reduce_max_sync(0xffffffffu, has ? c.hi : 0u);
+      const uint32_t l = __reduce_max_sync(0xffffffffu, (has && c.hi == h) ? c.lo : 0u);
+      const uint32_t p = __reduce_min_sync(0xffffffffu, (has && c.hi == h && c.lo == l) ? c.pos : 0xffffffffu);
+      const uint32_t rr = __reduce_max_sync(0xffffffffu, (has && c.pos == p) ? c.row : 0u);
+      if (lane == 0) *ctawin = Cand{h, l, p, rr};
+    }
+    __syncthreads();
+    const Cand cw = *ctawin;
+    // the owner of the CTA winner publishes its row locally
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if (valid[i] && pst[i] < 0 && (uint32_t)pos[i] == cw.pos) {
+        reinterpret_cast<uint4*>(rowbuf)[0] = make_uint4(cw.hi, cw.lo, cw.pos, cw.row);
+#pragma unroll
+        for (int j = 0; j < W; j += 2) reinterpret_cast<double2*>(rowbuf + 2)[j / 2] = make_double2(x[i][j], x[i][j + 1]);
+      }
+    }
+    if (cw.pos == 0xffffffffu && tid == 0)   // no candidate in this CTA
+      reinterpret_cast<uint4*>(rowbuf)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+    __syncthreads();
+    // ---- exchange: warp 0 copies the CTA winner to every CTA of the cluster
+    double* myex = exch + (size_t)((kk & 1) * CL + rank) * EXW;
+    if (warp == 0) {
+      const uint32_t base = smem_u32(myex);
+      constexpr int CHUNKS = EXW / 2;   // 16-byte chunks per entry
+      for (int t = lane; t < (int)CL * CHUNKS; t += 32) {
+        const uint32_t dst_rank = (uint32_t)(t / CHUNKS);
+        const int ch = t - (int)dst_rank * CHUNKS;
+        const uint4 v = reinterpret_cast<const uint4*>(rowbuf)[ch];
+        st_remote_v4(map_remote(base + 16u * ch, dst_rank), v);
+      }
+    }
+    cluster_sync_all();
+    // ---- cluster winner, pivot row
+    const double* ex0 = exch + (size_t)((kk & 1) * CL) * EXW;
+    int wr = -1;
+    Cand wc{0u, 0u, 0xffffffffu, 0u};
+    for (uint32_t r = 0; r < CL; ++r) {
+      const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)r * EXW);
+      const Cand c{k4.x, k4.y, k4.z, k4.w};
+      if (c.pos == 0xffffffffu) continue;
+      if (wr < 0 || better(c, wc)) { wc = c; wr = (int)r; }
+    }
+    const double* y = ex0 + (size_t)wr * EXW + 2;
+    const double p = y[kk];
+    const int q = (int)wc.pos;
+    if (rank == 0 && tid == 0) {
+      a.rec_p[kg] = p;
+      a.rec_q[kg] = q;
+      a.rec_row[kg] = (int)wc.row;
+    }
+    const double rp = __drcp_rn(p);
+    // ---- a3 + a5
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const bool is_piv = valid[i] && pst[i] < 0 && pos[i] == q;
+      if (pos[i] == kg) pos[i] = q;
+      if (is_piv) {
+        pos[i] = kg;
+        pst[i] = kg;
+        myrp[i] = rp;
+      }
+      const double nf = is_piv ? 0.0 : -(x[i][kk] * rp);
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (j != kk) x[i][j] = fma(nf, y[j], x[i][j]);
+      x[i][kk] = is_piv ? 1.0 : nf;
+    }
+  }
+  // deferred normalisation of this leaf's pivot rows; write back
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    if (!valid[i]) continue;
+    const int r = rowid[i];
+    const double s = (pst[i] >= c0 && pst[i] < c0 + W) ? myrp[i] : 1.0;
+    double2* dst = reinterpret_cast<double2*>(a.X + (int64_t)r * npad + c0);
+#pragma unroll
+    for (int j = 0; j < W; j += 2) dst[j / 2] = make_double2(x[i][j] * s, x[i][j + 1] * s);
+    a.pos[r] = pos[i];
+    a.pivstep[r] = pst[i];
+  }
+  cluster_sync_all();   // no CTA leaves while others may still read its exchange buffer
+}
+
+// ============================================================================ K4: GEMM update
+// C[i][c] = (replace(i) ? 0 : C[i][c]) + sum_s A[i][s] * B[s][c]
+//   A: M x K (ld lda)  = X[:, leaf/panel columns]
+//   B: K x N (ld ldb)  = gathered pivot rows R
+//   C: M x N (ld ldc)  = X[:, target columns], updated in place
+//   replace(i) = pivstep[i] in [rep_lo, rep_hi)
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int AST = BK + 4;    // A smem row stride (doubles): conflict-free fragment loads
+constexpr int BST = BN + 4;    // B smem row stride
+constexpr int kGemmThreads = 256;
+constexpr int GEMM_SMEM = 2 * (BM * AST + BK * BST) * (int)sizeof(double);
+
+struct GemmArgs {
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+  int M, N, K;
+  const int* pivstep;
+  int rep_lo, rep_hi;
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, bool pred) {
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+      "{%12,%13,%14,%15}, {%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]), "d"(b[1]),
+        "d"(b[2]), "d"(b[3]));
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_update_kernel(GemmArgs g) {
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                       // [2][BM][AST]
+  double* Bs = gsm + 2 * BM * AST;        // [2][BK][BST]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;       // 2 x 4 warps, warp tile 64 x 32
+  const int gq = lane >> 2, tq = lane & 3;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+
+  auto load_stage = [&](int st, int k0) {
+    // A: BM x BK doubles = 1024 16-byte chunks; B: BK x BN = 1024 chunks
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = tid + u * kGemmThreads;
+      const int r = c >> 3, kc = (c & 7) * 2;
+      const int gr = m0 + r;
+      const bool ok = gr < g.M && k0 + kc < g.K;
+      cp_async16(smem_u32(As + st * BM * AST + r * AST + kc), g.A + (ok ? (int64_t)gr * g.lda + k0 + kc : 0), ok);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = tid + u * kGemmThreads;
+      const int r = c >> 6, nc = (c & 63) * 2;
+      const int gc = n0 + nc;
+      const bool ok = gc < g.N && k0 + r < g.K;
+      cp_async16(smem_u32(Bs + st * BK * BST + r * BST + nc), g.B + (ok ? (int64_t)(k0 + r) * g.ldb + gc : 0), ok);
+    }
+  };
+
+  // accumulators initialised from C (0 for the rows the update replaces)
+  double acc[4][4][4];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = m0 + wm * 64 + mt * 16 + gq + 8 * h;
+      bool keep = r < g.M;
+      if (keep) {
+        const int ps = g.pivstep[r];
+        keep = !(ps >= g.rep_lo && ps < g.rep_hi);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = n0 + wn * 32 + nt * 8 + 2 * tq;
+        double2 v = make_double2(0.0, 0.0);
+        if (keep && c < g.N) v = *reinterpret_cast<const double2*>(g.C + (int64_t)r * g.ldc + c);
+        acc[mt][nt][2 * h] = v.x;
+        acc[mt][nt][2 * h + 1] = v.y;
+      }
+    }
+  }
+
+  const int nk = (g.K + BK - 1) / BK;   // K % 16 == 8 (8-wide leaves): zero-filled tail
+  load_stage(0, 0);
+  cp_async_commit();
+  for (int kb = 0; kb < nk; ++kb) {
+    if (kb + 1 < nk) load_stage((kb + 1) & 1, (kb + 1) * BK);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* as = As + (kb & 1) * BM * AST + (wm * 64) * AST;
+    const double* bs = Bs + (kb & 1) * BK * BST + wn * 32;
+    double bf[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) bf[nt][i] = bs[(tq + 4 * i) * BST + nt * 8 + gq];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      double af[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        af[2 * i] = as[(mt * 16 + gq) * AST + tq + 4 * i];
+        af[2 * i + 1] = as[(mt * 16 + gq + 8) * AST + tq + 4 * i];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma16816(acc[mt][nt], af, bf[nt]);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = m0 + wm * 64 + mt * 16 + gq + 8 * h;
+      if (r >= g.M) continue;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = n0 + wn * 32 + nt * 8 + 2 * tq;
+        if (c < g.N)
+          *reinterpret_cast<double2*>(g.C + (int64_t)r * g.ldc + c) = make_double2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]);
+      }
+    }
+}
+
+// ============================================================================ host driver
+struct Workspace {
+  double* X;        // npad^2
+  double* R;        // PANEL x npad
+  double* rec_p;    // npad
+  int* rec_q;       // npad
+  int* rec_row;     // npad
+  int* pos;         // npad
+  int* pivstep;     // npad
+  unsigned long long* smax;   // 1
+};
+
+constexpr int PANEL = 128;
+
+static int pad_to(int n, int m) { return (n + m - 1) / m * m; }
+
+size_t workspace_bytes(int n) {
+  const int npad = pad_to(n, 32);
+  size_t b = 0;
+  b += (size_t)npad * npad * 8;
+  b += (size_t)PANEL * npad * 8;
+  b += (size_t)npad * 8;
+  b += (size_t)npad * 4 * 4;
+  b += 256;
+  return b + 1024;
+}
+
+static Workspace carve(void* ws, int npad) {
+  Workspace w;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 255) / 256 * 256;
+    return r;
+  };
+  w.X = reinterpret_cast<double*>(take((size_t)npad * npad * 8));
+  w.R = reinterpret_cast<double*>(take((size_t)PANEL * npad * 8));
+  w.rec_p = reinterpret_cast<double*>(take((size_t)npad * 8));
+  w.rec_q = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.rec_row = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.pos = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.pivstep = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.smax = reinterpret_cast<unsigned long long*>(take(8));
+  return w;
+}
+
+template <int W, int RPT>
+static cudaError_t launch_leaf(const LeafArgs& la, int cl, cudaStream_t s) {
+  const size_t smem = 33 * sizeof(Cand) + 16 + (size_t)(W + 2) * 8 * (1 + 2 * cl) + 64;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(leaf_kernel<W, RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(leaf_kernel<W, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl, 1, 1);
+  cfg.blockDim = dim3(kLeafThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, leaf_kernel<W, RPT>, la);
+}
+
+static cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaSuccess;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
+  gemm_update_kernel<<<grid, kGemmThreads, GEMM_SMEM, s>>>(g);
+  return cudaGetLastError();
+}
+
+// Leaf configuration: cluster size and rows per thread, leaf width W.
+struct LeafCfg {
+  int cl, rpt, w;
+};
+static bool leaf_cfg(int npad, LeafCfg* c) {
+  // rows per cluster = cl * 512 * rpt; registers hold rpt * w doubles per thread
+  if (npad <= 16 * kLeafThreads) { *c = {16, 1, 32}; return true; }
+  if (npad <= 16 * kLeafThreads * 2) { *c = {16, 2, 16}; return true; }
+  if (npad <= 16 * kLeafThreads * 4) { *c = {16, 4, 8}; return true; }
+  return false;
+}
+
+static bool debug_sync() {
+  static int v = -1;
+  if (v < 0) v = getenv("GJ_DEBUG_SYNC") != nullptr ? 1 : 0;
+  return v == 1;
+}
+#define GJ_DBG(name)                                                                        \
+  do {                                                                                      \
+    if (debug_sync()) {                                                                     \
+      cudaError_t de = cudaStreamSynchronize(s);                                            \
+      if (de != cudaSuccess) {                                                              \
+        fprintf(stderr, "gjinv large: %s failed: %s\n", name, cudaGetErrorString(de));      \
+        return de;                                                                          \
+      }                                                                                     \
+    }                                                                                       \
+  } while (0)
+
+}  // namespace large
+
+size_t large_workspace_size(int n) { return large::workspace_bytes(n); }
+
+// Single fp64 matrix, n > 64.  All work on `s`; returns cudaSuccess or the error.
+cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, int64_t ldainv, int32_t* ipiv,
+                             double* logabsdet, int8_t* sign, double* det, int32_t* info, double tol, void* ws_ptr,
+                             cudaStream_t s) {
+  using namespace large;
+  const int npad = pad_to(n, 32);
+  LeafCfg lc;
+  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
+  Workspace w = carve(ws_ptr, npad);
+  cudaError_t e;
+  const int sms = device_sm_count();
+  init_perm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(npad, w.pos, w.pivstep);
+  copy_pad_kernel<<<sms * 8, 256, 0, s>>>(A, lda, n, w.X, npad);
+  cudaMemsetAsync(w.smax, 0, 8, s);
+  absmax_kernel<<<sms * 8, 256, 0, s>>>(A, lda, n, w.smax);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  GJ_DBG("setup");
+
+  for (int P0 = 0; P0 < npad; P0 += PANEL) {
+    const int pw = (npad - P0) < PANEL ? (npad - P0) : PANEL;
+    for (int L0 = P0; L0 < P0 + pw; L0 += lc.w) {
+      LeafArgs la{w.X, npad, L0, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row};
+      if (lc.w == 32)
+        e = launch_leaf<32, 1>(la, lc.cl, s);
+      else if (lc.w == 16)
+        e = launch_leaf<16, 2>(la, lc.cl, s);
+      else
+        e = launch_leaf<8, 4>(la, lc.cl, s);
+      if (e != cudaSuccess) return e;
+      GJ_DBG("leaf");
+      if (debug_sync()) {
+        int hr[64], hpos[64];
+        cudaMemcpy(hr, w.rec_row + L0, sizeof(int) * lc.w, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hpos, w.rec_q + L0, sizeof(int) * lc.w, cudaMemcpyDeviceToHost);
+        for (int t = 0; t < lc.w; ++t)
+          if (hr[t] < 0 || hr[t] >= npad || hpos[t] < L0 + t || hpos[t] >= npad)
+            fprintf(stderr, "gjinv large: leaf %d step %d bad record row=%d q=%d\n", L0, t, hr[t], hpos[t]);
+      }
+      // the leaf's transformation applied to the other columns of the panel (left: the
+      // D columns of earlier leaves, right: columns still to be factored)
+      if (pw > lc.w) {
+        gather_rows_kernel<<<dim3(1, lc.w), 128, 0, s>>>(w.X, npad, w.rec_row + L0, lc.w, w.R, P0, P0 + pw);
+        GJ_DBG("panel gather");
+        GemmArgs gl{w.X + L0, npad, w.R + P0, npad, w.X + P0, npad, npad, L0 - P0, lc.w, w.pivstep, L0, L0 + lc.w};
+        if ((e = launch_gemm(gl, s)) != cudaSuccess) return e;
+        GJ_DBG("panel gemm left");
+        const int T0 = L0 + lc.w, T1 = P0 + pw;
+        GemmArgs gr{w.X + L0, npad, w.R + T0, npad, w.X + T0, npad, npad, T1 - T0, lc.w, w.pivstep, L0, L0 + lc.w};
+        if ((e = launch_gemm(gr, s)) != cudaSuccess) return e;
+        GJ_DBG("panel gemm");
+      }
+    }
+    // trailing update of every column outside the panel
+    gather_rows_kernel<<<dim3((npad / 2 + 255) / 256, pw), 256, 0, s>>>(w.X, npad, w.rec_row + P0, pw, w.R, 0, npad);
+    GemmArgs gl{w.X + P0, npad, w.R, npad, w.X, npad, npad, P0, pw, w.pivstep, P0, P0 + pw};
+    if ((e = launch_gemm(gl, s)) != cudaSuccess) return e;
+    GemmArgs gr{w.X + P0, npad, w.R + P0 + pw, npad, w.X + P0 + pw, npad, npad, npad - P0 - pw, pw, w.pivstep, P0, P0 + pw};
+    if ((e = launch_gemm(gr, s)) != cudaSuccess) return e;
+    GJ_DBG("trailing gemm");
+  }
+  if (Ainv != nullptr)
+    unpermute_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
+  finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet, sign, det, info);
+  return cudaGetLastError();
+}
+
+}  // namespace gj
