@@ -29,6 +29,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gj_internal.h"
 #include "gj_ptx.cuh"
@@ -180,29 +181,98 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {   // a st
   return a.pos < b.pos;
 }
 
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_all(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// Index of the preferred candidate among the lanes with `ok` (all lanes get it): larger
+// |p| (high word, then low word), ties to the smallest position.  Fast path: a unique
+// high-word maximum decides without the other two reductions.
+__device__ __forceinline__ int warp_pick(const Cand& c, bool ok) {
+  const bool h = ok && c.pos != 0xffffffffu;
+  const uint32_t H = __reduce_max_sync(0xffffffffu, h ? c.hi : 0u);
+  const unsigned bh = __ballot_sync(0xffffffffu, h && c.hi == H);
+  if (__popc(bh) == 1) return __ffs(bh) - 1;
+  if (bh == 0) return 0;   // no candidate anywhere
+  const uint32_t Lo = __reduce_max_sync(0xffffffffu, (h && c.hi == H) ? c.lo : 0u);
+  const uint32_t P = __reduce_min_sync(0xffffffffu, (h && c.hi == H && c.lo == Lo) ? c.pos : 0xffffffffu);
+  const unsigned bp = __ballot_sync(0xffffffffu, h && c.pos == P);
+  return __ffs(bp) - 1;
+}
+// Bulk copy shared::cta -> shared::cluster, completing on the destination's mbarrier.
+__device__ __forceinline__ void bulk_s2c(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+// 1/p: MUFU approximation + two Newton steps (exact for powers of two).
+__device__ __forceinline__ double rcp_f64(double p) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+  double e = fma(-p, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-p, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Rotated leaf update (pivot column in register PC; the second step of a pair shifts the
+// registers two to the left and appends the two new D columns, as in K1).
+template <int W, int PC, bool SECOND>
+__device__ __forceinline__ void leaf_update(double (&x)[W], const double* y, double nf, double dcol) {
+  if constexpr (!SECOND) {
+#pragma unroll
+    for (int j = 1; j < W; ++j) x[j] = fma(nf, y[j], x[j]);
+    x[0] = dcol;
+  } else {
+    const double c0 = fma(nf, y[0], x[0]);
+#pragma unroll
+    for (int j = 0; j + 2 < W; ++j) x[j] = fma(nf, y[j + 2], x[j + 2]);
+    x[W - 2] = c0;
+    x[W - 1] = dcol;
+  }
+}
+
+// Shared-memory layout of the leaf kernel (bytes)
+template <int W>
+struct LeafSmem {
+  static constexpr int EXW = W + 2;                       // entry: key (2 doubles) + W row values
+  static constexpr int WSLOT = 0;                         // [kLeafThreads/32][EXW] doubles
+  static constexpr int EXCH = WSLOT + (kLeafThreads / 32) * EXW * 8;   // [2][CL][EXW]
+  static int bytes(int cl) { return EXCH + 2 * cl * EXW * 8 + 2 * 8 + 64; }
+};
+
 template <int W, int RPT>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
-  constexpr int EXW = W + 2;   // exchange entry: 2 doubles of key + W row values
+  using LS = LeafSmem<W>;
+  constexpr int EXW = LS::EXW;
+  constexpr int CHUNKS = EXW / 2;   // 16-byte chunks per entry
   extern __shared__ __align__(16) unsigned char smem[];
-  Cand* wslot = reinterpret_cast<Cand*>(smem);                              // [32]
-  Cand* ctawin = wslot + 32;                                                // [1]
-  double* rowbuf = reinterpret_cast<double*>(smem + 33 * sizeof(Cand) + 16 - (33 * sizeof(Cand)) % 16);  // [EXW]
-  double* exch = rowbuf + EXW;                                              // [2][CL][EXW]
+  double* wslot = reinterpret_cast<double*>(smem + LS::WSLOT);
+  double* exch = reinterpret_cast<double*>(smem + LS::EXCH);
 
   const uint32_t rank = cluster_rank();
   const uint32_t CL = cluster_size();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LS::EXCH + 2 * CL * EXW * 8);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npad = a.npad, c0 = a.c0;
+  const uint32_t entry_bytes = (uint32_t)(CL * EXW * 8);
 
   double x[RPT][W];
-  int pos[RPT], pst[RPT];
+  int pos[RPT], pst[RPT], rowid[RPT];
   bool valid[RPT];
-  int rowid[RPT];
+  double myrp[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int r = (int)(rank * (kLeafThreads * RPT)) + i * kLeafThreads + tid;
     rowid[i] = r;
     valid[i] = r < npad;
+    myrp[i] = 1.0;
     if (valid[i]) {
       const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)r * npad + c0);
 #pragma unroll
@@ -220,88 +290,93 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
       pst[i] = 0;
     }
   }
-  double myrp[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) myrp[i] = 1.0;
-  cluster_sync_all();   // every CTA of the cluster is resident before any DSMEM store
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bars[0], entry_bytes);   // steps 0, 2, 4, ...
+    mbar_expect_tx(&bars[1], entry_bytes);   // steps 1, 3, 5, ...
+  }
+  __syncthreads();
+  cluster_sync_all();   // every CTA resident and its barriers armed before any remote store
 
-#pragma unroll
-  for (int kk = 0; kk < W; ++kk) {
+  auto step = [&](int kk, auto pc_tag, auto second_tag) {
+    constexpr int PC = decltype(pc_tag)::value;
+    constexpr bool SECOND = decltype(second_tag)::value;
     const int kg = c0 + kk;
-    // ---- a2: candidates of this thread (rows not yet pivoted)
+    const int b = kk & 1;
+    // ---- a2: this thread's best candidate among its un-pivoted rows
     Cand best{0u, 0u, 0xffffffffu, 0u};
+    int bi = -1;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       if (valid[i] && pst[i] < 0) {
-        const unsigned long long b = (unsigned long long)__double_as_longlong(x[i][kk]) & 0x7fffffffffffffffull;
-        const Cand c{(uint32_t)(b >> 32), (uint32_t)b, (uint32_t)pos[i], (uint32_t)rowid[i]};
-        if (best.pos == 0xffffffffu || better(c, best)) best = c;
+        const unsigned long long u = (unsigned long long)__double_as_longlong(x[i][PC]) & 0x7fffffffffffffffull;
+        const Cand c{(uint32_t)(u >> 32), (uint32_t)u, (uint32_t)pos[i], (uint32_t)rowid[i]};
+        if (bi < 0 || better(c, best)) { best = c; bi = i; }
       }
     }
-    // warp winner
-    const uint32_t mh = __reduce_max_sync(0xffffffffu, best.pos == 0xffffffffu ? 0u : best.hi);
-    const uint32_t ml = __reduce_max_sync(0xffffffffu, (best.pos != 0xffffffffu && best.hi == mh) ? best.lo : 0u);
-    const uint32_t pw =
-        __reduce_min_sync(0xffffffffu, (best.pos != 0xffffffffu && best.hi == mh && best.lo == ml) ? best.pos : 0xffffffffu);
-    const uint32_t rw = __reduce_max_sync(0xffffffffu, (best.pos == pw && pw != 0xffffffffu) ? best.row : 0u);
-    if (lane == 0) wslot[warp] = Cand{mh, ml, pw, rw};
-    __syncthreads();
-    // CTA winner (warp 0)
-    if (warp == 0) {
-      const Cand c = lane < kLeafThreads / 32 ? wslot[lane] : Cand{0u, 0u, 0xffffffffu, 0u};
-      const bool has = c.pos != 0xffffffffu;
-      const uint32_t h = __reduce_max_sync(0xffffffffu, has ? c.hi : 0u);
-      const uint32_t l = __reduce_max_sync(0xffffffffu, (has && c.hi == h) ? c.lo : 0u);
-      const uint32_t p = __reduce_min_sync(0xffffffffu, (has && c.hi == h && c.lo == l) ? c.pos : 0xffffffffu);
-      const uint32_t rr = __reduce_max_sync(0xffffffffu, (has && c.pos == p) ? c.row : 0u);
-      if (lane == 0) *ctawin = Cand{h, l, p, rr};
-    }
-    __syncthreads();
-    const Cand cw = *ctawin;
-    // the owner of the CTA winner publishes its row locally
+    const bool has = bi >= 0;
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, has ? best.hi : 0u);
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, (has && best.hi == mh) ? best.lo : 0u);
+    const uint32_t pw = __reduce_min_sync(0xffffffffu, (has && best.hi == mh && best.lo == ml) ? best.pos : 0xffffffffu);
+    // the warp winner writes key + row into its slot (then fences them into the async
+    // proxy: warp 0 ships the CTA winner's slot with cp.async.bulk)
+    const bool wwin = has && best.pos == pw;
+    double* slot = wslot + warp * EXW;
+    if (pw == 0xffffffffu) {
+      if (lane == 0) reinterpret_cast<uint4*>(slot)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+    } else {
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      if (valid[i] && pst[i] < 0 && (uint32_t)pos[i] == cw.pos) {
-        reinterpret_cast<uint4*>(rowbuf)[0] = make_uint4(cw.hi, cw.lo, cw.pos, cw.row);
+      for (int i = 0; i < RPT; ++i) {
+        if (wwin && bi == i) {
+          reinterpret_cast<uint4*>(slot)[0] = make_uint4(best.hi, best.lo, best.pos, best.row);
 #pragma unroll
-        for (int j = 0; j < W; j += 2) reinterpret_cast<double2*>(rowbuf + 2)[j / 2] = make_double2(x[i][j], x[i][j + 1]);
+          for (int j = 0; j < W; j += 2) reinterpret_cast<double2*>(slot + 2)[j / 2] = make_double2(x[i][j], x[i][j + 1]);
+        }
       }
     }
-    if (cw.pos == 0xffffffffu && tid == 0)   // no candidate in this CTA
-      reinterpret_cast<uint4*>(rowbuf)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+    fence_async_smem();
     __syncthreads();
-    // ---- exchange: warp 0 copies the CTA winner to every CTA of the cluster
-    double* myex = exch + (size_t)((kk & 1) * CL + rank) * EXW;
+    // ---- warp 0: CTA winner; one bulk DSMEM copy per destination CTA (lane r -> CTA r),
+    // completing on the destination's mbarrier
     if (warp == 0) {
-      const uint32_t base = smem_u32(myex);
-      constexpr int CHUNKS = EXW / 2;   // 16-byte chunks per entry
-      for (int t = lane; t < (int)CL * CHUNKS; t += 32) {
-        const uint32_t dst_rank = (uint32_t)(t / CHUNKS);
-        const int ch = t - (int)dst_rank * CHUNKS;
-        const uint4 v = reinterpret_cast<const uint4*>(rowbuf)[ch];
-        st_remote_v4(map_remote(base + 16u * ch, dst_rank), v);
+      const int nw = kLeafThreads / 32;
+      Cand c{0u, 0u, 0xffffffffu, 0u};
+      if (lane < nw) {
+        const uint4 k4 = reinterpret_cast<const uint4*>(wslot + lane * EXW)[0];
+        c = Cand{k4.x, k4.y, k4.z, k4.w};
+      }
+      const int src_warp = warp_pick(c, lane < nw);
+      const uint32_t src = smem_u32(wslot + src_warp * EXW);
+      if (lane < (int)CL) {
+        const uint32_t ldst = smem_u32(exch + (size_t)(b * CL + rank) * EXW);
+        bulk_s2c(map_remote(ldst, (uint32_t)lane), src, (uint32_t)(EXW * 8), map_remote(smem_u32(&bars[b]), (uint32_t)lane));
       }
     }
-    cluster_sync_all();
-    // ---- cluster winner, pivot row
-    const double* ex0 = exch + (size_t)((kk & 1) * CL) * EXW;
-    int wr = -1;
-    Cand wc{0u, 0u, 0xffffffffu, 0u};
-    for (uint32_t r = 0; r < CL; ++r) {
-      const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)r * EXW);
-      const Cand c{k4.x, k4.y, k4.z, k4.w};
-      if (c.pos == 0xffffffffu) continue;
-      if (wr < 0 || better(c, wc)) { wc = c; wr = (int)r; }
+    // ---- all: wait for the CL entries of this step, pick the cluster winner
+    mbar_wait_all(&bars[b], (uint32_t)((kk >> 1) & 1));
+    if (tid == 0) mbar_expect_tx(&bars[b], entry_bytes);   // arm the barrier for step kk + 2
+    const double* ex0 = exch + (size_t)(b * CL) * EXW;
+    Cand cc{0u, 0u, 0xffffffffu, 0u};
+    if (lane < (int)CL) {
+      const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)lane * EXW);
+      cc = Cand{k4.x, k4.y, k4.z, k4.w};
     }
+    const int wr = warp_pick(cc, lane < (int)CL);
+    const Cand wc = [&] {
+      const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)wr * EXW);
+      return Cand{k4.x, k4.y, k4.z, k4.w};
+    }();
     const double* y = ex0 + (size_t)wr * EXW + 2;
-    const double p = y[kk];
+    const double p = y[PC];
     const int q = (int)wc.pos;
     if (rank == 0 && tid == 0) {
       a.rec_p[kg] = p;
       a.rec_q[kg] = q;
       a.rec_row[kg] = (int)wc.row;
     }
-    const double rp = __drcp_rn(p);
+    const double rp = rcp_f64(p);
     // ---- a3 + a5
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -312,26 +387,29 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         pst[i] = kg;
         myrp[i] = rp;
       }
-      const double nf = is_piv ? 0.0 : -(x[i][kk] * rp);
-#pragma unroll
-      for (int j = 0; j < W; ++j)
-        if (j != kk) x[i][j] = fma(nf, y[j], x[i][j]);
-      x[i][kk] = is_piv ? 1.0 : nf;
+      const double nf = is_piv ? 0.0 : -(x[i][PC] * rp);
+      const double dcol = is_piv ? 1.0 : nf;
+      leaf_update<W, PC, SECOND>(x[i], y, nf, dcol);
     }
+  };
+#pragma unroll 1
+  for (int kk = 0; kk < W; kk += 2) {
+    step(kk, std::integral_constant<int, 0>{}, std::integral_constant<bool, false>{});
+    step(kk + 1, std::integral_constant<int, 1>{}, std::integral_constant<bool, true>{});
   }
   // deferred normalisation of this leaf's pivot rows; write back
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     if (!valid[i]) continue;
     const int r = rowid[i];
-    const double s = (pst[i] >= c0 && pst[i] < c0 + W) ? myrp[i] : 1.0;
+    const double sc = (pst[i] >= c0 && pst[i] < c0 + W) ? myrp[i] : 1.0;
     double2* dst = reinterpret_cast<double2*>(a.X + (int64_t)r * npad + c0);
 #pragma unroll
-    for (int j = 0; j < W; j += 2) dst[j / 2] = make_double2(x[i][j] * s, x[i][j + 1] * s);
+    for (int j = 0; j < W; j += 2) dst[j / 2] = make_double2(x[i][j] * sc, x[i][j + 1] * sc);
     a.pos[r] = pos[i];
     a.pivstep[r] = pst[i];
   }
-  cluster_sync_all();   // no CTA leaves while others may still read its exchange buffer
+  cluster_sync_all();   // no CTA leaves while a peer's st.async may still target it
 }
 
 // ============================================================================ K4: GEMM update
@@ -519,7 +597,7 @@ static Workspace carve(void* ws, int npad) {
 
 template <int W, int RPT>
 static cudaError_t launch_leaf(const LeafArgs& la, int cl, cudaStream_t s) {
-  const size_t smem = 33 * sizeof(Cand) + 16 + (size_t)(W + 2) * 8 * (1 + 2 * cl) + 64;
+  const size_t smem = (size_t)LeafSmem<W>::bytes(cl);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(leaf_kernel<W, RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
