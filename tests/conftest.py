@@ -9,6 +9,9 @@ if ROOT not in sys.path:
 
 
 def pytest_configure(config):
+    # build libgjinv.so (nvcc cross-compiles without a GPU) before any test imports it
+    import __graft_entry__
+    __graft_entry__._builder().build()
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
