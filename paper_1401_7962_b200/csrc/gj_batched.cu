@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "gj_internal.h"
 #include "gj_ptx.cuh"
@@ -508,6 +509,369 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
   }
 }
 
+// ------------------------------------------------------------------ K1b: blocked, fp32 n = 32
+// The same elimination taken in blocks of BS steps (the aggregation of Eqs. (14)-(15) the
+// large-n path uses, applied inside one register-resident matrix).  Within a block, step
+// s only updates the BS panel columns (all the next pivot search needs); the pivot row's
+// panel values travel by one shuffle each.  At the end of the block the BS pivot rows'
+// other 32-BS values — untouched since the block began — are published to shared memory
+// ONCE and every row applies the block's BS rank-1 updates to its other columns at once:
+//     x_i[J'] += sum_s (W_is - S_is) R_s[J']
+// (W = the panel's compact columns after the block, R_s = the block-start row pivoted at
+// step s, S_is = 1 iff row i is that row; DESIGN.md §7 derives it).  The panel registers
+// hold W - S directly: a pivot row's own compact entry starts at 1 - 1 = 0, later updates
+// are additive, and the 1 is added back at the store.  Why: the per-step publish of a
+// whole pivot row (8 predicated STS.128 per slot, 4 smem cycles each whatever the lane
+// count; tools/ubench/smem_bench.cu) bounded the unblocked K1; here it happens once per
+// block.  Tie-break, logical swaps, record and epilogue are K1's.
+constexpr int kBlkStage = 64 * 128;   // one TMA stage: 2 matrices x 32 rows x 128 B
+
+template <int BS>
+struct BlkMisc {
+  static constexpr int RW = 32 - BS;
+  static constexpr int RBUF = 2 * BS * RW * 4;   // [matrix][block step][RW] pivot-row tails
+  static constexpr int REC = 2 * 32 * 8;         // [matrix][step] (p, q)
+  static constexpr int PERM = 2 * 32 * 4;
+  static constexpr int BYTES = RBUF + REC + PERM + 16;
+  static constexpr int smem(int nst) { return kWarpsPerBlock * (nst * kBlkStage + BYTES) + 1024; }
+};
+
+// One panel step s (static) at global step k on the panel registers P (branch-free, so
+// that a whole block stays one basic block and the scheduler can interleave the previous
+// block's trailing update into the latency of this chain).
+template <int BS>
+__device__ __forceinline__ void blk_panel_step(const int s, const int k, float (&P)[2][BS], uint32_t (&kmask)[2],
+                                               int (&pos)[2], int (&bs)[2], unsigned char* rec_g, int li, int g,
+                                               int lane) {
+  // a2: max |x_ik| over the un-pivoted rows (IEEE bit pattern of |x|, monotone)
+  const uint32_t key0 = __float_as_uint(P[0][s]) & kmask[0];
+  const uint32_t key1 = __float_as_uint(P[1][s]) & kmask[1];
+  const uint32_t m = group_max_u32<2, 16>(max(key0, key1), g);
+  // |1/p| and the unsigned multipliers start while the tie-break runs (|p| = m exactly)
+  const float ra = rcp(__uint_as_float(m));
+  const float t0 = P[0][s] * ra, t1 = P[1][s] * ra;
+  // ties -> smallest physical position (G3); the winner code carries (position, lane, slot)
+  const uint32_t c0 = (key0 == m && kmask[0] != 0u) ? ((uint32_t)pos[0] << 6 | (uint32_t)lane << 1) : 0xffffu;
+  const uint32_t c1 = (key1 == m && kmask[1] != 0u) ? ((uint32_t)pos[1] << 6 | (uint32_t)lane << 1 | 1u) : 0xffffu;
+  const uint32_t win = group_min_u32<2, 16>(min(c0, c1), g);
+  const int q = (int)(win >> 6);
+  const int src = (int)((win >> 1) & 31u);
+  const bool slot1 = (win & 1u) != 0u;
+  const bool pv0 = pos[0] == q, pv1 = pos[1] == q;
+  // the pivot row's panel values (one shuffle each from the pivot lane)
+  float z[BS];
+#pragma unroll
+  for (int j = 0; j < BS; ++j) z[j] = __shfl_sync(0xffffffffu, slot1 ? P[1][j] : P[0][j], src);
+  const float p = z[s];
+  const uint32_t psign = __float_as_uint(p) & 0x80000000u;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const bool pv = r ? pv1 : pv0;
+    // a5 on the panel: Eq. (15) with the deferred pivot-row scale, multiplier x_ik / p
+    const float nf = pv ? 0.0f : __uint_as_float((__float_as_uint(r ? t1 : t0) ^ psign) ^ 0x80000000u);
+#pragma unroll
+    for (int j = 0; j < BS; j += 2) {
+      if (j == s) {
+        P[r][j + 1] = fmaf(nf, z[j + 1], P[r][j + 1]);
+      } else if (j + 1 == s) {
+        P[r][j] = fmaf(nf, z[j], P[r][j]);
+      } else {
+        ffma2(P[r][j], P[r][j + 1], nf, z[j], z[j + 1]);
+      }
+    }
+    P[r][s] = nf;   // compact D entry; 0 on the pivot row (W - S: its 1 is held as 0)
+    kmask[r] = pv ? 0u : kmask[r];
+    bs[r] = pv ? s : bs[r];
+    // a3: the listing's swap of positions k and q (L156-L162), positions only
+    pos[r] = (pos[r] == k) ? q : pos[r];
+    pos[r] = pv ? k : pos[r];
+  }
+  if (li == 0) rec_store(rec_g, k, p, q);
+}
+
+// Publish the block's pivot rows: their other RW values T (unchanged since the block began).
+template <int BS>
+__device__ __forceinline__ void blk_publish(const float (&T)[2][32 - BS], const int (&bs)[2], float* rbuf_g) {
+  constexpr int RW = 32 - BS;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const uint32_t dst = smem_u32(rbuf_g) + (uint32_t)(bs[r] < 0 ? 0 : bs[r]) * (RW * 4);
+#pragma unroll
+    for (int j = 0; j < RW; j += 4)
+      st_shared_v4_if(bs[r] >= 0, dst + 4u * j, T[r][j], T[r][j + 1], T[r][j + 2], T[r][j + 3]);
+  }
+}
+
+// Rank-1 term s of the trailing update on columns [J0, J1) of T: T += (W - S)[:, s] R_s.
+template <int BS, int J0, int J1, int N>
+__device__ __forceinline__ void blk_trail_term(float (&T)[2][N], const float (&P)[2][BS], int s, const float* rbuf_g,
+                                               int tofs) {
+  constexpr int RW = 32 - BS;
+  float Rs[J1 - J0];
+  ld_row<float, J1 - J0>(Rs, rbuf_g + s * RW + J0);
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int j = 0; j < J1 - J0; j += 2) ffma2(T[r][tofs + j], T[r][tofs + j + 1], P[r][s], Rs[j], Rs[j + 1]);
+}
+
+// NST = TMA stages per warp: 2 = the next task streams in during this one; 1 = half the
+// shared memory (more resident warps), the next task is prefetched into L2 instead.
+template <int BS, int NST>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, NST == 1 ? 4 : 3)
+gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
+  using M = BlkMisc<BS>;
+  constexpr int RW = M::RW;
+  using TL = TmaLayout<float, 32>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  unsigned char* sbase = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stage0 = sbase + warp * NST * kBlkStage;
+  unsigned char* misc = sbase + kWarpsPerBlock * NST * kBlkStage + warp * M::BYTES;
+  float* rbuf = reinterpret_cast<float*>(misc);
+  unsigned char* rec = misc + M::RBUF;
+  int* permS = reinterpret_cast<int*>(rec + M::REC);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(misc + M::RBUF + M::REC + M::PERM);
+
+  const int g = lane >> 4;
+  const int li = lane & 15;
+  const unsigned gmask = 0xffffu << (16 * g);
+  float* rbuf_g = rbuf + g * BS * RW;
+  unsigned char* rec_g = rec + g * 32 * 8;
+  int* perm_g = permS + g * 32;
+
+  const int64_t ntasks = (a.batch + 1) / 2;
+  const int64_t wstride = (int64_t)gridDim.x * kWarpsPerBlock;
+  const int64_t task0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0 && task0 < ntasks) {
+    mbar_expect_tx(&bars[0], TL::BYTES);
+    tma_load_2d(stage0, &tm.a, 0, (int)(task0 * 64), &bars[0]);
+  }
+
+  int it = 0;
+  for (int64_t task = task0; task < ntasks; task += wstride, ++it) {
+    const int64_t item0 = task * 2;
+    const bool item_ok = item0 + g < a.batch;
+    unsigned char* stage = stage0 + (NST == 2 ? (it & 1) * kBlkStage : 0);
+    const int64_t nxt = task + wstride;
+    if constexpr (NST == 2) {
+      if (lane == 0 && nxt < ntasks) {
+        unsigned char* ns = stage0 + ((it + 1) & 1) * kBlkStage;
+        bulk_wait_read0();
+        mbar_expect_tx(&bars[(it + 1) & 1], TL::BYTES);
+        tma_load_2d(ns, &tm.a, 0, (int)(nxt * 64), &bars[(it + 1) & 1]);
+      }
+      mbar_wait_warp(&bars[it & 1], (it >> 1) & 1);
+    } else {
+      if (lane == 0 && nxt < ntasks)
+        bulk_prefetch_l2(static_cast<const float*>(a.A) + nxt * 64 * 32, TL::BYTES);
+      mbar_wait_warp(&bars[0], it & 1);
+    }
+    // ---- a1: rows li and li + 16 of matrix g into registers ----
+    float x[2][32];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = li + 16 * r;
+      stage_ld_row<float, 32, true>(x[r], stage, g * 32 + row);
+      if (!item_ok) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[r][j] = (row == j) ? 1.0f : 0.0f;
+      }
+    }
+    __syncwarp();
+    float rowmax = 0.0f;
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) rowmax = fmaxf(rowmax, fabsf(x[r][j]));
+    const double smax = (double)__uint_as_float(group_max_u32<2, 16>(__float_as_uint(rowmax), g));
+    const float tau = round_down_to(a.tol * smax, 0.0f);
+
+    uint32_t kmask[2] = {0x7fffffffu, 0x7fffffffu};
+    int pos[2] = {li, li + 16};
+    // P: panel columns of the current block; T: the other 32 - BS columns, rotated so
+    // that T[0..BS) is the next panel and the finished compact D columns sit at the end
+    float P[2][BS], T[2][RW];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int j = 0; j < BS; ++j) P[r][j] = x[r][j];
+#pragma unroll
+      for (int j = 0; j < RW; ++j) T[r][j] = x[r][BS + j];
+    }
+    int bs[2] = {-1, -1};
+#pragma unroll
+    for (int s = 0; s < BS; ++s) blk_panel_step<BS>(s, s, P, kmask, pos, bs, rec_g, li, g, lane);
+    // look-ahead: per iteration, publish block kb's pivot rows, apply its update to the
+    // next panel first, then factor that panel while the rest of block kb's update runs
+#pragma unroll 1
+    for (int kb = 0; kb + BS < 32; kb += BS) {
+      blk_publish<BS>(T, bs, rbuf_g);
+      __syncwarp();
+      float NP[2][BS];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < BS; ++j) NP[r][j] = T[r][j];
+#pragma unroll
+      for (int s = 0; s < BS; ++s) blk_trail_term<BS, 0, BS, BS>(NP, P, s, rbuf_g, 0);
+      bs[0] = -1;
+      bs[1] = -1;
+#pragma unroll
+      for (int s = 0; s < BS; ++s) {
+        blk_panel_step<BS>(s, kb + BS + s, NP, kmask, pos, bs, rec_g, li, g, lane);
+        blk_trail_term<BS, BS, RW, RW>(T, P, s, rbuf_g, BS);
+      }
+      __syncwarp();   // every lane has read rbuf before the next publish
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+#pragma unroll
+        for (int j = 0; j < RW - BS; ++j) T[r][j] = T[r][j + BS];
+#pragma unroll
+        for (int j = 0; j < BS; ++j) {
+          T[r][RW - BS + j] = P[r][j];
+          P[r][j] = NP[r][j];
+        }
+      }
+    }
+    // last block: its whole update, then x = [T | P] (register j = compact column j)
+    blk_publish<BS>(T, bs, rbuf_g);
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < BS; ++s) blk_trail_term<BS, 0, RW, RW>(T, P, s, rbuf_g, 0);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int j = 0; j < RW; ++j) x[r][j] = T[r][j];
+#pragma unroll
+      for (int j = 0; j < BS; ++j) x[r][RW + j] = P[r][j];
+    }
+
+    // ---- a6: det / ipiv / singular flag from the per-step record ----
+    float myrp[2];
+    unsigned failb = 0;
+    int nswap = 0, nneg = 0;
+    double lgl = 0.0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = li + 16 * r;
+      float p_own, p_k;
+      int q_own, q_k;
+      rec_load(rec_g, pos[r], p_own, q_own);
+      rec_load(rec_g, row, p_k, q_k);
+      (void)q_own;
+      myrp[r] = rcp(p_own);
+      const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau) & gmask;
+      if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * 16 + r * 16);
+      nswap += __popc(__ballot_sync(0xffffffffu, q_k != row) & gmask);
+      nneg += __popc(__ballot_sync(0xffffffffu, p_k < 0.0f) & gmask);
+      lgl += log_abs(p_k);
+      if (a.ipiv && item_ok) a.ipiv[(item0 + g) * 32 + row] = q_k + 1;
+    }
+    const int info = (int)failb;
+    const double lg = group_sum<16>(lgl);
+    const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
+    if (item_ok && li == 0) {
+      const int64_t item = item0 + g;
+      if (a.info) a.info[item] = info;
+      if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
+      if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
+      if (a.det) static_cast<float*>(a.det)[item] = info ? 0.0f : (float)(sgn * exp(lg));
+    }
+
+    // ---- a7 + a8: un-permuted store through the staging buffer ----
+    if (a.Ainv != nullptr) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) perm_g[pos[r]] = (li + 16 * r) * 4;   // output column (bytes)
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const RowAddr<float, 32, true> dst(g * 32 + pos[r]);
+#pragma unroll
+        for (int kp = 0; kp < 32; kp += 4) {
+          const int4 cb = *reinterpret_cast<const int4*>(perm_g + kp);
+          const int cbs[4] = {cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) *reinterpret_cast<float*>(stage + dst.at_b((uint32_t)cbs[u])) = myrp[r] * x[r][kp + u];
+        }
+        // the row's own compact entry was held as W - 1 (see above): add the 1 back
+        float* own = reinterpret_cast<float*>(stage + dst.at_b((uint32_t)((li + 16 * r) * 4)));
+        *own = *own + myrp[r];
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&tm.x, 0, (int)(task * 64), stage);
+        bulk_commit();
+      }
+    }
+    __syncwarp();
+    if constexpr (NST == 1) {
+      if (lane == 0 && nxt < ntasks) {
+        bulk_wait_read0();   // the store has read the stage
+        mbar_expect_tx(&bars[0], TL::BYTES);
+        tma_load_2d(stage0, &tm.a, 0, (int)(nxt * 64), &bars[0]);
+      }
+    }
+  }
+  if (lane == 0) bulk_wait0();
+}
+
+template <int BS, int NST>
+cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
+  const size_t smem = BlkMisc<BS>::smem(NST);
+  auto kern = gj_blk32_kernel<BS, NST>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntasks = (a.batch + 1) / 2;
+  const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int64_t cap = (int64_t)device_sm_count() * per_sm;
+  const int grid = (int)(need < cap ? need : cap);
+  kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(a, maps);
+  return cudaGetLastError();
+}
+
+// Variant of the fp32 n = 32 path: 0 = unblocked K1, 4 / 8 = K1b block size.  Fixed at
+// the best measured value; GJ_K1_BLOCK overrides it for A/B measurement only.
+int k1_block_size() {
+  static int v = -1;
+  if (v < 0) {
+    v = 4;
+    if (const char* e = getenv("GJ_K1_BLOCK")) {
+      const int t = atoi(e);
+      if (t == 0 || t == 4 || t == 8) v = t;
+    }
+  }
+  return v;
+}
+int k1_stages() {
+  static int v = -1;
+  if (v < 0) {
+    v = 2;
+    if (const char* e = getenv("GJ_K1_STAGES")) {
+      const int t = atoi(e);
+      if (t == 1 || t == 2) v = t;
+    }
+  }
+  return v;
+}
+
 // ------------------------------------------------------------------ host side
 template <typename T, int NP, bool TMA>
 cudaError_t launch_warp(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
@@ -548,6 +912,12 @@ cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
         make_tma_map_2d(&maps.a, f64, a.A, NP, rows, NP * sizeof(T), TL::BOX_COLS, TL::ROWS, swz) &&
         (a.Ainv == nullptr || make_tma_map_2d(&maps.x, f64, a.Ainv, NP, rows, NP * sizeof(T), TL::BOX_COLS, TL::ROWS, swz))) {
       if (a.Ainv == nullptr) maps.x = maps.a;
+      if constexpr (NP == 32 && sizeof(T) == 4) {
+        const int bsz = k1_block_size();
+        const bool one = k1_stages() == 1;
+        if (bsz == 8) return one ? launch_blk32<8, 1>(a, maps, s) : launch_blk32<8, 2>(a, maps, s);
+        if (bsz == 4) return one ? launch_blk32<4, 1>(a, maps, s) : launch_blk32<4, 2>(a, maps, s);
+      }
       return launch_warp<T, NP, true>(a, maps, s);
     }
   }
