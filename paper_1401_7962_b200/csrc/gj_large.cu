@@ -161,7 +161,8 @@ __device__ __forceinline__ void st_remote_v4(uint32_t raddr, uint4 v) {
 struct LeafArgs {
   double* X;         // npad x npad, ld npad
   int npad;          // padded order
-  int c0;            // first column (= first global step) of the leaf
+  int c0;            // first column (= first global step) of the panel
+  int pw;            // panel width (a multiple of the leaf width W)
   int* pos;          // [npad] physical position of each row
   int* pivstep;      // [npad] step at which the row was pivot, -1 if not yet
   double* rec_p;     // [npad] pivot value per step
@@ -242,17 +243,27 @@ __device__ __forceinline__ void leaf_update(double (&x)[W], const double* y, dou
 template <int W>
 struct LeafSmem {
   static constexpr int EXW = W + 2;                       // entry: key (2 doubles) + W row values
-  static constexpr int WSLOT = 0;                         // [kLeafThreads/32][EXW] doubles
+  static constexpr int RS = 0;                            // [W][PANEL_MAX] pivot rows of a leaf
+  static constexpr int PROW = RS + W * 128 * 8;           // [W] pivot row ids of the current leaf
+  static constexpr int WSLOT = PROW + W * 4;              // [kLeafThreads/32][EXW] doubles
   static constexpr int EXCH = WSLOT + (kLeafThreads / 32) * EXW * 8;   // [2][CL][EXW]
   static int bytes(int cl) { return EXCH + 2 * cl * EXW * 8 + 2 * 8 + 64; }
 };
 
+// K3 as one launch per PANEL: the panel's leaves one after another, each followed by its
+// update of the panel's other columns for this CTA's rows (X[i, T] += (W_i - S_i) R_L[T]
+// with the leaf's pivot rows R_L staged in shared memory).  The kernel releases its
+// programmatic dependents at once, so the trailing GEMM of the previous panel (launched
+// right after it with programmatic stream serialisation) runs on the other SMs while
+// this panel is factored (look-ahead).
 template <int W, int RPT>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   using LS = LeafSmem<W>;
   constexpr int EXW = LS::EXW;
-  constexpr int CHUNKS = EXW / 2;   // 16-byte chunks per entry
   extern __shared__ __align__(16) unsigned char smem[];
+  double* Rs = reinterpret_cast<double*>(smem + LS::RS);
+  int* prow = reinterpret_cast<int*>(smem + LS::PROW);
   double* wslot = reinterpret_cast<double*>(smem + LS::WSLOT);
   double* exch = reinterpret_cast<double*>(smem + LS::EXCH);
 
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   const uint32_t CL = cluster_size();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LS::EXCH + 2 * CL * EXW * 8);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int npad = a.npad, c0 = a.c0;
+  const int npad = a.npad, P0 = a.c0, pw = a.pw;
   const uint32_t entry_bytes = (uint32_t)(CL * EXW * 8);
 
   double x[RPT][W];
@@ -272,23 +283,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     const int r = (int)(rank * (kLeafThreads * RPT)) + i * kLeafThreads + tid;
     rowid[i] = r;
     valid[i] = r < npad;
-    myrp[i] = 1.0;
-    if (valid[i]) {
-      const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)r * npad + c0);
-#pragma unroll
-      for (int j = 0; j < W; j += 2) {
-        const double2 v = src[j / 2];
-        x[i][j] = v.x;
-        x[i][j + 1] = v.y;
-      }
-      pos[i] = a.pos[r];
-      pst[i] = a.pivstep[r];
-    } else {
-#pragma unroll
-      for (int j = 0; j < W; ++j) x[i][j] = 0.0;
-      pos[i] = 0x7fffffff;
-      pst[i] = 0;
-    }
+    pos[i] = valid[i] ? a.pos[r] : 0x7fffffff;
+    pst[i] = valid[i] ? a.pivstep[r] : 0;
   }
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -300,116 +296,185 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   __syncthreads();
   cluster_sync_all();   // every CTA resident and its barriers armed before any remote store
 
-  auto step = [&](int kk, auto pc_tag, auto second_tag) {
-    constexpr int PC = decltype(pc_tag)::value;
-    constexpr bool SECOND = decltype(second_tag)::value;
-    const int kg = c0 + kk;
-    const int b = kk & 1;
-    // ---- a2: this thread's best candidate among its un-pivoted rows
-    Cand best{0u, 0u, 0xffffffffu, 0u};
-    int bi = -1;
+  for (int c0 = P0, leaf = 0; c0 < P0 + pw; c0 += W, ++leaf) {
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      if (valid[i] && pst[i] < 0) {
-        const unsigned long long u = (unsigned long long)__double_as_longlong(x[i][PC]) & 0x7fffffffffffffffull;
-        const Cand c{(uint32_t)(u >> 32), (uint32_t)u, (uint32_t)pos[i], (uint32_t)rowid[i]};
-        if (bi < 0 || better(c, best)) { best = c; bi = i; }
+      myrp[i] = 1.0;
+      if (valid[i]) {
+        const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)rowid[i] * npad + c0);
+#pragma unroll
+        for (int j = 0; j < W; j += 2) {
+          const double2 v = src[j / 2];
+          x[i][j] = v.x;
+          x[i][j + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[i][j] = 0.0;
       }
     }
-    const bool has = bi >= 0;
-    const uint32_t mh = __reduce_max_sync(0xffffffffu, has ? best.hi : 0u);
-    const uint32_t ml = __reduce_max_sync(0xffffffffu, (has && best.hi == mh) ? best.lo : 0u);
-    const uint32_t pw = __reduce_min_sync(0xffffffffu, (has && best.hi == mh && best.lo == ml) ? best.pos : 0xffffffffu);
-    // the warp winner writes key + row into its slot (then fences them into the async
-    // proxy: warp 0 ships the CTA winner's slot with cp.async.bulk)
-    const bool wwin = has && best.pos == pw;
-    double* slot = wslot + warp * EXW;
-    if (pw == 0xffffffffu) {
-      if (lane == 0) reinterpret_cast<uint4*>(slot)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
-    } else {
+    auto step = [&](int kk, auto pc_tag, auto second_tag) {
+      constexpr int PC = decltype(pc_tag)::value;
+      constexpr bool SECOND = decltype(second_tag)::value;
+      const int kg = c0 + kk;
+      const int gk = leaf * W + kk;   // step count within this launch: mbarrier phase
+      const int b = gk & 1;
+      // ---- a2: this thread's best candidate among its un-pivoted rows
+      Cand best{0u, 0u, 0xffffffffu, 0u};
+      int bi = -1;
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
-        if (wwin && bi == i) {
-          reinterpret_cast<uint4*>(slot)[0] = make_uint4(best.hi, best.lo, best.pos, best.row);
-#pragma unroll
-          for (int j = 0; j < W; j += 2) reinterpret_cast<double2*>(slot + 2)[j / 2] = make_double2(x[i][j], x[i][j + 1]);
+        if (valid[i] && pst[i] < 0) {
+          const unsigned long long u = (unsigned long long)__double_as_longlong(x[i][PC]) & 0x7fffffffffffffffull;
+          const Cand c{(uint32_t)(u >> 32), (uint32_t)u, (uint32_t)pos[i], (uint32_t)rowid[i]};
+          if (bi < 0 || better(c, best)) { best = c; bi = i; }
         }
       }
-    }
-    fence_async_smem();
-    __syncthreads();
-    // ---- warp 0: CTA winner; one bulk DSMEM copy per destination CTA (lane r -> CTA r),
-    // completing on the destination's mbarrier
-    if (warp == 0) {
-      const int nw = kLeafThreads / 32;
-      Cand c{0u, 0u, 0xffffffffu, 0u};
-      if (lane < nw) {
-        const uint4 k4 = reinterpret_cast<const uint4*>(wslot + lane * EXW)[0];
-        c = Cand{k4.x, k4.y, k4.z, k4.w};
+      const bool has = bi >= 0;
+      const uint32_t mh = __reduce_max_sync(0xffffffffu, has ? best.hi : 0u);
+      const uint32_t ml = __reduce_max_sync(0xffffffffu, (has && best.hi == mh) ? best.lo : 0u);
+      const uint32_t pw_ = __reduce_min_sync(0xffffffffu, (has && best.hi == mh && best.lo == ml) ? best.pos : 0xffffffffu);
+      // the warp winner writes key + row into its slot (then fences them into the async
+      // proxy: warp 0 ships the CTA winner's slot with cp.async.bulk)
+      const bool wwin = has && best.pos == pw_;
+      double* slot = wslot + warp * EXW;
+      if (pw_ == 0xffffffffu) {
+        if (lane == 0) reinterpret_cast<uint4*>(slot)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+      } else {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          if (wwin && bi == i) {
+            reinterpret_cast<uint4*>(slot)[0] = make_uint4(best.hi, best.lo, best.pos, best.row);
+#pragma unroll
+            for (int j = 0; j < W; j += 2) reinterpret_cast<double2*>(slot + 2)[j / 2] = make_double2(x[i][j], x[i][j + 1]);
+          }
+        }
       }
-      const int src_warp = warp_pick(c, lane < nw);
-      const uint32_t src = smem_u32(wslot + src_warp * EXW);
+      fence_async_smem();
+      __syncthreads();
+      // ---- warp 0: CTA winner; one bulk DSMEM copy per destination CTA (lane r -> CTA r),
+      // completing on the destination's mbarrier
+      if (warp == 0) {
+        const int nw = kLeafThreads / 32;
+        Cand c{0u, 0u, 0xffffffffu, 0u};
+        if (lane < nw) {
+          const uint4 k4 = reinterpret_cast<const uint4*>(wslot + lane * EXW)[0];
+          c = Cand{k4.x, k4.y, k4.z, k4.w};
+        }
+        const int src_warp = warp_pick(c, lane < nw);
+        const uint32_t src = smem_u32(wslot + src_warp * EXW);
+        if (lane < (int)CL) {
+          const uint32_t ldst = smem_u32(exch + (size_t)(b * CL + rank) * EXW);
+          bulk_s2c(map_remote(ldst, (uint32_t)lane), src, (uint32_t)(EXW * 8), map_remote(smem_u32(&bars[b]), (uint32_t)lane));
+        }
+      }
+      // ---- all: wait for the CL entries of this step, pick the cluster winner
+      mbar_wait_all(&bars[b], (uint32_t)((gk >> 1) & 1));
+      if (tid == 0) mbar_expect_tx(&bars[b], entry_bytes);   // arm the barrier for step gk + 2
+      const double* ex0 = exch + (size_t)(b * CL) * EXW;
+      Cand cc{0u, 0u, 0xffffffffu, 0u};
       if (lane < (int)CL) {
-        const uint32_t ldst = smem_u32(exch + (size_t)(b * CL + rank) * EXW);
-        bulk_s2c(map_remote(ldst, (uint32_t)lane), src, (uint32_t)(EXW * 8), map_remote(smem_u32(&bars[b]), (uint32_t)lane));
+        const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)lane * EXW);
+        cc = Cand{k4.x, k4.y, k4.z, k4.w};
       }
+      const int wr = warp_pick(cc, lane < (int)CL);
+      const Cand wc = [&] {
+        const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)wr * EXW);
+        return Cand{k4.x, k4.y, k4.z, k4.w};
+      }();
+      const double* y = ex0 + (size_t)wr * EXW + 2;
+      const double p = y[PC];
+      const int q = (int)wc.pos;
+      if (tid == 0) {
+        prow[kk] = (int)wc.row;
+        if (rank == 0) {
+          a.rec_p[kg] = p;
+          a.rec_q[kg] = q;
+          a.rec_row[kg] = (int)wc.row;
+        }
+      }
+      const double rp = rcp_f64(p);
+      // ---- a3 + a5
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const bool is_piv = valid[i] && pst[i] < 0 && pos[i] == q;
+        if (pos[i] == kg) pos[i] = q;
+        if (is_piv) {
+          pos[i] = kg;
+          pst[i] = kg;
+          myrp[i] = rp;
+        }
+        const double nf = is_piv ? 0.0 : -(x[i][PC] * rp);
+        const double dcol = is_piv ? 1.0 : nf;
+        leaf_update<W, PC, SECOND>(x[i], y, nf, dcol);
+      }
+    };
+#pragma unroll 1
+    for (int kk = 0; kk < W; kk += 2) {
+      step(kk, std::integral_constant<int, 0>{}, std::integral_constant<bool, false>{});
+      step(kk + 1, std::integral_constant<int, 1>{}, std::integral_constant<bool, true>{});
     }
-    // ---- all: wait for the CL entries of this step, pick the cluster winner
-    mbar_wait_all(&bars[b], (uint32_t)((kk >> 1) & 1));
-    if (tid == 0) mbar_expect_tx(&bars[b], entry_bytes);   // arm the barrier for step kk + 2
-    const double* ex0 = exch + (size_t)(b * CL) * EXW;
-    Cand cc{0u, 0u, 0xffffffffu, 0u};
-    if (lane < (int)CL) {
-      const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)lane * EXW);
-      cc = Cand{k4.x, k4.y, k4.z, k4.w};
-    }
-    const int wr = warp_pick(cc, lane < (int)CL);
-    const Cand wc = [&] {
-      const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)wr * EXW);
-      return Cand{k4.x, k4.y, k4.z, k4.w};
-    }();
-    const double* y = ex0 + (size_t)wr * EXW + 2;
-    const double p = y[PC];
-    const int q = (int)wc.pos;
-    if (rank == 0 && tid == 0) {
-      a.rec_p[kg] = p;
-      a.rec_q[kg] = q;
-      a.rec_row[kg] = (int)wc.row;
-    }
-    const double rp = rcp_f64(p);
-    // ---- a3 + a5
+    // deferred normalisation of this leaf's pivot rows; write back the leaf columns (W)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const bool is_piv = valid[i] && pst[i] < 0 && pos[i] == q;
-      if (pos[i] == kg) pos[i] = q;
-      if (is_piv) {
-        pos[i] = kg;
-        pst[i] = kg;
-        myrp[i] = rp;
-      }
-      const double nf = is_piv ? 0.0 : -(x[i][PC] * rp);
-      const double dcol = is_piv ? 1.0 : nf;
-      leaf_update<W, PC, SECOND>(x[i], y, nf, dcol);
+      const double sc = (pst[i] >= c0 && pst[i] < c0 + W) ? myrp[i] : 1.0;
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[i][j] *= sc;
+      if (!valid[i]) continue;
+      double2* dst = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * npad + c0);
+#pragma unroll
+      for (int j = 0; j < W; j += 2) dst[j / 2] = make_double2(x[i][j], x[i][j + 1]);
     }
-  };
+    if (pw > W) {
+      // the leaf's transformation on the panel's other columns (left: D columns of earlier
+      // leaves, right: columns still to be factored), for this CTA's rows
+      cluster_sync_all();   // every CTA's earlier updates of the pivot rows are visible
+      const int half = pw / 2;
+      for (int e = tid; e < W * half; e += kLeafThreads) {
+        const int sidx = e / half, cc2 = e - sidx * half;
+        reinterpret_cast<double2*>(Rs + sidx * 128)[cc2] =
+            reinterpret_cast<const double2*>(a.X + (int64_t)prow[sidx] * npad + P0)[cc2];
+      }
+      cluster_sync_all();   // every CTA has its copy before any CTA rewrites a pivot row
 #pragma unroll 1
-  for (int kk = 0; kk < W; kk += 2) {
-    step(kk, std::integral_constant<int, 0>{}, std::integral_constant<bool, false>{});
-    step(kk + 1, std::integral_constant<int, 1>{}, std::integral_constant<bool, true>{});
+      for (int t0 = 0; t0 < pw; t0 += 8) {
+        if (t0 >= c0 - P0 && t0 < c0 - P0 + W) continue;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          if (!valid[i]) continue;
+          const bool rep = pst[i] >= c0 && pst[i] < c0 + W;   // pivot row of this leaf: replaced
+          double2* row = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * npad + P0 + t0);
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const double2 u = rep ? make_double2(0.0, 0.0) : row[j / 2];
+            v[j] = u.x;
+            v[j + 1] = u.y;
+          }
+#pragma unroll
+          for (int sidx = 0; sidx < W; ++sidx) {
+            const double2* rr = reinterpret_cast<const double2*>(Rs + sidx * 128 + t0);
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+              const double2 r2 = rr[j / 2];
+              v[j] = fma(x[i][sidx], r2.x, v[j]);
+              v[j + 1] = fma(x[i][sidx], r2.y, v[j + 1]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) row[j / 2] = make_double2(v[j], v[j + 1]);
+        }
+      }
+      __syncthreads();   // Rs / prow are rewritten by the next leaf
+    }
   }
-  // deferred normalisation of this leaf's pivot rows; write back
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     if (!valid[i]) continue;
-    const int r = rowid[i];
-    const double sc = (pst[i] >= c0 && pst[i] < c0 + W) ? myrp[i] : 1.0;
-    double2* dst = reinterpret_cast<double2*>(a.X + (int64_t)r * npad + c0);
-#pragma unroll
-    for (int j = 0; j < W; j += 2) dst[j / 2] = make_double2(x[i][j] * sc, x[i][j + 1] * sc);
-    a.pos[r] = pos[i];
-    a.pivstep[r] = pst[i];
+    a.pos[rowid[i]] = pos[i];
+    a.pivstep[rowid[i]] = pst[i];
   }
-  cluster_sync_all();   // no CTA leaves while a peer's st.async may still target it
+  cluster_sync_all();   // no CTA leaves while a peer's bulk copy may still target it
 }
 
 // ============================================================================ K4: GEMM update
@@ -418,10 +483,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 //   B: K x N (ld ldb)  = gathered pivot rows R
 //   C: M x N (ld ldc)  = X[:, target columns], updated in place
 //   replace(i) = pivstep[i] in [rep_lo, rep_hi)
-constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int BM = 128, BN = 64, BK = 16;   // 2 CTAs per SM: one streams C while the other computes
 constexpr int AST = BK + 4;    // A smem row stride (doubles): conflict-free fragment loads
 constexpr int BST = BN + 4;    // B smem row stride
-constexpr int kGemmThreads = 256;
+constexpr int kGemmThreads = 128;
 constexpr int GEMM_SMEM = 2 * (BM * AST + BK * BST) * (int)sizeof(double);
 
 struct GemmArgs {
@@ -431,9 +496,10 @@ struct GemmArgs {
   int64_t ldb;
   double* C;
   int64_t ldc;
-  int M, N, K;
+  int M, N, K;          // N counts the updated columns (the skipped range excluded)
   const int* pivstep;
   int rep_lo, rep_hi;
+  int skip_lo, skip_hi; // B / C columns [skip_lo, skip_hi) are not part of the update (128-aligned)
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, bool pred) {
@@ -444,6 +510,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
@@ -453,31 +524,38 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
         "d"(b[2]), "d"(b[3]));
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_update_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g) {
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                       // [2][BM][AST]
   double* Bs = gsm + 2 * BM * AST;        // [2][BK][BST]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;       // 2 x 4 warps, warp tile 64 x 32
+  const int wm = warp >> 1, wn = warp & 1;       // 2 x 2 warps, warp tile 64 x 32
   const int gq = lane >> 2, tq = lane & 3;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int ntn = (g.N + BN - 1) / BN, ntm = (g.M + BM - 1) / BM;
+  const int shift = g.skip_hi - g.skip_lo;
+  // persistent: tiles in column-major order of the tile grid (consecutive CTAs share B)
+  for (int tile = blockIdx.x; tile < ntn * ntm; tile += gridDim.x) {
+  const int m0 = (tile % ntm) * BM;
+  const int nc0 = (tile / ntm) * BN;                       // compact column of the tile
+  const int n0 = nc0 + (nc0 >= g.skip_lo ? shift : 0);     // real column
+  const int nlim = n0 + (g.N - nc0);                        // real column bound of this tile
 
   auto load_stage = [&](int st, int k0) {
-    // A: BM x BK doubles = 1024 16-byte chunks; B: BK x BN = 1024 chunks
+    // A: BM x BK doubles in 16-byte chunks (BK/2 per row); B: BK x BN (BN/2 per row)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < BM * BK / 2 / kGemmThreads; ++u) {
       const int c = tid + u * kGemmThreads;
-      const int r = c >> 3, kc = (c & 7) * 2;
+      const int r = c / (BK / 2), kc = (c % (BK / 2)) * 2;
       const int gr = m0 + r;
       const bool ok = gr < g.M && k0 + kc < g.K;
       cp_async16(smem_u32(As + st * BM * AST + r * AST + kc), g.A + (ok ? (int64_t)gr * g.lda + k0 + kc : 0), ok);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < BK * BN / 2 / kGemmThreads; ++u) {
       const int c = tid + u * kGemmThreads;
-      const int r = c >> 6, nc = (c & 63) * 2;
+      const int r = c / (BN / 2), nc = (c % (BN / 2)) * 2;
       const int gc = n0 + nc;
-      const bool ok = gc < g.N && k0 + r < g.K;
+      const bool ok = gc < nlim && k0 + r < g.K;
       cp_async16(smem_u32(Bs + st * BK * BST + r * BST + nc), g.B + (ok ? (int64_t)(k0 + r) * g.ldb + gc : 0), ok);
     }
   };
@@ -498,7 +576,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_update_kernel(GemmArgs g
       for (int nt = 0; nt < 4; ++nt) {
         const int c = n0 + wn * 32 + nt * 8 + 2 * tq;
         double2 v = make_double2(0.0, 0.0);
-        if (keep && c < g.N) v = *reinterpret_cast<const double2*>(g.C + (int64_t)r * g.ldc + c);
+        if (keep && c < nlim) v = *reinterpret_cast<const double2*>(g.C + (int64_t)r * g.ldc + c);
         acc[mt][nt][2 * h] = v.x;
         acc[mt][nt][2 * h + 1] = v.y;
       }
@@ -515,6 +593,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_update_kernel(GemmArgs g
     __syncthreads();
     const double* as = As + (kb & 1) * BM * AST + (wm * 64) * AST;
     const double* bs = Bs + (kb & 1) * BK * BST + wn * 32;
+    // m16n8k16 (8 DMMA.8x8x4 in SASS); measured faster here than k-outer m8n8k4 issue
     double bf[4][4];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
@@ -543,10 +622,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_update_kernel(GemmArgs g
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const int c = n0 + wn * 32 + nt * 8 + 2 * tq;
-        if (c < g.N)
+        if (c < nlim)
           *reinterpret_cast<double2*>(g.C + (int64_t)r * g.ldc + c) = make_double2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]);
       }
     }
+  __syncthreads();   // the next tile's first cp.async overwrites stage 0
+  }
+  // launched as a programmatic dependent of the panel kernel: complete only after it
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ============================================================================ host driver
@@ -619,17 +702,32 @@ static cudaError_t launch_leaf(const LeafArgs& la, int cl, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, leaf_kernel<W, RPT>, la);
 }
 
-static cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
+// grid_sms: SMs the persistent grid may use; pdl: launch as a programmatic dependent of the
+// preceding kernel in the stream (it may start once that kernel has released it).
+static cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s, int grid_sms = 0, bool pdl = false) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(gemm_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_update_kernel, kGemmThreads, GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
-  gemm_update_kernel<<<grid, kGemmThreads, GEMM_SMEM, s>>>(g);
-  return cudaGetLastError();
+  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
+  const int sms = grid_sms > 0 ? grid_sms : device_sm_count();
+  const int grid = tiles < sms * per_sm ? tiles : sms * per_sm;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.dynamicSmemBytes = GEMM_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, gemm_update_kernel, g);
 }
 
 // Leaf configuration: cluster size and rows per thread, leaf width W.
@@ -682,46 +780,31 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   GJ_DBG("setup");
 
+  // Look-ahead over panels: panel k+1 is updated by panel k first and factored by the
+  // cluster kernel while the rest of panel k's update runs on the other SMs.
+  auto factor_panel = [&](int P0, int pw) -> cudaError_t {
+    LeafArgs la{w.X, npad, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row};
+    if (lc.w == 32) return launch_leaf<32, 1>(la, lc.cl, s);
+    if (lc.w == 16) return launch_leaf<16, 2>(la, lc.cl, s);
+    return launch_leaf<8, 4>(la, lc.cl, s);
+  };
+  auto width = [&](int P0) { return (npad - P0) < PANEL ? (npad - P0) : PANEL; };
+  if ((e = factor_panel(0, width(0))) != cudaSuccess) return e;
+  GJ_DBG("panel 0");
   for (int P0 = 0; P0 < npad; P0 += PANEL) {
-    const int pw = (npad - P0) < PANEL ? (npad - P0) : PANEL;
-    for (int L0 = P0; L0 < P0 + pw; L0 += lc.w) {
-      LeafArgs la{w.X, npad, L0, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row};
-      if (lc.w == 32)
-        e = launch_leaf<32, 1>(la, lc.cl, s);
-      else if (lc.w == 16)
-        e = launch_leaf<16, 2>(la, lc.cl, s);
-      else
-        e = launch_leaf<8, 4>(la, lc.cl, s);
-      if (e != cudaSuccess) return e;
-      GJ_DBG("leaf");
-      if (debug_sync()) {
-        int hr[64], hpos[64];
-        cudaMemcpy(hr, w.rec_row + L0, sizeof(int) * lc.w, cudaMemcpyDeviceToHost);
-        cudaMemcpy(hpos, w.rec_q + L0, sizeof(int) * lc.w, cudaMemcpyDeviceToHost);
-        for (int t = 0; t < lc.w; ++t)
-          if (hr[t] < 0 || hr[t] >= npad || hpos[t] < L0 + t || hpos[t] >= npad)
-            fprintf(stderr, "gjinv large: leaf %d step %d bad record row=%d q=%d\n", L0, t, hr[t], hpos[t]);
-      }
-      // the leaf's transformation applied to the other columns of the panel (left: the
-      // D columns of earlier leaves, right: columns still to be factored)
-      if (pw > lc.w) {
-        gather_rows_kernel<<<dim3(1, lc.w), 128, 0, s>>>(w.X, npad, w.rec_row + L0, lc.w, w.R, P0, P0 + pw);
-        GJ_DBG("panel gather");
-        GemmArgs gl{w.X + L0, npad, w.R + P0, npad, w.X + P0, npad, npad, L0 - P0, lc.w, w.pivstep, L0, L0 + lc.w};
-        if ((e = launch_gemm(gl, s)) != cudaSuccess) return e;
-        GJ_DBG("panel gemm left");
-        const int T0 = L0 + lc.w, T1 = P0 + pw;
-        GemmArgs gr{w.X + L0, npad, w.R + T0, npad, w.X + T0, npad, npad, T1 - T0, lc.w, w.pivstep, L0, L0 + lc.w};
-        if ((e = launch_gemm(gr, s)) != cudaSuccess) return e;
-        GJ_DBG("panel gemm");
-      }
-    }
-    // trailing update of every column outside the panel
+    const int pw = width(P0);
+    const int P1 = P0 + pw;
+    const int pw1 = P1 < npad ? width(P1) : 0;
     gather_rows_kernel<<<dim3((npad / 2 + 255) / 256, pw), 256, 0, s>>>(w.X, npad, w.rec_row + P0, pw, w.R, 0, npad);
-    GemmArgs gl{w.X + P0, npad, w.R, npad, w.X, npad, npad, P0, pw, w.pivstep, P0, P0 + pw};
-    if ((e = launch_gemm(gl, s)) != cudaSuccess) return e;
-    GemmArgs gr{w.X + P0, npad, w.R + P0 + pw, npad, w.X + P0 + pw, npad, npad, npad - P0 - pw, pw, w.pivstep, P0, P0 + pw};
-    if ((e = launch_gemm(gr, s)) != cudaSuccess) return e;
+    if (pw1 > 0) {
+      GemmArgs ga{w.X + P0, npad, w.R + P1, npad, w.X + P1, npad, npad, pw1, pw, w.pivstep, P0, P0 + pw, 0, 0};
+      if ((e = launch_gemm(ga, s)) != cudaSuccess) return e;
+      GJ_DBG("look-ahead gemm");
+      if ((e = factor_panel(P1, pw1)) != cudaSuccess) return e;
+    }
+    // every column outside panels k and k+1 (the D columns on the left included)
+    GemmArgs gb{w.X + P0, npad, w.R, npad, w.X, npad, npad, npad - pw - pw1, pw, w.pivstep, P0, P0 + pw, P0, P1 + pw1};
+    if ((e = launch_gemm(gb, s, pw1 > 0 ? sms - lc.cl : 0, pw1 > 0 && !debug_sync())) != cudaSuccess) return e;
     GJ_DBG("trailing gemm");
   }
   if (Ainv != nullptr)
