@@ -126,6 +126,74 @@ gj_status gj_invert_batched_host(gj_dtype dt, int n, int64_t batch, const void* 
                                  int8_t* sign_host, void* det_host, int32_t* info_host,
                                  double tol, int64_t chunk);
 
+/*
+ * ---------------------------------------------------------------------------------------
+ * Distributed large-n inversion (fp64, n > 64) over P ranks, one GPU each: the building
+ * blocks of the column-block-cyclic Gauss–Jordan.  The global matrix is
+ * padded with an identity block to npad = ceil(n / GJ_DIST_BLOCK) * GJ_DIST_BLOCK;
+ * global column block j (GJ_DIST_BLOCK columns) lives on rank j % P.  Rows are complete
+ * on every rank, so the pivot search of a panel (the max-|a_ik| rule, Obs. 3 L60) is
+ * local to the panel's owner.  The collectives are the caller's (NCCL via
+ * torch.distributed in paper_1401_7962_b200/dist.py): per panel k the owner calls
+ * gj_dist_factor, broadcasts W, pos, pivstep and the record of steps [k*B, (k+1)*B),
+ * then every rank calls gj_dist_update; the un-permutation (listing L179-L198) is one
+ * all-to-all of columns planned by gj_dist_unpermute_plan.  Same pivots, det and
+ * inverse as gj_invert (the aggregation of Eqs. (14)-(15), L61-L72, is identical).
+ * All pointers are DEVICE pointers owned by the caller; work is enqueued on `stream`.
+ * Replicated arrays (length npad, int32 unless stated): pos (physical position of each
+ * row in the listing's swapped array), pivstep (step at which a row was pivot, -1 if
+ * not yet), rec_p (fp64 pivot per step), rec_q (pivot position per step), rec_row
+ * (pivot row per step).  X_local is npad x ncols_local row-major (this rank's padded
+ * columns in increasing global order), W is npad x GJ_DIST_BLOCK, R GJ_DIST_BLOCK x
+ * ncols_local.  Errors: GJ_ERR_ARG for bad sizes / ranks / NULL, GJ_ERR_CUDA on launch
+ * failure.
+ * ---------------------------------------------------------------------------------------
+ */
+#define GJ_DIST_BLOCK 128
+#define GJ_DIST_MAX_RANKS 8
+
+/* npad, this rank's padded column count and how many of them are real (< n). */
+gj_status gj_dist_sizes(int n, int nranks, int rank, int* npad, int* ncols_local, int* ncols_local_real);
+
+/* X_local = this rank's columns of blockdiag(A, I); A_local holds the rank's ncols_local_real
+ * real columns (n rows, row stride lda >= ncols_local_real).  pos/pivstep initialised;
+ * *smax_bits = bit pattern of max |a_ij| over the local columns (reduce MAX over ranks
+ * before gj_dist_finalize: the zero threshold of Obs. 2, L59, is relative to it, G1). */
+gj_status gj_dist_init(int n, int nranks, int rank, const double* A_local, int64_t lda, double* X_local,
+                       int32_t* pos, int32_t* pivstep, uint64_t* smax_bits, void* stream);
+
+/* Owner of panel k (k % nranks == rank) only: GJ_DIST_BLOCK pivot steps (a2-a6) on the
+ * panel's local columns, in place, updating pos / pivstep / rec_* and copying the
+ * factored panel to W. */
+gj_status gj_dist_factor(int n, int nranks, int rank, int k, double* X_local, int32_t* pos, int32_t* pivstep,
+                         double* rec_p, int32_t* rec_q, int32_t* rec_row, double* W, void* stream);
+
+/* Every rank, after the broadcast of panel k: X_local[:, c] += (W - S) R for every local
+ * column c outside panel k (R = the panel's pivot rows of X_local, staged in R). */
+gj_status gj_dist_update(int n, int nranks, int rank, int k, double* X_local, const double* W, const int32_t* pivstep,
+                         const int32_t* rec_row, double* R, void* stream);
+
+/* log|det|, sign, info and ipiv from the replicated record (Eq. (13) + G4); tol as
+ * gj_invert (< 0: n * eps). Any rank; outputs may be NULL. */
+gj_status gj_dist_finalize(int n, const double* rec_p, const int32_t* rec_q, double tol, const uint64_t* smax_bits,
+                           int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, void* stream);
+
+/* Un-permutation plan: send_cols (<= ncols_local) = local compact columns ordered by
+ * (destination rank, output column); recv_cols = local output columns ordered by
+ * (source rank, output column); counts[0..P) columns sent to / counts[P..2P) received
+ * from each rank. nranks <= GJ_DIST_MAX_RANKS. */
+gj_status gj_dist_unpermute_plan(int n, int nranks, int rank, const int32_t* pivstep, int32_t* send_cols,
+                                 int32_t* recv_cols, int32_t* counts, void* stream);
+
+/* sendbuf[t][i] = X_local[rec_row[i]][send_cols[t]], t < m, i < n (m columns of n). */
+gj_status gj_dist_unpermute_pack(int n, int nranks, int rank, const double* X_local, const int32_t* rec_row,
+                                 const int32_t* send_cols, int m, double* sendbuf, void* stream);
+
+/* Ainv_local[i][recv_cols[t]] = recvbuf[t][i]: Ainv_local is n x (this rank's real output
+ * columns, in increasing global order) with row stride ld. */
+gj_status gj_dist_unpermute_unpack(int n, const double* recvbuf, const int32_t* recv_cols, int m, double* Ainv_local,
+                                   int64_t ld, void* stream);
+
 /* Static description of a status code. */
 const char* gj_status_string(gj_status s);
 

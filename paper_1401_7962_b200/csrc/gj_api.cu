@@ -170,4 +170,72 @@ gj_status gj_invert_batched_host(gj_dtype dt, int n, int64_t batch, const void* 
   return st;
 }
 
+// ---------------------------------------------------------------- distributed large n
+static bool dist_args_ok(int n, int P, int rank) { return n > GJ_BATCHED_MAX_N && P >= 1 && P <= GJ_DIST_MAX_RANKS && rank >= 0 && rank < P; }
+
+gj_status gj_dist_sizes(int n, int nranks, int rank, int* npad, int* ncols_local, int* ncols_local_real) {
+  if (!dist_args_ok(n, nranks, rank) || !npad || !ncols_local || !ncols_local_real) return GJ_ERR_ARG;
+  dist_sizes(n, nranks, rank, npad, ncols_local, ncols_local_real);
+  return GJ_OK;
+}
+
+gj_status gj_dist_init(int n, int nranks, int rank, const double* A_local, int64_t lda, double* X_local,
+                       int32_t* pos, int32_t* pivstep, uint64_t* smax_bits, void* stream) {
+  if (!dist_args_ok(n, nranks, rank) || !X_local || !pos || !pivstep || !smax_bits) return GJ_ERR_ARG;
+  int npad, nl, nr;
+  dist_sizes(n, nranks, rank, &npad, &nl, &nr);
+  if (nr > 0 && (!A_local || lda < nr)) return GJ_ERR_ARG;
+  return dist_init(n, nranks, rank, A_local, lda, X_local, pos, pivstep, reinterpret_cast<unsigned long long*>(smax_bits),
+                   static_cast<cudaStream_t>(stream)) == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
+gj_status gj_dist_factor(int n, int nranks, int rank, int k, double* X_local, int32_t* pos, int32_t* pivstep,
+                         double* rec_p, int32_t* rec_q, int32_t* rec_row, double* W, void* stream) {
+  if (!dist_args_ok(n, nranks, rank) || !X_local || !pos || !pivstep || !rec_p || !rec_q || !rec_row || !W) return GJ_ERR_ARG;
+  int npad, nl, nr;
+  dist_sizes(n, nranks, rank, &npad, &nl, &nr);
+  if (k < 0 || k >= npad / GJ_DIST_BLOCK || k % nranks != rank) return GJ_ERR_ARG;
+  return dist_factor(n, nranks, rank, k, X_local, pos, pivstep, rec_p, rec_q, rec_row, W,
+                     static_cast<cudaStream_t>(stream)) == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
+gj_status gj_dist_update(int n, int nranks, int rank, int k, double* X_local, const double* W, const int32_t* pivstep,
+                         const int32_t* rec_row, double* R, void* stream) {
+  if (!dist_args_ok(n, nranks, rank) || !W || !pivstep || !rec_row) return GJ_ERR_ARG;
+  int npad, nl, nr;
+  dist_sizes(n, nranks, rank, &npad, &nl, &nr);
+  if (k < 0 || k >= npad / GJ_DIST_BLOCK) return GJ_ERR_ARG;
+  if (nl > 0 && (!X_local || !R)) return GJ_ERR_ARG;
+  return dist_update(n, nranks, rank, k, X_local, W, pivstep, rec_row, R, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? GJ_OK : GJ_ERR_CUDA;
+}
+
+gj_status gj_dist_finalize(int n, const double* rec_p, const int32_t* rec_q, double tol, const uint64_t* smax_bits,
+                           int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, void* stream) {
+  if (n < 1 || !rec_p || !rec_q || !smax_bits) return GJ_ERR_ARG;
+  return dist_finalize(n, rec_p, rec_q, resolve_tol(GJ_F64, n, tol), reinterpret_cast<const unsigned long long*>(smax_bits),
+                       ipiv, logabsdet, sign, info, static_cast<cudaStream_t>(stream)) == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
+gj_status gj_dist_unpermute_plan(int n, int nranks, int rank, const int32_t* pivstep, int32_t* send_cols,
+                                 int32_t* recv_cols, int32_t* counts, void* stream) {
+  if (!dist_args_ok(n, nranks, rank) || !pivstep || !send_cols || !recv_cols || !counts) return GJ_ERR_ARG;
+  return dist_unpermute_plan(n, nranks, rank, pivstep, send_cols, recv_cols, counts, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
+gj_status gj_dist_unpermute_pack(int n, int nranks, int rank, const double* X_local, const int32_t* rec_row,
+                                 const int32_t* send_cols, int m, double* sendbuf, void* stream) {
+  if (!dist_args_ok(n, nranks, rank) || m < 0 || (m > 0 && (!X_local || !rec_row || !send_cols || !sendbuf))) return GJ_ERR_ARG;
+  return dist_unpermute_pack(n, nranks, rank, X_local, rec_row, send_cols, m, sendbuf, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
+gj_status gj_dist_unpermute_unpack(int n, const double* recvbuf, const int32_t* recv_cols, int m, double* Ainv_local,
+                                   int64_t ld, void* stream) {
+  if (n < 1 || m < 0 || (m > 0 && (!recvbuf || !recv_cols || !Ainv_local))) return GJ_ERR_ARG;
+  return dist_unpermute_unpack(n, recvbuf, recv_cols, m, Ainv_local, ld, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? GJ_OK : GJ_ERR_CUDA;
+}
+
 }  // extern "C"

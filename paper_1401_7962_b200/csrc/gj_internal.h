@@ -31,6 +31,23 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
                              double* logabsdet, int8_t* sign, double* det, int32_t* info, double tol, void* ws,
                              cudaStream_t s);
 
+// Distributed large-n steps (gj_large.cu; column-block-cyclic, block 128).
+void dist_sizes(int n, int P, int rank, int* npad, int* nl, int* nl_real);
+cudaError_t dist_init(int n, int P, int rank, const double* A_local, int64_t lda, double* Xl, int* pos, int* pivstep,
+                      unsigned long long* smax, cudaStream_t s);
+cudaError_t dist_factor(int n, int P, int rank, int k, double* Xl, int* pos, int* pivstep, double* rec_p, int* rec_q,
+                        int* rec_row, double* W, cudaStream_t s);
+cudaError_t dist_update(int n, int P, int rank, int k, double* Xl, const double* W, const int* pivstep,
+                        const int* rec_row, double* R, cudaStream_t s);
+cudaError_t dist_finalize(int n, const double* rec_p, const int* rec_q, double tol, const unsigned long long* smax,
+                          int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, cudaStream_t s);
+cudaError_t dist_unpermute_plan(int n, int P, int rank, const int* pivstep, int* send_cols, int* recv_cols, int* counts,
+                                cudaStream_t s);
+cudaError_t dist_unpermute_pack(int n, int P, int rank, const double* Xl, const int* rec_row, const int* send_cols,
+                                int m, double* sendbuf, cudaStream_t s);
+cudaError_t dist_unpermute_unpack(int n, const double* recvbuf, const int* recv_cols, int m, double* Ainv_local,
+                                  int64_t ld, cudaStream_t s);
+
 // Number of SMs of the current device (cached per device).
 int device_sm_count();
 

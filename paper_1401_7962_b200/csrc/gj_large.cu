@@ -75,12 +75,12 @@ __global__ void absmax_kernel(const double* __restrict__ A, int64_t lda, int n, 
 
 // R[s][c] = X[rows[s]][c] for s < w, c in [c_lo, c_hi) (R has leading dimension npad;
 // c_lo, c_hi even)
-__global__ void gather_rows_kernel(const double* __restrict__ X, int npad, const int* __restrict__ rows, int w,
+__global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ld, const int* __restrict__ rows, int w,
                                    double* __restrict__ R, int c_lo, int c_hi) {
   const int s = blockIdx.y;
   if (s >= w) return;
-  const double2* src = reinterpret_cast<const double2*>(X + (int64_t)rows[s] * npad + c_lo);
-  double2* dst = reinterpret_cast<double2*>(R + (int64_t)s * npad + c_lo);
+  const double2* src = reinterpret_cast<const double2*>(X + (int64_t)rows[s] * ld + c_lo);
+  double2* dst = reinterpret_cast<double2*>(R + (int64_t)s * ld + c_lo);
   const int m = (c_hi - c_lo) / 2;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) dst[j] = src[j];
 }
@@ -159,9 +159,11 @@ __device__ __forceinline__ void st_remote_v4(uint32_t raddr, uint4 v) {
 }
 
 struct LeafArgs {
-  double* X;         // npad x npad, ld npad
-  int npad;          // padded order
-  int c0;            // first column (= first global step) of the panel
+  double* X;         // npad rows, leading dimension ld (all columns, or one rank's local columns)
+  int64_t ld;        // row stride of X (elements)
+  int npad;          // padded order (rows)
+  int c0;            // first column of the panel in X
+  int k0;            // global step of the panel's first column
   int pw;            // panel width (a multiple of the leaf width W)
   int* pos;          // [npad] physical position of each row
   int* pivstep;      // [npad] step at which the row was pivot, -1 if not yet
@@ -272,6 +274,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LS::EXCH + 2 * CL * EXW * 8);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npad = a.npad, P0 = a.c0, pw = a.pw;
+  const int64_t ld = a.ld;
   const uint32_t entry_bytes = (uint32_t)(CL * EXW * 8);
 
   double x[RPT][W];
@@ -296,12 +299,14 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   __syncthreads();
   cluster_sync_all();   // every CTA resident and its barriers armed before any remote store
 
-  for (int c0 = P0, leaf = 0; c0 < P0 + pw; c0 += W, ++leaf) {
+  for (int off = 0, leaf = 0; off < pw; off += W, ++leaf) {
+    const int c0 = P0 + off;       // column of the leaf in X
+    const int s0 = a.k0 + off;     // global step of the leaf's first column
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       myrp[i] = 1.0;
       if (valid[i]) {
-        const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)rowid[i] * npad + c0);
+        const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)rowid[i] * ld + c0);
 #pragma unroll
         for (int j = 0; j < W; j += 2) {
           const double2 v = src[j / 2];
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     auto step = [&](int kk, auto pc_tag, auto second_tag) {
       constexpr int PC = decltype(pc_tag)::value;
       constexpr bool SECOND = decltype(second_tag)::value;
-      const int kg = c0 + kk;
+      const int kg = s0 + kk;
       const int gk = leaf * W + kk;   // step count within this launch: mbarrier phase
       const int b = gk & 1;
       // ---- a2: this thread's best candidate among its un-pivoted rows
@@ -417,11 +422,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     // deferred normalisation of this leaf's pivot rows; write back the leaf columns (W)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const double sc = (pst[i] >= c0 && pst[i] < c0 + W) ? myrp[i] : 1.0;
+      const double sc = (pst[i] >= s0 && pst[i] < s0 + W) ? myrp[i] : 1.0;
 #pragma unroll
       for (int j = 0; j < W; ++j) x[i][j] *= sc;
       if (!valid[i]) continue;
-      double2* dst = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * npad + c0);
+      double2* dst = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * ld + c0);
 #pragma unroll
       for (int j = 0; j < W; j += 2) dst[j / 2] = make_double2(x[i][j], x[i][j + 1]);
     }
@@ -433,7 +438,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
       for (int e = tid; e < W * half; e += kLeafThreads) {
         const int sidx = e / half, cc2 = e - sidx * half;
         reinterpret_cast<double2*>(Rs + sidx * 128)[cc2] =
-            reinterpret_cast<const double2*>(a.X + (int64_t)prow[sidx] * npad + P0)[cc2];
+            reinterpret_cast<const double2*>(a.X + (int64_t)prow[sidx] * ld + P0)[cc2];
       }
       cluster_sync_all();   // every CTA has its copy before any CTA rewrites a pivot row
 #pragma unroll 1
@@ -442,8 +447,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           if (!valid[i]) continue;
-          const bool rep = pst[i] >= c0 && pst[i] < c0 + W;   // pivot row of this leaf: replaced
-          double2* row = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * npad + P0 + t0);
+          const bool rep = pst[i] >= s0 && pst[i] < s0 + W;   // pivot row of this leaf: replaced
+          double2* row = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * ld + P0 + t0);
           double v[8];
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
@@ -783,7 +788,7 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
   // Look-ahead over panels: panel k+1 is updated by panel k first and factored by the
   // cluster kernel while the rest of panel k's update runs on the other SMs.
   auto factor_panel = [&](int P0, int pw) -> cudaError_t {
-    LeafArgs la{w.X, npad, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row};
+    LeafArgs la{w.X, npad, npad, P0, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row};
     if (lc.w == 32) return launch_leaf<32, 1>(la, lc.cl, s);
     if (lc.w == 16) return launch_leaf<16, 2>(la, lc.cl, s);
     return launch_leaf<8, 4>(la, lc.cl, s);
@@ -810,6 +815,236 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
   if (Ainv != nullptr)
     unpermute_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
   finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet, sign, det, info);
+  return cudaGetLastError();
+}
+
+// ============================================================================ distributed
+// Column-block-cyclic large-n inversion over P ranks: global column block j
+// (DB = 128 columns, the panel width) lives on rank j % P.  Rows are complete on every
+// rank, so a panel's pivot search is local to its owner; each panel step is
+//   owner:  dist_factor  (the panel kernel above, on the owner's local columns) -> W
+//   all:    broadcast W + the step record + positions from the owner (caller, NCCL)
+//   all:    dist_update  (gather the panel's pivot rows of the local columns, DMMA GEMM)
+// and the un-permutation (listing L179-L198) is one all-to-all of columns at the end.
+namespace dist {
+constexpr int DB = large::PANEL;
+
+__host__ __device__ inline int nblocks(int npad) { return npad / DB; }
+__host__ __device__ inline int local_blocks(int npad, int P, int rank) { return (nblocks(npad) - rank + P - 1) / P; }
+__host__ __device__ inline int global_col(int lc, int P, int rank) { return ((lc / DB) * P + rank) * DB + lc % DB; }
+__host__ __device__ inline int owner(int gc, int P) { return (gc / DB) % P; }
+__host__ __device__ inline int local_col(int gc, int P) { return (gc / DB / P) * DB + gc % DB; }
+
+// X_local (npad x nl) = this rank's columns of blockdiag(A, I); A_local holds the rank's
+// real columns (global column < n) in increasing order, row stride lda.
+__global__ void init_local_kernel(const double* __restrict__ A, int64_t lda, int n, int npad, int P, int rank, int nl,
+                                  double* __restrict__ X, unsigned long long* smax) {
+  double m = 0.0;
+  const int64_t tot = (int64_t)npad * nl;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / nl), lc = (int)(e - (int64_t)i * nl);
+    const int gc = global_col(lc, P, rank);
+    double v;
+    if (i < n && gc < n) {
+      v = A[(int64_t)i * lda + lc];   // local real columns come first, in order (gc < n <=> lc < real count)
+      m = fmax(m, fabs(v));
+    } else {
+      v = (i == gc) ? 1.0 : 0.0;
+    }
+    X[e] = v;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong(m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+    b = ob > b ? ob : b;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(smax, b);
+}
+
+// W (npad x DB, ld DB) = X[:, c0 .. c0 + DB)
+__global__ void copy_panel_kernel(const double* __restrict__ X, int64_t ld, int npad, int c0, double* __restrict__ W) {
+  const int64_t tot = (int64_t)npad * (DB / 2);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / (DB / 2)), c = (int)(e - (int64_t)i * (DB / 2));
+    reinterpret_cast<double2*>(W + (int64_t)i * DB)[c] = reinterpret_cast<const double2*>(X + (int64_t)i * ld + c0)[c];
+  }
+}
+
+// Exchange plan of the un-permutation Ainv[i][j] = X[rec_row[i]][pivstep[j]] (one CTA):
+// for every output column j < n, source compact column c = pivstep[j] on rank owner(c),
+// destination rank owner(j).  This rank sends its columns ordered by (destination, j) and
+// receives ordered by (source, j).  counts[0..P) = columns sent to each rank,
+// counts[P..2P) = columns received from each rank.
+constexpr int kPlanThreads = 512, kMaxP = 8;
+__global__ void __launch_bounds__(kPlanThreads) unpermute_plan_kernel(int n, int P, int rank, const int* __restrict__ pivstep,
+                                                                      int* send_cols, int* recv_cols, int* counts) {
+  __shared__ int cs[kMaxP][kPlanThreads + 1], cr[kMaxP][kPlanThreads + 1];
+  __shared__ int bs[kMaxP + 1], br[kMaxP + 1];
+  const int t = threadIdx.x;
+  const int chunk = (n + kPlanThreads - 1) / kPlanThreads;
+  const int j0 = t * chunk, j1 = min(n, j0 + chunk);
+  int ls[kMaxP], lr[kMaxP];
+#pragma unroll
+  for (int d = 0; d < kMaxP; ++d) ls[d] = lr[d] = 0;
+  for (int j = j0; j < j1; ++j) {
+    const int c = pivstep[j];
+    const int src = owner(c, P), dst = owner(j, P);
+#pragma unroll
+    for (int d = 0; d < kMaxP; ++d) {
+      if (src == rank && dst == d) ++ls[d];
+      if (dst == rank && src == d) ++lr[d];
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < kMaxP; ++d) {
+    cs[d][t] = ls[d];
+    cr[d][t] = lr[d];
+  }
+  __syncthreads();
+  if (t < 2 * kMaxP) {   // exclusive scans over threads, one per (direction, rank)
+    int* a = t < kMaxP ? cs[t] : cr[t - kMaxP];
+    int run = 0;
+    for (int u = 0; u < kPlanThreads; ++u) {
+      const int v = a[u];
+      a[u] = run;
+      run += v;
+    }
+    a[kPlanThreads] = run;
+  }
+  __syncthreads();
+  if (t == 0) {
+    int x = 0, y = 0;
+    for (int d = 0; d < kMaxP; ++d) {
+      bs[d] = x;
+      br[d] = y;
+      x += cs[d][kPlanThreads];
+      y += cr[d][kPlanThreads];
+      if (d < P) {
+        counts[d] = cs[d][kPlanThreads];
+        counts[P + d] = cr[d][kPlanThreads];
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < kMaxP; ++d) {
+    ls[d] = bs[d] + cs[d][t];
+    lr[d] = br[d] + cr[d][t];
+  }
+  for (int j = j0; j < j1; ++j) {
+    const int c = pivstep[j];
+    const int src = owner(c, P), dst = owner(j, P);
+#pragma unroll
+    for (int d = 0; d < kMaxP; ++d) {
+      if (src == rank && dst == d) send_cols[ls[d]++] = local_col(c, P);
+      if (dst == rank && src == d) recv_cols[lr[d]++] = local_col(j, P);
+    }
+  }
+}
+
+// sendbuf[t][i] = X[rec_row[i]][send_cols[t]] (i < n): row gather of the un-permutation
+__global__ void unpermute_pack_kernel(int n, const double* __restrict__ X, int64_t ld, const int* __restrict__ rec_row,
+                                      const int* __restrict__ send_cols, int m, double* __restrict__ out) {
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n) return;
+  const double* src = X + (int64_t)rec_row[i] * ld;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x)
+    out[(int64_t)t * n + i] = src[send_cols[t]];
+}
+// Ainv_local[i][recv_cols[t]] = in[t][i]
+__global__ void unpermute_unpack_kernel(int n, const double* __restrict__ in, const int* __restrict__ recv_cols, int m,
+                                        double* __restrict__ Y, int64_t ldy) {
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n) return;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x)
+    Y[(int64_t)i * ldy + recv_cols[t]] = in[(int64_t)t * n + i];
+}
+}  // namespace dist
+
+void dist_sizes(int n, int P, int rank, int* npad, int* nl, int* nl_real) {
+  const int np = (n + dist::DB - 1) / dist::DB * dist::DB;
+  *npad = np;
+  *nl = dist::local_blocks(np, P, rank) * dist::DB;
+  int cnt = 0;
+  for (int lc = 0; lc < *nl; ++lc)
+    if (dist::global_col(lc, P, rank) < n) ++cnt;
+  *nl_real = cnt;
+}
+
+cudaError_t dist_init(int n, int P, int rank, const double* A_local, int64_t lda, double* Xl, int* pos, int* pivstep,
+                      unsigned long long* smax, cudaStream_t s) {
+  int npad, nl, nr;
+  dist_sizes(n, P, rank, &npad, &nl, &nr);
+  const int sms = device_sm_count();
+  large::init_perm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(npad, pos, pivstep);
+  cudaMemsetAsync(smax, 0, 8, s);
+  if (nl > 0) dist::init_local_kernel<<<sms * 8, 256, 0, s>>>(A_local, lda, n, npad, P, rank, nl, Xl, smax);
+  return cudaGetLastError();
+}
+
+cudaError_t dist_factor(int n, int P, int rank, int k, double* Xl, int* pos, int* pivstep, double* rec_p, int* rec_q,
+                        int* rec_row, double* W, cudaStream_t s) {
+  using namespace large;
+  int npad, nl, nr;
+  dist_sizes(n, P, rank, &npad, &nl, &nr);
+  if (k < 0 || k >= dist::nblocks(npad) || k % P != rank) return cudaErrorInvalidValue;
+  LeafCfg lc;
+  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
+  const int c0 = (k / P) * dist::DB;
+  LeafArgs la{Xl, nl, npad, c0, k * dist::DB, dist::DB, pos, pivstep, rec_p, rec_q, rec_row};
+  cudaError_t e = lc.w == 32 ? launch_leaf<32, 1>(la, lc.cl, s)
+                  : lc.w == 16 ? launch_leaf<16, 2>(la, lc.cl, s)
+                               : launch_leaf<8, 4>(la, lc.cl, s);
+  if (e != cudaSuccess) return e;
+  dist::copy_panel_kernel<<<device_sm_count() * 4, 256, 0, s>>>(Xl, nl, npad, c0, W);
+  return cudaGetLastError();
+}
+
+cudaError_t dist_update(int n, int P, int rank, int k, double* Xl, const double* W, const int* pivstep,
+                        const int* rec_row, double* R, cudaStream_t s) {
+  using namespace large;
+  int npad, nl, nr;
+  dist_sizes(n, P, rank, &npad, &nl, &nr);
+  if (k < 0 || k >= dist::nblocks(npad)) return cudaErrorInvalidValue;
+  if (nl == 0) return cudaSuccess;
+  const int k0 = k * dist::DB;
+  gather_rows_kernel<<<dim3((nl / 2 + 255) / 256, dist::DB), 256, 0, s>>>(Xl, nl, rec_row + k0, dist::DB, R, 0, nl);
+  const bool own = k % P == rank;
+  const int c0 = own ? (k / P) * dist::DB : 0;
+  GemmArgs g{W, dist::DB, R, nl, Xl, nl, npad, nl - (own ? dist::DB : 0), dist::DB, pivstep, k0, k0 + dist::DB,
+             own ? c0 : 0, own ? c0 + dist::DB : 0};
+  return launch_gemm(g, s);
+}
+
+cudaError_t dist_finalize(int n, const double* rec_p, const int* rec_q, double tol, const unsigned long long* smax,
+                          int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, cudaStream_t s) {
+  large::finalize_kernel<<<1, 1024, 0, s>>>(n, rec_p, rec_q, tol, smax, ipiv, logabsdet, sign, nullptr, info);
+  return cudaGetLastError();
+}
+
+cudaError_t dist_unpermute_plan(int n, int P, int rank, const int* pivstep, int* send_cols, int* recv_cols, int* counts,
+                                cudaStream_t s) {
+  if (P > dist::kMaxP) return cudaErrorInvalidValue;
+  dist::unpermute_plan_kernel<<<1, dist::kPlanThreads, 0, s>>>(n, P, rank, pivstep, send_cols, recv_cols, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t dist_unpermute_pack(int n, int P, int rank, const double* Xl, const int* rec_row, const int* send_cols,
+                                int m, double* sendbuf, cudaStream_t s) {
+  int npad, nl, nr;
+  dist_sizes(n, P, rank, &npad, &nl, &nr);
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  dim3 blk(32, 8), grd((m + 31) / 32 < 64 ? (m + 31) / 32 : 64, (n + 7) / 8);
+  dist::unpermute_pack_kernel<<<grd, blk, 0, s>>>(n, Xl, nl, rec_row, send_cols, m, sendbuf);
+  return cudaGetLastError();
+}
+
+cudaError_t dist_unpermute_unpack(int n, const double* recvbuf, const int* recv_cols, int m, double* Ainv_local,
+                                  int64_t ld, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  dim3 blk(32, 8), grd((m + 31) / 32 < 64 ? (m + 31) / 32 : 64, (n + 7) / 8);
+  dist::unpermute_unpack_kernel<<<grd, blk, 0, s>>>(n, recvbuf, recv_cols, m, Ainv_local, ld);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,90 @@
+"""GPU parity of the distributed large-n path (gj_dist_* through paper_1401_7962_b200/dist.py)
+on the one GPU available: world size 1 (the full path, its all-to-all degenerate) and world
+size 2 as two processes sharing cuda:0 over a gloo group (host-staged collectives, so the
+two ranks' kernels never wait on one another).  Against the oracle, the exact Hadamard pin
+and the single-GPU gj_invert (invariant P4)."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, P, n, kind, port, outdir):
+    import torch
+    import torch.distributed as tdist
+    from paper_1401_7962_b200.dist import invert_dist, local_columns
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=P, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        A = synth.gen_gaussian(n, seed=70 + n) if kind == "gauss" else synth.hadamard_pd(n, seed=5)[0]
+        cols = local_columns(n, P, rank)
+        A_local = torch.from_numpy(np.ascontiguousarray(A[:, cols])).cuda()
+        r = invert_dist(A_local, n)
+        torch.cuda.synchronize()
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), inv=r.inverse_local.cpu().numpy(), cols=np.array(cols),
+                 lg=r.logabsdet, sign=r.sign, info=r.info, ipiv=r.ipiv.cpu().numpy())
+    finally:
+        tdist.destroy_process_group()
+
+
+def run_dist(P, n, kind="gauss"):
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_worker, args=(P, n, kind, _free_port(), d), nprocs=P, join=True, start_method="spawn")
+        X = np.zeros((n, n))
+        outs = [np.load(os.path.join(d, f"r{r}.npz")) for r in range(P)]
+        for o in outs:
+            if len(o["cols"]):
+                X[:, o["cols"]] = o["inv"]
+        o0 = outs[0]
+        return X, float(o0["lg"]), int(o0["sign"]), int(o0["info"]), o0["ipiv"]
+
+
+def single(n, A):
+    import torch
+    import paper_1401_7962_b200 as gj
+    r = gj.invert(torch.from_numpy(A).cuda(), tol=n * 2.0 ** -52)
+    torch.cuda.synchronize()
+    return r.inverse.cpu().numpy(), float(r.logabsdet), int(r.sign), r.ipiv.cpu().numpy()
+
+
+@pytest.mark.parametrize("P,n", [(1, 300), (2, 300), (2, 1000), (1, 2048)])
+def test_dist_gaussian(P, n):
+    X, lg, sg, info, ipiv = run_dist(P, n)
+    A = synth.gen_gaussian(n, seed=70 + n)
+    ref = oracle.invert(A, tol=n * 2.0 ** -52)
+    kappa = oracle.kappa_inf(A, ref.inverse[0])[0]
+    e = np.abs(X - ref.inverse[0]).max() / np.abs(ref.inverse[0]).max()
+    assert info == 0
+    assert e <= max(1e-10, kappa * 2.0 ** -52), (e, kappa)
+    assert np.array_equal(ipiv, ref.ipiv[0])
+    assert sg == ref.sign[0]
+    assert abs(lg - ref.logabsdet[0]) <= max(1e-10, kappa * 2.0 ** -52)
+    # same pivots and (to rounding of a different GEMM blocking) the same inverse as 1 GPU
+    Xs, lgs, sgs, ipivs = single(n, A)
+    assert np.array_equal(ipiv, ipivs) and sg == sgs
+    assert np.abs(X - Xs).max() / np.abs(Xs).max() <= max(1e-12, kappa * 2.0 ** -52)
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_dist_hadamard_exact(P):
+    n = 1024
+    X, lg, sg, info, ipiv = run_dist(P, n, kind="hadamard")
+    A = synth.hadamard_pd(n, seed=5)[0]
+    assert np.array_equal(X, A.T / n)
+    assert abs(lg - (n / 2) * np.log(n)) <= 1e-9
