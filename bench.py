@@ -44,7 +44,11 @@ def parse():
     p.add_argument("--batch", type=int, default=BATCH, help="items per GPU (default: the C2 config)")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=65536, help="oracle sample size (items)")
+    p.add_argument("--cpu-sample", type=int, default=655360, help="oracle sample size (items, ~10 s of host work)")
+    p.add_argument("--no-c4", action="store_true", help="skip the secondary n=8192 fp64 measurement")
+    p.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                   help="c2: the headline batched line; c5: one fp64 32768^2 matrix, column-block-cyclic over the ranks")
+    p.add_argument("--n", type=int, default=32768, help="order for --workload c5")
     return p.parse_args()
 
 
@@ -131,11 +135,64 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(load)}
 
 
-def cpu_baseline(sample: int):
+def compute_peaks():
+    """FP64 tensor (DMMA) peak: measured on this pool's B200s (profiles/peaks_r01.json)."""
+    path = os.path.join(ROOT, "profiles", "peaks_r01.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["fp64_dmma_tflops"]), "measured (profiles/peaks_r01.json, tools/dmma_probe.cu mma.sync f64)"
+    return 37.2, "derived (148 SMs x 64 FP64 lanes x 2 x 1.965 GHz)"
+
+
+def c4_measure(dev, reps: int = 3):
+    """BASELINE configs[3]: one fp64 8192 x 8192 N(0,1)/sqrt(n) matrix (seed 3) through
+    gj_invert (panel kernel + DMMA trailing GEMMs); GFLOP/s for 2n^3 - n^2 flops."""
+    import torch
+    import paper_1401_7962_b200 as gj
+    import synth
+    n = 8192
+    A = torch.from_numpy(synth.gen_c4(n)).to(dev)
+    X = torch.empty_like(A)
+    ws_bytes = gj.lib.gj_workspace_size(1, n, 1, 1)
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+    outs = [torch.empty(n, dtype=torch.int32, device=dev), torch.empty(1, dtype=torch.float64, device=dev),
+            torch.empty(1, dtype=torch.int8, device=dev), torch.empty(1, dtype=torch.int32, device=dev)]
+    s = torch.cuda.current_stream(dev)
+
+    def run():
+        st = gj.lib.gj_invert(1, n, A.data_ptr(), n, X.data_ptr(), n, outs[0].data_ptr(), outs[1].data_ptr(),
+                              outs[2].data_ptr(), outs[3].data_ptr(), -1.0, ws.data_ptr(), ws_bytes, s.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    run()
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        run()
+        b.record(s)
+        torch.cuda.synchronize(dev)
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    fl = 2.0 * n ** 3 - n ** 2
+    peak, src = compute_peaks()
+    tf = fl / (ms / 1e3) / 1e12
+    return {"workload": "C4: one fp64 8192x8192 N(0,1)/sqrt(n), seed 3 (BASELINE.json configs[3])",
+            "metric": "fp64 GFLOP/s at n=8192", "value": tf * 1e3, "unit": "GFLOP/s", "ms": ms, "reps": reps,
+            "logabsdet": float(outs[1].item()), "sign": int(outs[2].item()), "info": int(outs[3].item()),
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                         "traffic": None, "peak_source": src,
+                         "kernel": "whole gj_invert (leaf_kernel panels overlapped with gemm_update_kernel DMMA)"}}
+
+
+def cpu_baseline(sample: int, A_host=None):
     """The oracle as it stands, on the host's cores, on the first `sample` items of C2."""
     import oracle
     import synth
-    A = synth.gen_c2(batch=sample)
+    A = A_host[:sample] if A_host is not None and len(A_host) >= sample else synth.gen_c2(batch=sample)
     nth = oracle.threads()
     t0 = time.perf_counter()
     oracle.invert_batched(A, tol=N * 2.0 ** -23, nthreads=nth)
@@ -172,11 +229,77 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_c5(args, rank, world, local):
+    """BASELINE configs[4]: one fp64 n x n N(0,1)/sqrt(n) matrix (seed 4), column-block-cyclic
+    over the ranks (paper_1401_7962_b200/dist.py; NCCL broadcast of each factored panel).
+    Rank 0 generates A and broadcasts it; every rank keeps its own columns."""
+    import torch
+    import torch.distributed as tdist
+    from paper_1401_7962_b200.dist import invert_dist, local_columns
+    import synth
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not tdist.is_initialized():
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+        tdist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    n = args.n
+    A = torch.empty((n, n), dtype=torch.float64, device=dev)
+    if rank == 0:
+        A.copy_(torch.from_numpy(synth.gen_c5(n) if n == 32768 else synth.gen_gaussian(n, seed=4)))
+    tdist.broadcast(A, 0)
+    cols = local_columns(n, world, rank)
+    A_local = A[:, cols].contiguous()
+    del A
+    torch.cuda.empty_cache()
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        tdist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        invert_dist(A_local, n)
+    times, res = [], None
+    for _ in range(args.steps):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = invert_dist(A_local, n)
+        b.record()
+        barrier()
+        times.append(a.elapsed_time(b))
+    t = torch.tensor([float(np.mean(times))], device=dev, dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    fl = 2.0 * n ** 3 - n ** 2
+    peak, src = compute_peaks()
+    tf = fl / (ms / 1e3) / 1e12
+    if rank == 0:
+        print(json.dumps({"metric": f"fp64 GFLOP/s at n={n} (distributed)", "value": tf * 1e3, "unit": "GFLOP/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic",
+                          "config": {"workload": f"C5: one fp64 {n}x{n} N(0,1)/sqrt(n), seed 4, column-block-cyclic "
+                                                 f"(block 128) over {world} GPU(s) (BASELINE.json configs[4])",
+                                     "parallelism": f"column-block-cyclic x{world}, NCCL panel broadcast"},
+                          "roofline": {"bound": "tensor", "achieved": tf, "peak": peak * world, "unit": "TFLOP/s",
+                                       "frac": tf / (peak * world), "traffic": None, "peak_source": src + f" x {world}"},
+                          "logabsdet": res.logabsdet, "sign": res.sign, "info": res.info,
+                          "gpu_launches": None}), flush=True)
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.workload == "c5":
+        run_c5(args, rank, world, local)
         return
     import torch
     import paper_1401_7962_b200 as gj
@@ -284,8 +407,10 @@ def main():
                            "l2": "inputs (4 GiB/GPU) larger than L2 (126 MB); no flush needed",
                            "outputs": "inverse, logabsdet, sign"},
                 "roofline": roof, "gpu_launches": args.steps, "clocks": clk.summary(), "e2e": e2e}
+        if not args.no_c4:
+            line["secondary"] = c4_measure(dev)
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
+            line["cpu_baseline"] = cpu_baseline(args.cpu_sample, A_host)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()
