@@ -524,51 +524,88 @@ gj_batched_warp_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
 // whole pivot row (8 predicated STS.128 per slot, 4 smem cycles each whatever the lane
 // count; tools/ubench/smem_bench.cu) bounded the unblocked K1; here it happens once per
 // block.  Tie-break, logical swaps, record and epilogue are K1's.
-constexpr int kBlkStage = 64 * 128;   // one TMA stage: 2 matrices x 32 rows x 128 B
+// R rows per lane (R = 2: 16 lanes and 2 matrices per warp; R = 4: 8 lanes and 4
+// matrices per warp: every shared-memory read of the trailing update then feeds four rows).
+template <int R>
+struct BlkGeo {
+  static constexpr int L = 32 / R;       // lanes per matrix
+  static constexpr int M = R;            // matrices per warp task
+  static constexpr int ROWS = 32 * M;    // rows per warp task
+  static constexpr int STAGE = ROWS * 128;
+};
 
-template <int BS>
+template <int R, int BS>
 struct BlkMisc {
   static constexpr int RW = 32 - BS;
-  static constexpr int RBUF = 2 * BS * RW * 4;   // [matrix][block step][RW] pivot-row tails
-  static constexpr int REC = 2 * 32 * 8;         // [matrix][step] (p, q)
-  static constexpr int PERM = 2 * 32 * 4;
+  static constexpr int RBUF = BlkGeo<R>::M * BS * RW * 4;   // [matrix][block step][RW] pivot-row tails
+  static constexpr int REC = BlkGeo<R>::M * 32 * 8;         // [matrix][step] (p, q)
+  static constexpr int PERM = BlkGeo<R>::M * 32 * 4;
   static constexpr int BYTES = RBUF + REC + PERM + 16;
-  static constexpr int smem(int nst) { return kWarpsPerBlock * (nst * kBlkStage + BYTES) + 1024; }
+  static constexpr int smem(int nst) { return kWarpsPerBlock * (nst * BlkGeo<R>::STAGE + BYTES) + 1024; }
 };
+
+// group reductions over the L lanes of a matrix
+template <int R>
+__device__ __forceinline__ uint32_t blk_gmax(uint32_t v, int g) {
+  return group_max_u32<BlkGeo<R>::M, BlkGeo<R>::L>(v, g);
+}
+template <int R>
+__device__ __forceinline__ uint32_t blk_gmin(uint32_t v, int g) {
+  return group_min_u32<BlkGeo<R>::M, BlkGeo<R>::L>(v, g);
+}
 
 // One panel step s (static) at global step k on the panel registers P (branch-free, so
 // that a whole block stays one basic block and the scheduler can interleave the previous
 // block's trailing update into the latency of this chain).
-template <int BS>
-__device__ __forceinline__ void blk_panel_step(const int s, const int k, float (&P)[2][BS], uint32_t (&kmask)[2],
-                                               int (&pos)[2], int (&bs)[2], unsigned char* rec_g, int li, int g,
+template <int R, int BS>
+__device__ __forceinline__ void blk_panel_step(const int s, const int k, float (&P)[R][BS], uint32_t (&kmask)[R],
+                                               int (&pos)[R], int (&bs)[R], unsigned char* rec_g, int li, int g,
                                                int lane) {
+  constexpr int SB = R == 2 ? 1 : 2;   // slot bits in the winner code
   // a2: max |x_ik| over the un-pivoted rows (IEEE bit pattern of |x|, monotone)
-  const uint32_t key0 = __float_as_uint(P[0][s]) & kmask[0];
-  const uint32_t key1 = __float_as_uint(P[1][s]) & kmask[1];
-  const uint32_t m = group_max_u32<2, 16>(max(key0, key1), g);
+  uint32_t key[R];
+  uint32_t km = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    key[r] = __float_as_uint(P[r][s]) & kmask[r];
+    km = max(km, key[r]);
+  }
+  const uint32_t m = blk_gmax<R>(km, g);
   // |1/p| and the unsigned multipliers start while the tie-break runs (|p| = m exactly)
   const float ra = rcp(__uint_as_float(m));
-  const float t0 = P[0][s] * ra, t1 = P[1][s] * ra;
+  float t[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) t[r] = P[r][s] * ra;
   // ties -> smallest physical position (G3); the winner code carries (position, lane, slot)
-  const uint32_t c0 = (key0 == m && kmask[0] != 0u) ? ((uint32_t)pos[0] << 6 | (uint32_t)lane << 1) : 0xffffu;
-  const uint32_t c1 = (key1 == m && kmask[1] != 0u) ? ((uint32_t)pos[1] << 6 | (uint32_t)lane << 1 | 1u) : 0xffffu;
-  const uint32_t win = group_min_u32<2, 16>(min(c0, c1), g);
-  const int q = (int)(win >> 6);
-  const int src = (int)((win >> 1) & 31u);
-  const bool slot1 = (win & 1u) != 0u;
-  const bool pv0 = pos[0] == q, pv1 = pos[1] == q;
+  uint32_t cmin = 0xffffffu;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t c = (key[r] == m && kmask[r] != 0u)
+                           ? ((uint32_t)pos[r] << (5 + SB) | (uint32_t)lane << SB | (uint32_t)r) : 0xffffffu;
+    cmin = min(cmin, c);
+  }
+  const uint32_t win = blk_gmin<R>(cmin, g);
+  const int q = (int)(win >> (5 + SB));
+  const int src = (int)((win >> SB) & 31u);
+  const int slot = (int)(win & ((1u << SB) - 1u));
+  bool pv[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) pv[r] = pos[r] == q;
   // the pivot row's panel values (one shuffle each from the pivot lane)
   float z[BS];
 #pragma unroll
-  for (int j = 0; j < BS; ++j) z[j] = __shfl_sync(0xffffffffu, slot1 ? P[1][j] : P[0][j], src);
+  for (int j = 0; j < BS; ++j) {
+    float v = P[0][j];
+#pragma unroll
+    for (int r = 1; r < R; ++r) v = slot == r ? P[r][j] : v;
+    z[j] = __shfl_sync(0xffffffffu, v, src);
+  }
   const float p = z[s];
   const uint32_t psign = __float_as_uint(p) & 0x80000000u;
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const bool pv = r ? pv1 : pv0;
+  for (int r = 0; r < R; ++r) {
     // a5 on the panel: Eq. (15) with the deferred pivot-row scale, multiplier x_ik / p
-    const float nf = pv ? 0.0f : __uint_as_float((__float_as_uint(r ? t1 : t0) ^ psign) ^ 0x80000000u);
+    const float nf = pv[r] ? 0.0f : __uint_as_float((__float_as_uint(t[r]) ^ psign) ^ 0x80000000u);
 #pragma unroll
     for (int j = 0; j < BS; j += 2) {
       if (j == s) {
@@ -580,21 +617,21 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
       }
     }
     P[r][s] = nf;   // compact D entry; 0 on the pivot row (W - S: its 1 is held as 0)
-    kmask[r] = pv ? 0u : kmask[r];
-    bs[r] = pv ? s : bs[r];
+    kmask[r] = pv[r] ? 0u : kmask[r];
+    bs[r] = pv[r] ? s : bs[r];
     // a3: the listing's swap of positions k and q (L156-L162), positions only
     pos[r] = (pos[r] == k) ? q : pos[r];
-    pos[r] = pv ? k : pos[r];
+    pos[r] = pv[r] ? k : pos[r];
   }
   if (li == 0) rec_store(rec_g, k, p, q);
 }
 
 // Publish the block's pivot rows: their other RW values T (unchanged since the block began).
-template <int BS>
-__device__ __forceinline__ void blk_publish(const float (&T)[2][32 - BS], const int (&bs)[2], float* rbuf_g) {
+template <int R, int BS>
+__device__ __forceinline__ void blk_publish(const float (&T)[R][32 - BS], const int (&bs)[R], float* rbuf_g) {
   constexpr int RW = 32 - BS;
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < R; ++r) {
     const uint32_t dst = smem_u32(rbuf_g) + (uint32_t)(bs[r] < 0 ? 0 : bs[r]) * (RW * 4);
 #pragma unroll
     for (int j = 0; j < RW; j += 4)
@@ -603,45 +640,45 @@ __device__ __forceinline__ void blk_publish(const float (&T)[2][32 - BS], const 
 }
 
 // Rank-1 term s of the trailing update on columns [J0, J1) of T: T += (W - S)[:, s] R_s.
-template <int BS, int J0, int J1, int N>
-__device__ __forceinline__ void blk_trail_term(float (&T)[2][N], const float (&P)[2][BS], int s, const float* rbuf_g,
+template <int R, int BS, int J0, int J1, int N>
+__device__ __forceinline__ void blk_trail_term(float (&T)[R][N], const float (&P)[R][BS], int s, const float* rbuf_g,
                                                int tofs) {
   constexpr int RW = 32 - BS;
   float Rs[J1 - J0];
   ld_row<float, J1 - J0>(Rs, rbuf_g + s * RW + J0);
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int j = 0; j < J1 - J0; j += 2) ffma2(T[r][tofs + j], T[r][tofs + j + 1], P[r][s], Rs[j], Rs[j + 1]);
 }
 
 // NST = TMA stages per warp: 2 = the next task streams in during this one; 1 = half the
 // shared memory (more resident warps), the next task is prefetched into L2 instead.
-template <int BS, int NST>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, NST == 1 ? 4 : 3)
+template <int R, int BS, int NST>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, R == 4 ? 2 : (NST == 1 ? 4 : 3))
 gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
-  using M = BlkMisc<BS>;
-  constexpr int RW = M::RW;
-  using TL = TmaLayout<float, 32>;
+  using Geo = BlkGeo<R>;
+  using M = BlkMisc<R, BS>;
+  constexpr int RW = M::RW, L = Geo::L, MT = Geo::M;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   unsigned char* sbase = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* stage0 = sbase + warp * NST * kBlkStage;
-  unsigned char* misc = sbase + kWarpsPerBlock * NST * kBlkStage + warp * M::BYTES;
+  unsigned char* stage0 = sbase + warp * NST * Geo::STAGE;
+  unsigned char* misc = sbase + kWarpsPerBlock * NST * Geo::STAGE + warp * M::BYTES;
   float* rbuf = reinterpret_cast<float*>(misc);
   unsigned char* rec = misc + M::RBUF;
   int* permS = reinterpret_cast<int*>(rec + M::REC);
   uint64_t* bars = reinterpret_cast<uint64_t*>(misc + M::RBUF + M::REC + M::PERM);
 
-  const int g = lane >> 4;
-  const int li = lane & 15;
-  const unsigned gmask = 0xffffu << (16 * g);
+  const int g = lane / L;
+  const int li = lane % L;
+  const unsigned gmask = (L == 32 ? 0xffffffffu : ((1u << L) - 1u)) << (L * g);
   float* rbuf_g = rbuf + g * BS * RW;
   unsigned char* rec_g = rec + g * 32 * 8;
   int* perm_g = permS + g * 32;
 
-  const int64_t ntasks = (a.batch + 1) / 2;
+  const int64_t ntasks = (a.batch + MT - 1) / MT;
   const int64_t wstride = (int64_t)gridDim.x * kWarpsPerBlock;
   const int64_t task0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
 
@@ -652,34 +689,34 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
   }
   __syncwarp();
   if (lane == 0 && task0 < ntasks) {
-    mbar_expect_tx(&bars[0], TL::BYTES);
-    tma_load_2d(stage0, &tm.a, 0, (int)(task0 * 64), &bars[0]);
+    mbar_expect_tx(&bars[0], Geo::STAGE);
+    tma_load_2d(stage0, &tm.a, 0, (int)(task0 * Geo::ROWS), &bars[0]);
   }
 
   int it = 0;
   for (int64_t task = task0; task < ntasks; task += wstride, ++it) {
-    const int64_t item0 = task * 2;
+    const int64_t item0 = task * MT;
     const bool item_ok = item0 + g < a.batch;
-    unsigned char* stage = stage0 + (NST == 2 ? (it & 1) * kBlkStage : 0);
+    unsigned char* stage = stage0 + (NST == 2 ? (it & 1) * Geo::STAGE : 0);
     const int64_t nxt = task + wstride;
     if constexpr (NST == 2) {
       if (lane == 0 && nxt < ntasks) {
-        unsigned char* ns = stage0 + ((it + 1) & 1) * kBlkStage;
+        unsigned char* ns = stage0 + ((it + 1) & 1) * Geo::STAGE;
         bulk_wait_read0();
-        mbar_expect_tx(&bars[(it + 1) & 1], TL::BYTES);
-        tma_load_2d(ns, &tm.a, 0, (int)(nxt * 64), &bars[(it + 1) & 1]);
+        mbar_expect_tx(&bars[(it + 1) & 1], Geo::STAGE);
+        tma_load_2d(ns, &tm.a, 0, (int)(nxt * Geo::ROWS), &bars[(it + 1) & 1]);
       }
       mbar_wait_warp(&bars[it & 1], (it >> 1) & 1);
     } else {
       if (lane == 0 && nxt < ntasks)
-        bulk_prefetch_l2(static_cast<const float*>(a.A) + nxt * 64 * 32, TL::BYTES);
+        bulk_prefetch_l2(static_cast<const float*>(a.A) + nxt * Geo::ROWS * 32, Geo::STAGE);
       mbar_wait_warp(&bars[0], it & 1);
     }
-    // ---- a1: rows li and li + 16 of matrix g into registers ----
-    float x[2][32];
+    // ---- a1: rows li + L r of matrix g into registers ----
+    float x[R][32];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int row = li + 16 * r;
+    for (int r = 0; r < R; ++r) {
+      const int row = li + L * r;
       stage_ld_row<float, 32, true>(x[r], stage, g * 32 + row);
       if (!item_ok) {
 #pragma unroll
@@ -689,50 +726,52 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     __syncwarp();
     float rowmax = 0.0f;
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int j = 0; j < 32; ++j) rowmax = fmaxf(rowmax, fabsf(x[r][j]));
-    const double smax = (double)__uint_as_float(group_max_u32<2, 16>(__float_as_uint(rowmax), g));
+    const double smax = (double)__uint_as_float(blk_gmax<R>(__float_as_uint(rowmax), g));
     const float tau = round_down_to(a.tol * smax, 0.0f);
 
-    uint32_t kmask[2] = {0x7fffffffu, 0x7fffffffu};
-    int pos[2] = {li, li + 16};
+    uint32_t kmask[R];
+    int pos[R], bs[R];
     // P: panel columns of the current block; T: the other 32 - BS columns, rotated so
     // that T[0..BS) is the next panel and the finished compact D columns sit at the end
-    float P[2][BS], T[2][RW];
+    float P[R][BS], T[R][RW];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < R; ++r) {
+      kmask[r] = 0x7fffffffu;
+      pos[r] = li + L * r;
+      bs[r] = -1;
 #pragma unroll
       for (int j = 0; j < BS; ++j) P[r][j] = x[r][j];
 #pragma unroll
       for (int j = 0; j < RW; ++j) T[r][j] = x[r][BS + j];
     }
-    int bs[2] = {-1, -1};
 #pragma unroll
-    for (int s = 0; s < BS; ++s) blk_panel_step<BS>(s, s, P, kmask, pos, bs, rec_g, li, g, lane);
+    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS>(s, s, P, kmask, pos, bs, rec_g, li, g, lane);
     // look-ahead: per iteration, publish block kb's pivot rows, apply its update to the
     // next panel first, then factor that panel while the rest of block kb's update runs
 #pragma unroll 1
     for (int kb = 0; kb + BS < 32; kb += BS) {
-      blk_publish<BS>(T, bs, rbuf_g);
+      blk_publish<R, BS>(T, bs, rbuf_g);
       __syncwarp();
-      float NP[2][BS];
+      float NP[R][BS];
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int j = 0; j < BS; ++j) NP[r][j] = T[r][j];
 #pragma unroll
-      for (int s = 0; s < BS; ++s) blk_trail_term<BS, 0, BS, BS>(NP, P, s, rbuf_g, 0);
-      bs[0] = -1;
-      bs[1] = -1;
+      for (int s = 0; s < BS; ++s) blk_trail_term<R, BS, 0, BS, BS>(NP, P, s, rbuf_g, 0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) bs[r] = -1;
 #pragma unroll
       for (int s = 0; s < BS; ++s) {
-        blk_panel_step<BS>(s, kb + BS + s, NP, kmask, pos, bs, rec_g, li, g, lane);
-        blk_trail_term<BS, BS, RW, RW>(T, P, s, rbuf_g, BS);
+        blk_panel_step<R, BS>(s, kb + BS + s, NP, kmask, pos, bs, rec_g, li, g, lane);
+        blk_trail_term<R, BS, BS, RW, RW>(T, P, s, rbuf_g, BS);
       }
       __syncwarp();   // every lane has read rbuf before the next publish
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < R; ++r) {
 #pragma unroll
         for (int j = 0; j < RW - BS; ++j) T[r][j] = T[r][j + BS];
 #pragma unroll
@@ -743,12 +782,12 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
       }
     }
     // last block: its whole update, then x = [T | P] (register j = compact column j)
-    blk_publish<BS>(T, bs, rbuf_g);
+    blk_publish<R, BS>(T, bs, rbuf_g);
     __syncwarp();
 #pragma unroll
-    for (int s = 0; s < BS; ++s) blk_trail_term<BS, 0, RW, RW>(T, P, s, rbuf_g, 0);
+    for (int s = 0; s < BS; ++s) blk_trail_term<R, BS, 0, RW, RW>(T, P, s, rbuf_g, 0);
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < R; ++r) {
 #pragma unroll
       for (int j = 0; j < RW; ++j) x[r][j] = T[r][j];
 #pragma unroll
@@ -756,13 +795,13 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     }
 
     // ---- a6: det / ipiv / singular flag from the per-step record ----
-    float myrp[2];
+    float myrp[R];
     unsigned failb = 0;
     int nswap = 0, nneg = 0;
     double lgl = 0.0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int row = li + 16 * r;
+    for (int r = 0; r < R; ++r) {
+      const int row = li + L * r;
       float p_own, p_k;
       int q_own, q_k;
       rec_load(rec_g, pos[r], p_own, q_own);
@@ -770,14 +809,14 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
       (void)q_own;
       myrp[r] = rcp(p_own);
       const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau) & gmask;
-      if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * 16 + r * 16);
+      if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * L + r * L);
       nswap += __popc(__ballot_sync(0xffffffffu, q_k != row) & gmask);
       nneg += __popc(__ballot_sync(0xffffffffu, p_k < 0.0f) & gmask);
       lgl += log_abs(p_k);
       if (a.ipiv && item_ok) a.ipiv[(item0 + g) * 32 + row] = q_k + 1;
     }
     const int info = (int)failb;
-    const double lg = group_sum<16>(lgl);
+    const double lg = group_sum<L>(lgl);
     const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
     if (item_ok && li == 0) {
       const int64_t item = item0 + g;
@@ -790,10 +829,10 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     // ---- a7 + a8: un-permuted store through the staging buffer ----
     if (a.Ainv != nullptr) {
 #pragma unroll
-      for (int r = 0; r < 2; ++r) perm_g[pos[r]] = (li + 16 * r) * 4;   // output column (bytes)
+      for (int r = 0; r < R; ++r) perm_g[pos[r]] = (li + L * r) * 4;   // output column (bytes)
       __syncwarp();
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < R; ++r) {
         const RowAddr<float, 32, true> dst(g * 32 + pos[r]);
 #pragma unroll
         for (int kp = 0; kp < 32; kp += 4) {
@@ -803,13 +842,13 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
           for (int u = 0; u < 4; ++u) *reinterpret_cast<float*>(stage + dst.at_b((uint32_t)cbs[u])) = myrp[r] * x[r][kp + u];
         }
         // the row's own compact entry was held as W - 1 (see above): add the 1 back
-        float* own = reinterpret_cast<float*>(stage + dst.at_b((uint32_t)((li + 16 * r) * 4)));
+        float* own = reinterpret_cast<float*>(stage + dst.at_b((uint32_t)((li + L * r) * 4)));
         *own = *own + myrp[r];
       }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(&tm.x, 0, (int)(task * 64), stage);
+        tma_store_2d(&tm.x, 0, (int)(task * Geo::ROWS), stage);
         bulk_commit();
       }
     }
@@ -817,18 +856,18 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     if constexpr (NST == 1) {
       if (lane == 0 && nxt < ntasks) {
         bulk_wait_read0();   // the store has read the stage
-        mbar_expect_tx(&bars[0], TL::BYTES);
-        tma_load_2d(stage0, &tm.a, 0, (int)(nxt * 64), &bars[0]);
+        mbar_expect_tx(&bars[0], Geo::STAGE);
+        tma_load_2d(stage0, &tm.a, 0, (int)(nxt * Geo::ROWS), &bars[0]);
       }
     }
   }
   if (lane == 0) bulk_wait0();
 }
 
-template <int BS, int NST>
+template <int R, int BS, int NST>
 cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
-  const size_t smem = BlkMisc<BS>::smem(NST);
-  auto kern = gj_blk32_kernel<BS, NST>;
+  const size_t smem = BlkMisc<R, BS>::smem(NST);
+  auto kern = gj_blk32_kernel<R, BS, NST>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -839,7 +878,7 @@ cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const int64_t ntasks = (a.batch + 1) / 2;
+  const int64_t ntasks = (a.batch + R - 1) / R;
   const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int64_t cap = (int64_t)device_sm_count() * per_sm;
   const int grid = (int)(need < cap ? need : cap);
@@ -856,6 +895,17 @@ int k1_block_size() {
     if (const char* e = getenv("GJ_K1_BLOCK")) {
       const int t = atoi(e);
       if (t == 0 || t == 4 || t == 8) v = t;
+    }
+  }
+  return v;
+}
+int k1_rows() {
+  static int v = -1;
+  if (v < 0) {
+    v = 2;
+    if (const char* e = getenv("GJ_K1_ROWS")) {
+      const int t = atoi(e);
+      if (t == 2 || t == 4) v = t;
     }
   }
   return v;
@@ -908,16 +958,26 @@ cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
     const bool f64 = sizeof(T) == 8;
     const uint64_t rows = (uint64_t)a.batch * NP;
     const int swz = TL::SPAN >= 32 ? TL::SPAN : 0;
+    if constexpr (NP == 32 && sizeof(T) == 4) {
+      // K1b (blocked): box of 32 * R rows (R matrices per warp task)
+      const int bsz = k1_block_size();
+      const int R = k1_rows();
+      if (full && aligned && rows_ok && bsz != 0) {
+        const uint32_t box_rows = 32u * R;
+        if (make_tma_map_2d(&maps.a, false, a.A, 32, rows, 128, 32, box_rows, 128) &&
+            (a.Ainv == nullptr || make_tma_map_2d(&maps.x, false, a.Ainv, 32, rows, 128, 32, box_rows, 128))) {
+          if (a.Ainv == nullptr) maps.x = maps.a;
+          const bool one = k1_stages() == 1;
+          if (R == 4) return bsz == 8 ? launch_blk32<4, 8, 1>(a, maps, s) : launch_blk32<4, 4, 1>(a, maps, s);
+          if (bsz == 8) return one ? launch_blk32<2, 8, 1>(a, maps, s) : launch_blk32<2, 8, 2>(a, maps, s);
+          return one ? launch_blk32<2, 4, 1>(a, maps, s) : launch_blk32<2, 4, 2>(a, maps, s);
+        }
+      }
+    }
     if (full && aligned && rows_ok &&
         make_tma_map_2d(&maps.a, f64, a.A, NP, rows, NP * sizeof(T), TL::BOX_COLS, TL::ROWS, swz) &&
         (a.Ainv == nullptr || make_tma_map_2d(&maps.x, f64, a.Ainv, NP, rows, NP * sizeof(T), TL::BOX_COLS, TL::ROWS, swz))) {
       if (a.Ainv == nullptr) maps.x = maps.a;
-      if constexpr (NP == 32 && sizeof(T) == 4) {
-        const int bsz = k1_block_size();
-        const bool one = k1_stages() == 1;
-        if (bsz == 8) return one ? launch_blk32<8, 1>(a, maps, s) : launch_blk32<8, 2>(a, maps, s);
-        if (bsz == 4) return one ? launch_blk32<4, 1>(a, maps, s) : launch_blk32<4, 2>(a, maps, s);
-      }
       return launch_warp<T, NP, true>(a, maps, s);
     }
   }
