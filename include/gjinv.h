@@ -168,10 +168,15 @@ gj_status gj_dist_init(int n, int nranks, int rank, const double* A_local, int64
 gj_status gj_dist_factor(int n, int nranks, int rank, int k, double* X_local, int32_t* pos, int32_t* pivstep,
                          double* rec_p, int32_t* rec_q, int32_t* rec_row, double* W, void* stream);
 
-/* Every rank, after the broadcast of panel k: X_local[:, c] += (W - S) R for every local
- * column c outside panel k (R = the panel's pivot rows of X_local, staged in R). */
-gj_status gj_dist_update(int n, int nranks, int rank, int k, double* X_local, const double* W, const int32_t* pivstep,
-                         const int32_t* rec_row, double* R, void* stream);
+/* Every rank, after the broadcast of panel k: X_local[:, c] += (W - S) R for the local
+ * columns c outside panel k (R = the panel's pivot rows of X_local, staged in R).
+ *   part 0: all of them (gathers R first);
+ *   part 1: only the local columns of panel k+1 (gathers R first; the rank must own k+1);
+ *   part 2: the rest, after part 1 and gj_dist_factor(k+1) on the same stream: launched as
+ *           a programmatic dependent of that factorisation so the two overlap (look-ahead).
+ * Parts 1 and 2 need (k+1) % nranks == rank. */
+gj_status gj_dist_update(int n, int nranks, int rank, int k, int part, double* X_local, const double* W,
+                         const int32_t* pivstep, const int32_t* rec_row, double* R, void* stream);
 
 /* log|det|, sign, info and ipiv from the replicated record (Eq. (13) + G4); tol as
  * gj_invert (< 0: n * eps). Any rank; outputs may be NULL. */

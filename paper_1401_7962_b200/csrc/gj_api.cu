@@ -199,15 +199,18 @@ gj_status gj_dist_factor(int n, int nranks, int rank, int k, double* X_local, in
                      static_cast<cudaStream_t>(stream)) == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_dist_update(int n, int nranks, int rank, int k, double* X_local, const double* W, const int32_t* pivstep,
-                         const int32_t* rec_row, double* R, void* stream) {
-  if (!dist_args_ok(n, nranks, rank) || !W || !pivstep || !rec_row) return GJ_ERR_ARG;
+gj_status gj_dist_update(int n, int nranks, int rank, int k, int part, double* X_local, const double* W,
+                         const int32_t* pivstep, const int32_t* rec_row, double* R, void* stream) {
+  if (!dist_args_ok(n, nranks, rank) || !W || !pivstep || !rec_row || part < 0 || part > 2) return GJ_ERR_ARG;
   int npad, nl, nr;
   dist_sizes(n, nranks, rank, &npad, &nl, &nr);
-  if (k < 0 || k >= npad / GJ_DIST_BLOCK) return GJ_ERR_ARG;
+  const int nb = npad / GJ_DIST_BLOCK;
+  if (k < 0 || k >= nb) return GJ_ERR_ARG;
+  if (part > 0 && (k + 1 >= nb || (k + 1) % nranks != rank)) return GJ_ERR_ARG;
+  if (part == 2 && k % nranks == rank && nranks != 1) return GJ_ERR_ARG;
   if (nl > 0 && (!X_local || !R)) return GJ_ERR_ARG;
-  return dist_update(n, nranks, rank, k, X_local, W, pivstep, rec_row, R, static_cast<cudaStream_t>(stream)) == cudaSuccess
-             ? GJ_OK : GJ_ERR_CUDA;
+  return dist_update(n, nranks, rank, k, part, X_local, W, pivstep, rec_row, R, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
 gj_status gj_dist_finalize(int n, const double* rec_p, const int32_t* rec_q, double tol, const uint64_t* smax_bits,

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "gj_internal.h"
 #include "gj_ptx.cuh"
@@ -378,10 +379,24 @@ cudaError_t dispatch64(const BatchedArgs& a, cudaStream_t s) {
   return launch64<T, false>(a, maps, s);
 }
 
+// fp64 n = 64: 1 = column-split blocked K2b (default), 0 = K2 (GJ_K2_VARIANT, A/B only)
+int k2_variant() {
+  static int v = -1;
+  if (v < 0) {
+    v = 1;
+    if (const char* e = getenv("GJ_K2_VARIANT")) v = atoi(e) == 0 ? 0 : 1;
+  }
+  return v;
+}
+
 }  // namespace
 
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s) {
   if (a.batch == 0) return cudaSuccess;
+  if (dt == GJ_F64 && a.n == 64 && k2_variant() == 1) {
+    const cudaError_t e = launch_batched64b(a, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   return dt == GJ_F32 ? dispatch64<float>(a, s) : dispatch64<double>(a, s);
 }
 

@@ -24,6 +24,8 @@ struct BatchedArgs {
 // Return cudaSuccess or the launch error.
 cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
+// K2b, fp64 n = 64 (gj_batched64b.cu); cudaErrorNotSupported if the buffers do not suit it.
+cudaError_t launch_batched64b(const BatchedArgs& a, cudaStream_t s);
 
 // Large-n blocked path (gj_large.cu), fp64, one matrix; Ainv may be null (det only).
 size_t large_workspace_size(int n);
@@ -37,7 +39,7 @@ cudaError_t dist_init(int n, int P, int rank, const double* A_local, int64_t lda
                       unsigned long long* smax, cudaStream_t s);
 cudaError_t dist_factor(int n, int P, int rank, int k, double* Xl, int* pos, int* pivstep, double* rec_p, int* rec_q,
                         int* rec_row, double* W, cudaStream_t s);
-cudaError_t dist_update(int n, int P, int rank, int k, double* Xl, const double* W, const int* pivstep,
+cudaError_t dist_update(int n, int P, int rank, int k, int part, double* Xl, const double* W, const int* pivstep,
                         const int* rec_row, double* R, cudaStream_t s);
 cudaError_t dist_finalize(int n, const double* rec_p, const int* rec_q, double tol, const unsigned long long* smax,
                           int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, cudaStream_t s);

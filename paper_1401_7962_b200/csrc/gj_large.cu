@@ -170,6 +170,7 @@ struct LeafArgs {
   double* rec_p;     // [npad] pivot value per step
   int* rec_q;        // [npad] pivot's physical position per step
   int* rec_row;      // [npad] pivot row per step
+  double* Wout;      // if non-null: the factored panel, npad x pw (ld pw), written at the end
 };
 
 constexpr int kLeafThreads = 512;
@@ -478,6 +479,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     if (!valid[i]) continue;
     a.pos[rowid[i]] = pos[i];
     a.pivstep[rowid[i]] = pst[i];
+    if (a.Wout != nullptr) {   // this thread wrote every final panel value of its rows itself
+      const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)rowid[i] * ld + P0);
+      double2* dst = reinterpret_cast<double2*>(a.Wout + (int64_t)rowid[i] * pw);
+      for (int j = 0; j < pw / 2; ++j) dst[j] = src[j];
+    }
   }
   cluster_sync_all();   // no CTA leaves while a peer's bulk copy may still target it
 }
@@ -788,7 +794,7 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
   // Look-ahead over panels: panel k+1 is updated by panel k first and factored by the
   // cluster kernel while the rest of panel k's update runs on the other SMs.
   auto factor_panel = [&](int P0, int pw) -> cudaError_t {
-    LeafArgs la{w.X, npad, npad, P0, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row};
+    LeafArgs la{w.X, npad, npad, P0, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
     if (lc.w == 32) return launch_leaf<32, 1>(la, lc.cl, s);
     if (lc.w == 16) return launch_leaf<16, 2>(la, lc.cl, s);
     return launch_leaf<8, 4>(la, lc.cl, s);
@@ -860,15 +866,6 @@ __global__ void init_local_kernel(const double* __restrict__ A, int64_t lda, int
     b = ob > b ? ob : b;
   }
   if ((threadIdx.x & 31) == 0) atomicMax(smax, b);
-}
-
-// W (npad x DB, ld DB) = X[:, c0 .. c0 + DB)
-__global__ void copy_panel_kernel(const double* __restrict__ X, int64_t ld, int npad, int c0, double* __restrict__ W) {
-  const int64_t tot = (int64_t)npad * (DB / 2);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / (DB / 2)), c = (int)(e - (int64_t)i * (DB / 2));
-    reinterpret_cast<double2*>(W + (int64_t)i * DB)[c] = reinterpret_cast<const double2*>(X + (int64_t)i * ld + c0)[c];
-  }
 }
 
 // Exchange plan of the un-permutation Ainv[i][j] = X[rec_row[i]][pivstep[j]] (one CTA):
@@ -992,29 +989,54 @@ cudaError_t dist_factor(int n, int P, int rank, int k, double* Xl, int* pos, int
   LeafCfg lc;
   if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
   const int c0 = (k / P) * dist::DB;
-  LeafArgs la{Xl, nl, npad, c0, k * dist::DB, dist::DB, pos, pivstep, rec_p, rec_q, rec_row};
-  cudaError_t e = lc.w == 32 ? launch_leaf<32, 1>(la, lc.cl, s)
-                  : lc.w == 16 ? launch_leaf<16, 2>(la, lc.cl, s)
-                               : launch_leaf<8, 4>(la, lc.cl, s);
-  if (e != cudaSuccess) return e;
-  dist::copy_panel_kernel<<<device_sm_count() * 4, 256, 0, s>>>(Xl, nl, npad, c0, W);
-  return cudaGetLastError();
+  // the panel kernel also writes W itself, so a following programmatic-dependent GEMM
+  // (gj_dist_update part 2) overlaps it directly
+  LeafArgs la{Xl, nl, npad, c0, k * dist::DB, dist::DB, pos, pivstep, rec_p, rec_q, rec_row, W};
+  return lc.w == 32 ? launch_leaf<32, 1>(la, lc.cl, s)
+         : lc.w == 16 ? launch_leaf<16, 2>(la, lc.cl, s)
+                      : launch_leaf<8, 4>(la, lc.cl, s);
 }
 
-cudaError_t dist_update(int n, int P, int rank, int k, double* Xl, const double* W, const int* pivstep,
+// part 0: every local column except this rank's own panel k (gather + GEMM);
+// part 1: gather, then only the local columns of panel k+1 (this rank must own k+1);
+// part 2: the local columns outside panels k and k+1, R already gathered by part 1,
+//         launched as a programmatic dependent of the preceding kernel (the factorisation
+//         of panel k+1) on the SMs its cluster leaves free — the look-ahead of §8e.
+cudaError_t dist_update(int n, int P, int rank, int k, int part, double* Xl, const double* W, const int* pivstep,
                         const int* rec_row, double* R, cudaStream_t s) {
   using namespace large;
   int npad, nl, nr;
   dist_sizes(n, P, rank, &npad, &nl, &nr);
-  if (k < 0 || k >= dist::nblocks(npad)) return cudaErrorInvalidValue;
+  const int nb = dist::nblocks(npad);
+  if (k < 0 || k >= nb || part < 0 || part > 2) return cudaErrorInvalidValue;
+  if (part > 0 && (k + 1 >= nb || (k + 1) % P != rank)) return cudaErrorInvalidValue;
   if (nl == 0) return cudaSuccess;
   const int k0 = k * dist::DB;
-  gather_rows_kernel<<<dim3((nl / 2 + 255) / 256, dist::DB), 256, 0, s>>>(Xl, nl, rec_row + k0, dist::DB, R, 0, nl);
+  if (part != 2)
+    gather_rows_kernel<<<dim3((nl / 2 + 255) / 256, dist::DB), 256, 0, s>>>(Xl, nl, rec_row + k0, dist::DB, R, 0, nl);
   const bool own = k % P == rank;
-  const int c0 = own ? (k / P) * dist::DB : 0;
-  GemmArgs g{W, dist::DB, R, nl, Xl, nl, npad, nl - (own ? dist::DB : 0), dist::DB, pivstep, k0, k0 + dist::DB,
-             own ? c0 : 0, own ? c0 + dist::DB : 0};
-  return launch_gemm(g, s);
+  const int c0 = (k / P) * dist::DB;             // local block of panel k (if owned)
+  const int c1 = ((k + 1) / P) * dist::DB;       // local block of panel k+1 (if owned)
+  if (part == 1) {
+    GemmArgs g{W, dist::DB, R + c1, nl, Xl + c1, nl, npad, dist::DB, dist::DB, pivstep, k0, k0 + dist::DB, 0, 0};
+    return launch_gemm(g, s);
+  }
+  if (part == 0) {
+    GemmArgs g{W, dist::DB, R, nl, Xl, nl, npad, nl - (own ? dist::DB : 0), dist::DB, pivstep, k0, k0 + dist::DB,
+               own ? c0 : 0, own ? c0 + dist::DB : 0};
+    return launch_gemm(g, s);
+  }
+  // part 2: skip [c1, c1 + DB) and, when this rank also owns panel k (P == 1: adjacent), [c0, c0 + DB)
+  int lo = c1, hi = c1 + dist::DB;
+  if (own) {
+    lo = c0 < c1 ? c0 : c1;
+    hi = (c0 > c1 ? c0 : c1) + dist::DB;
+    if (hi - lo != 2 * dist::DB) return cudaErrorInvalidValue;   // only adjacent blocks (P == 1)
+  }
+  GemmArgs g{W, dist::DB, R, nl, Xl, nl, npad, nl - (hi - lo), dist::DB, pivstep, k0, k0 + dist::DB, lo, hi};
+  LeafCfg lc;
+  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
+  return launch_gemm(g, s, device_sm_count() - lc.cl, true);
 }
 
 cudaError_t dist_finalize(int n, const double* rec_p, const int* rec_q, double tol, const unsigned long long* smax,

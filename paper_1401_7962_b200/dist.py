@@ -62,7 +62,7 @@ class CudaSteps:
             ("gj_dist_sizes", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3),
             ("gj_dist_init", [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 5),
             ("gj_dist_factor", [ctypes.c_int] * 4 + [ctypes.c_void_p] * 8),
-            ("gj_dist_update", [ctypes.c_int] * 4 + [ctypes.c_void_p] * 6),
+            ("gj_dist_update", [ctypes.c_int] * 5 + [ctypes.c_void_p] * 6),
             ("gj_dist_finalize", [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double] + [ctypes.c_void_p] * 6),
             ("gj_dist_unpermute_plan", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 5),
             ("gj_dist_unpermute_pack", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
@@ -88,9 +88,9 @@ class CudaSteps:
         self._check(self.lib.gj_dist_factor(self.n, self.P, self.rank, k, X.data_ptr(), pos.data_ptr(), pivstep.data_ptr(),
                                             rec_p.data_ptr(), rec_q.data_ptr(), rec_row.data_ptr(), W.data_ptr(), self._s()))
 
-    def update(self, k, X, W, pivstep, rec_row, R):
-        self._check(self.lib.gj_dist_update(self.n, self.P, self.rank, k, self._p(X), W.data_ptr(), pivstep.data_ptr(),
-                                            rec_row.data_ptr(), self._p(R), self._s()))
+    def update(self, k, part, X, W, pivstep, rec_row, R):
+        self._check(self.lib.gj_dist_update(self.n, self.P, self.rank, k, part, self._p(X), W.data_ptr(),
+                                            pivstep.data_ptr(), rec_row.data_ptr(), self._p(R), self._s()))
 
     def finalize(self, rec_p, rec_q, tol, smax, ipiv, logabsdet, sign, info):
         self._check(self.lib.gj_dist_finalize(self.n, rec_p.data_ptr(), rec_q.data_ptr(), tol, smax.data_ptr(),
@@ -175,33 +175,78 @@ def invert_dist(A_local: torch.Tensor, n: int, *, group=None, tol: Optional[floa
     f64 = dict(dtype=torch.float64, device=device)
     i32 = dict(dtype=torch.int32, device=device)
     X = torch.empty((npad, max(nl, 1)), **f64)
-    # replicated integer state, broadcast as one buffer: pos | pivstep | rec_q | rec_row
-    ibuf = torch.empty(4 * npad, **i32)
-    pos, pivstep, rec_q, rec_row = ibuf[:npad], ibuf[npad:2 * npad], ibuf[2 * npad:3 * npad], ibuf[3 * npad:]
-    # replicated fp64 state, broadcast as one buffer: W (npad x BLOCK) | rec_p
-    fbuf = torch.empty(npad * BLOCK + npad, **f64)
-    W, rec_p = fbuf[:npad * BLOCK].view(npad, BLOCK), fbuf[npad * BLOCK:]
+    # replicated state, broadcast by the panel owner as one int32 buffer:
+    # pos | pivstep | rec_q | rec_row | rec_p (fp64 viewed as 2 x int32)
+    ibuf = torch.empty(6 * npad, **i32)
+    pos, pivstep, rec_q, rec_row = ibuf[:npad], ibuf[npad:2 * npad], ibuf[2 * npad:3 * npad], ibuf[3 * npad:4 * npad]
+    rec_p = ibuf[4 * npad:].view(torch.float64)
+    # the factored panel W, double-buffered: W_{k+1} arrives while panel k's update still reads W_k
+    wbuf = [torch.empty((npad, BLOCK), **f64) for _ in range(2)]
     R = torch.empty((BLOCK, max(nl, 1)), **f64)
     smax = torch.zeros(1, dtype=torch.int64, device=device)
     ev = []
+    cuda = device.type == "cuda"
+    main = torch.cuda.current_stream(device) if cuda else None
+    side = torch.cuda.Stream(device=device) if cuda else None
 
     def mark(name):
-        if timing and device.type == "cuda":
+        if timing and cuda:
             e = torch.cuda.Event(enable_timing=True)
-            e.record()
+            e.record(main)
             ev.append((name, e))
 
+    def record(stream):
+        if not cuda:
+            return None
+        e = torch.cuda.Event()
+        e.record(stream)
+        return e
+
     mark("start")
+    nb = npad // BLOCK
     steps.init(A_local if nr else None, max(nr, 1), X, pos, pivstep, smax)
     allreduce_max(smax)   # bit patterns of non-negative doubles order like the values
-    for k in range(npad // BLOCK):
-        src = k % P
-        if rank == src:
-            steps.factor(k, X, pos, pivstep, rec_p, rec_q, rec_row, W)
-        if P > 1:
-            bcast(ibuf, src)
-            bcast(fbuf, src)
-        steps.update(k, X if nl else None, W, pivstep, rec_row, R if nl else None)
+    Xo = X if nl else None
+    Ro = R if nl else None
+    # panel 0: factored and broadcast before the loop
+    if rank == 0:
+        steps.factor(0, X, pos, pivstep, rec_p, rec_q, rec_row, wbuf[0])
+    if P > 1:
+        bcast(ibuf, 0)
+        bcast(wbuf[0], 0)
+    ev_upd = record(main)
+    for k in range(nb):
+        W = wbuf[k % 2]
+        nxt = k + 1 < nb
+        own_next = nxt and (k + 1) % P == rank
+        ev_fac = None
+        if own_next:
+            # look-ahead: panel k+1's columns first, factor it, then the rest of panel k's
+            # update runs beside that factorisation (programmatic dependent launch)
+            steps.update(k, 1, Xo, W, pivstep, rec_row, Ro)
+            steps.factor(k + 1, X, pos, pivstep, rec_p, rec_q, rec_row, wbuf[(k + 1) % 2])
+            ev_fac = record(main)
+            steps.update(k, 2, Xo, W, pivstep, rec_row, Ro)
+        else:
+            steps.update(k, 0, Xo, W, pivstep, rec_row, Ro)
+        if nxt and P > 1:
+            # panel k+1 travels on a side stream: after its factorisation (owner) and after the
+            # last update that read the buffer it lands in (everyone); not after panel k's update
+            if cuda:
+                side.wait_event(ev_upd)
+                if ev_fac is not None:
+                    side.wait_event(ev_fac)
+                with torch.cuda.stream(side):
+                    bcast(ibuf, (k + 1) % P)
+                    bcast(wbuf[(k + 1) % 2], (k + 1) % P)
+                ev_b = record(side)
+                ev_upd = record(main)
+                main.wait_event(ev_b)
+            else:
+                bcast(ibuf, (k + 1) % P)
+                bcast(wbuf[(k + 1) % 2], (k + 1) % P)
+        elif cuda:
+            ev_upd = record(main)
     mark("eliminated")
     ipiv = torch.empty(n, **i32)
     lg = torch.empty(1, **f64)

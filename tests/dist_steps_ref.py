@@ -78,18 +78,29 @@ class RefSteps:
             X[r, J] = rowp
         W.copy_(X[:, J])
 
-    def update(self, k, X, W, pivstep, rec_row, R):
+    def update(self, k, part, X, W, pivstep, rec_row, R):
+        """part 0: all local columns but the own panel k; part 1: gather R, then only the
+        local columns of panel k+1; part 2: the rest (R from part 1)."""
         if X is None:
             return
         k0 = k * BLOCK
         rows = rec_row[k0:k0 + BLOCK].long()
-        Rt = X[rows, :].clone()
+        if part != 2:
+            R.copy_(X[rows, :])
         cols = torch.ones(self.nl, dtype=torch.bool)
         if k % self.P == self.rank:
             cols[(k // self.P) * BLOCK:(k // self.P + 1) * BLOCK] = False
+        nxt = torch.zeros(self.nl, dtype=torch.bool)
+        if part > 0:
+            c1 = ((k + 1) // self.P) * BLOCK
+            nxt[c1:c1 + BLOCK] = True
+        if part == 1:
+            cols = nxt
+        elif part == 2:
+            cols &= ~nxt
         idx = torch.nonzero(cols).flatten()
-        upd = X[:, idx] + W @ Rt[:, idx]
-        upd[rows] -= Rt[:, idx]
+        upd = X[:, idx] + W @ R[:, idx]
+        upd[rows] -= R[:, idx]
         X[:, idx] = upd
 
     def finalize(self, rec_p, rec_q, tol, smax, ipiv, logabsdet, sign, info):
