@@ -50,6 +50,12 @@ using namespace ptx;
 using namespace rowops;
 
 constexpr int kWarpsPerBlock = 4;
+#ifndef GJ_K1_FAST_PIVOT
+#define GJ_K1_FAST_PIVOT 0
+#endif
+// K1b: ballot fast path for the (usual) unique maximum; measured no faster on C2 (kept
+// as a build-time option, -DGJ_K1_FAST_PIVOT=1)
+constexpr bool kFastPivot = GJ_K1_FAST_PIVOT != 0;
 
 // R rows per lane: two rows share every pivot-row load (halving the shared-memory
 // traffic of the broadcast, which bounds the fp32 n = 32 case); L = NP/R lanes per matrix.
@@ -576,21 +582,49 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
   float t[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) t[r] = P[r][s] * ra;
-  // ties -> smallest physical position (G3); the winner code carries (position, lane, slot)
-  uint32_t cmin = 0xffffffu;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t c = (key[r] == m && kmask[r] != 0u)
-                           ? ((uint32_t)pos[r] << (5 + SB) | (uint32_t)lane << SB | (uint32_t)r) : 0xffffffu;
-    cmin = min(cmin, c);
-  }
-  const uint32_t win = blk_gmin<R>(cmin, g);
-  const int q = (int)(win >> (5 + SB));
-  const int src = (int)((win >> SB) & 31u);
-  const int slot = (int)(win & ((1u << SB) - 1u));
+  int q, src, slot;
   bool pv[R];
+  // fast path: exactly one row per matrix attains the maximum (warp-uniform test on the
+  // ballots; an all-zero column makes every row tie and takes the slow path)
+  unsigned ball[R];
+  int tot = 0;
+  if constexpr (kFastPivot) {
 #pragma unroll
-  for (int r = 0; r < R; ++r) pv[r] = pos[r] == q;
+    for (int r = 0; r < R; ++r) {
+      pv[r] = key[r] == m;
+      ball[r] = __ballot_sync(0xffffffffu, pv[r]);
+      tot += __popc(ball[r]);
+    }
+  }
+  if (kFastPivot && tot == BlkGeo<R>::M) {
+    unsigned any = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) any |= ball[r];
+    const unsigned gm = (BlkGeo<R>::L == 32 ? 0xffffffffu : ((1u << BlkGeo<R>::L) - 1u)) << (BlkGeo<R>::L * g);
+    src = __ffs(any & gm) - 1;
+    slot = 0;
+#pragma unroll
+    for (int r = 1; r < R; ++r) slot = ((ball[r] >> src) & 1u) ? r : slot;
+    int ps = pos[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) ps = pv[r] ? pos[r] : ps;
+    q = __shfl_sync(0xffffffffu, ps, src);
+  } else {
+    // ties -> smallest physical position (G3); the winner code carries (position, lane, slot)
+    uint32_t cmin = 0xffffffu;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t c = (key[r] == m && kmask[r] != 0u)
+                             ? ((uint32_t)pos[r] << (5 + SB) | (uint32_t)lane << SB | (uint32_t)r) : 0xffffffu;
+      cmin = min(cmin, c);
+    }
+    const uint32_t win = blk_gmin<R>(cmin, g);
+    q = (int)(win >> (5 + SB));
+    src = (int)((win >> SB) & 31u);
+    slot = (int)(win & ((1u << SB) - 1u));
+#pragma unroll
+    for (int r = 0; r < R; ++r) pv[r] = pos[r] == q;
+  }
   // the pivot row's panel values (one shuffle each from the pivot lane)
   float z[BS];
 #pragma unroll
@@ -640,7 +674,9 @@ __device__ __forceinline__ void blk_publish(const float (&T)[R][32 - BS], const 
 }
 
 // Rank-1 term s of the trailing update on columns [J0, J1) of T: T += (W - S)[:, s] R_s.
-template <int R, int BS, int J0, int J1, int N>
+// SHIFT: write the result BS registers to the left (T[j - BS] = T[j] + ...), in increasing
+// j, which realises the block's register rotation without moves (the last term does it).
+template <int R, int BS, int J0, int J1, int N, bool SHIFT = false>
 __device__ __forceinline__ void blk_trail_term(float (&T)[R][N], const float (&P)[R][BS], int s, const float* rbuf_g,
                                                int tofs) {
   constexpr int RW = 32 - BS;
@@ -649,7 +685,16 @@ __device__ __forceinline__ void blk_trail_term(float (&T)[R][N], const float (&P
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int j = 0; j < J1 - J0; j += 2) ffma2(T[r][tofs + j], T[r][tofs + j + 1], P[r][s], Rs[j], Rs[j + 1]);
+    for (int j = 0; j < J1 - J0; j += 2) {
+      if constexpr (SHIFT) {
+        float u0 = T[r][tofs + j], u1 = T[r][tofs + j + 1];
+        ffma2(u0, u1, P[r][s], Rs[j], Rs[j + 1]);
+        T[r][tofs + j - BS] = u0;
+        T[r][tofs + j + 1 - BS] = u1;
+      } else {
+        ffma2(T[r][tofs + j], T[r][tofs + j + 1], P[r][s], Rs[j], Rs[j + 1]);
+      }
+    }
 }
 
 // NST = TMA stages per warp: 2 = the next task streams in during this one; 1 = half the
@@ -767,13 +812,14 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
 #pragma unroll
       for (int s = 0; s < BS; ++s) {
         blk_panel_step<R, BS>(s, kb + BS + s, NP, kmask, pos, bs, rec_g, li, g, lane);
-        blk_trail_term<R, BS, BS, RW, RW>(T, P, s, rbuf_g, BS);
+        if (s + 1 < BS)
+          blk_trail_term<R, BS, BS, RW, RW>(T, P, s, rbuf_g, BS);
+        else
+          blk_trail_term<R, BS, BS, RW, RW, true>(T, P, s, rbuf_g, BS);   // + the rotation
       }
       __syncwarp();   // every lane has read rbuf before the next publish
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-#pragma unroll
-        for (int j = 0; j < RW - BS; ++j) T[r][j] = T[r][j + BS];
 #pragma unroll
         for (int j = 0; j < BS; ++j) {
           T[r][RW - BS + j] = P[r][j];
