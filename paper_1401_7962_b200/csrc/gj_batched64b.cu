@@ -1,23 +1,27 @@
 // K2b — batched Gauss–Jordan inversion for fp64 n = 64 on sm_100a (BASELINE configs[2],
-// C3): one matrix per CTA of two warps, COLUMN-SPLIT: warp w holds columns [32w, 32w+32)
-// of rows q and q + 32 in lane q (two half rows per thread), so every shared-memory
-// read of the trailing update feeds two rows (the unsplit one-row-per-thread K2 has
-// every thread read every pivot row whole, which bounds it by shared-memory delivery).
+// C3): one matrix per CTA of two warps.  Lane q of each warp holds rows q and q + 32
+// ("two half rows per thread": every shared-memory read of an update feeds two rows);
+// the 64 columns are split in eight blocks of BS = 8, warp w holding the blocks j with
+// j % 2 == w.
 //
 // The elimination (§2, Eqs. (14)-(15), L61-L72; Obs. 2-3 L59-L60; listing
-// L150-L177) is taken in blocks of BS = 8 steps, as K1b does (gj_batched.cu):
-//   panel phase (owner warp = the warp holding the block's columns): per step the
-//     max-|x_ik| pivot among the un-pivoted rows (ties to the smallest physical position,
-//     reading G3; three redux.sync on the fp64 bit pattern), the pivot row's 8 panel
-//     values by shuffle, the panel columns updated with the deferred-normalisation
-//     multiplier x_ik / p; the compact D entry of the pivot row is held as 1 - 1 = 0
-//     (W - S);
-//   block end: the owner publishes W - S (64 rows x 8) and its part of the block's pivot
-//     rows; the other warp publishes its part; both apply X[:, J'] += (W - S) R.
-// Rows never move (logical swaps on positions); the un-permutation (L179-L198) happens in
-// the un-permuted store, as in K1/K2.  The owner warp rotates its registers by BS per
-// block (four blocks per half: back to the identity); positions are handed from warp 0
-// to warp 1 at the half boundary and back at the end.
+// L150-L177) is taken block by block, as K1b does (gj_batched.cu):
+//   factor(b)  (the warp owning block b): BS pivot steps on the block's columns — per step
+//              the max-|x_ik| pivot among the un-pivoted rows (ties to the smallest physical
+//              position, reading G3; three redux.sync on the fp64 bit pattern), the pivot
+//              row's block values by shuffle, the block's columns updated with the
+//              deferred-normalisation multiplier x_ik / p (the pivot row's own compact
+//              entry held as 1 - 1 = 0: W - S);
+//   E_b        every other column: X[:, c] += (W_b - S_b) R_b[c], R_b = the block's pivot
+//              rows before the update.  A column's update needs only
+//              that column's R values, so each warp publishes and reads only its own.
+// Cross-warp look-ahead: the only data crossing warps is W_b (64 x 8) and the block's
+// pivot record.  The owner of b publishes them and goes on with E_b on its own columns;
+// the other warp (the owner of b+1) applies E_b to its next block first, factors b+1 at
+// once, and applies E_b to its remaining columns afterwards — so the two warps' panel
+// chains and updates overlap.  Producer/consumer named barriers (bar.arrive / bar.sync)
+// per W buffer parity; rows never move (logical swaps on positions, replayed by the
+// non-owner from the record); the un-permutation (L179-L198) happens in the store.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cmath>
@@ -34,36 +38,32 @@ using namespace ptx;
 using namespace rowops;
 
 constexpr int NPB = 64;         // matrix order
-constexpr int BSB = 8;          // block (panel) width
+constexpr int BSB = 8;          // block width
 constexpr int HW = 32;          // columns per warp
-constexpr int RWO = HW - BSB;   // owner's trailing columns
+constexpr int RWO = HW - BSB;   // a warp's columns outside its front block
 constexpr int kThreadsB = 64;
 
 struct SmemB {
   static constexpr int STAGE = NPB * NPB * 8;                 // 4 TMA boxes [64 rows][128 B]
-  static constexpr int W = 2 * NPB * BSB * 8;                 // [2][64 rows][BS] W - S
-  static constexpr int RO = 2 * BSB * RWO * 8;                // [2][BS][RWO] owner part of pivot rows
-  static constexpr int RT = 2 * BSB * HW * 8;                 // [2][BS][32] other part
+  static constexpr int W = 2 * NPB * BSB * 8;                 // [parity][64 rows][BS] W - S
+  static constexpr int BSM = 2 * HW * 2 * 4;                  // [parity][lane][slot] block step of a pivot row
+  static constexpr int RO = 2 * BSB * HW * 8;                 // [warp][BS][32] each warp's pivot-row values
   static constexpr int REC = NPB * 16;                        // [step] (p, q)
-  static constexpr int BSM = 2 * HW * 2 * 4;                  // [2][lane][slot] block step of pivot
-  static constexpr int POS = NPB * 4;                         // [row] position hand-over
+  static constexpr int POS = NPB * 4;
   static constexpr int PERM = NPB * 4;
   static constexpr int EX = 64;
-  static constexpr int TOTAL = STAGE + W + RO + RT + REC + BSM + POS + PERM + EX + 16;
+  static constexpr int TOTAL = STAGE + W + BSM + RO + REC + POS + PERM + EX + 16;
 };
 
-// (row, column byte) inside the TMA stage: 4 regions of [64 rows][128 B], 128-byte swizzle
 __device__ __forceinline__ uint32_t st_addr(int row, uint32_t cb) {
   return (cb >> 7) * (NPB * 128) + (uint32_t)row * 128u + ((cb & 127u) ^ ((uint32_t)(row & 7) << 4));
 }
-
 __device__ __forceinline__ double shfl_d(double v, int src) {
   const long long b = __double_as_longlong(v);
   const int lo = __shfl_sync(0xffffffffu, (int)(b & 0xffffffffll), src);
   const int hi = __shfl_sync(0xffffffffu, (int)(b >> 32), src);
   return __longlong_as_double(((long long)hi << 32) | (unsigned int)lo);
 }
-
 __device__ __forceinline__ double rcp64(double p) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
@@ -72,11 +72,14 @@ __device__ __forceinline__ double rcp64(double p) {
   e = fma(-p, r, 1.0);
   return fma(r, e, r);
 }
+// named barriers over both warps: the producer arrives, the consumer waits
+__device__ __forceinline__ void nb_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nb_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+constexpr int kFull = 1, kEmpty = 3;   // + parity
 
-// One panel step of the owner warp: s static, k = global step.
+// One pivot step s (static) of factor(b) at global step k on registers x[.][0..BS).
 __device__ __forceinline__ void panel_step64(const int s, const int k, double (&x)[2][HW], uint32_t (&kmask)[2],
                                              int (&pos)[2], int (&bs)[2], unsigned char* rec, int lane) {
-  // a2: (hi, lo) words of |x| among the un-pivoted rows; ties -> smallest position
   uint32_t hi[2], lo[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -98,9 +101,6 @@ __device__ __forceinline__ void panel_step64(const int s, const int k, double (&
   const int q = (int)(win >> 6);
   const int src = (int)((win >> 1) & 31u);
   const bool slot1 = (win & 1u) != 0u;
-  bool pv[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) pv[r] = pos[r] == q;
   double z[BSB];
 #pragma unroll
   for (int j = 0; j < BSB; ++j) z[j] = shfl_d(slot1 ? x[1][j] : x[0][j], src);
@@ -108,17 +108,68 @@ __device__ __forceinline__ void panel_step64(const int s, const int k, double (&
   const double rp = rcp64(p);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const double nf = pv[r] ? 0.0 : -(x[r][s] * rp);
+    const bool pv = pos[r] == q;
+    const double nf = pv ? 0.0 : -(x[r][s] * rp);
 #pragma unroll
     for (int j = 0; j < BSB; ++j)
       if (j != s) x[r][j] = fma(nf, z[j], x[r][j]);
     x[r][s] = nf;   // W - S
-    kmask[r] = pv[r] ? 0u : kmask[r];
-    bs[r] = pv[r] ? s : bs[r];
+    kmask[r] = pv ? 0u : kmask[r];
+    bs[r] = pv ? s : bs[r];
     pos[r] = (pos[r] == k) ? q : pos[r];
-    pos[r] = pv[r] ? k : pos[r];
+    pos[r] = pv ? k : pos[r];
   }
   if (lane == 0) rec_store(rec, k, p, q);
+}
+
+// Publish this warp's values of the block's pivot rows, registers [J0, J0 + N) -> R[s][0..N).
+template <int J0, int N>
+__device__ __forceinline__ void publish_rows(const double (&x)[2][HW], const int (&bs)[2], double* R) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (bs[r] >= 0) {
+      double2* d = reinterpret_cast<double2*>(R + bs[r] * HW);
+#pragma unroll
+      for (int j = 0; j < N; j += 2) d[j / 2] = make_double2(x[r][J0 + j], x[r][J0 + j + 1]);
+    }
+  }
+}
+
+// E_b on registers [J0, J0 + N): x[r][c] += sum_s w[r][s] R[s][c - J0]; SHIFT writes the
+// result BS registers to the left (the owner's rotation after its own panel).
+template <int J0, int N, bool SHIFT>
+__device__ __forceinline__ void apply_update(double (&x)[2][HW], const double (&w)[2][BSB], const double* R) {
+#pragma unroll
+  for (int s = 0; s < BSB; ++s) {
+    const double2* rs = reinterpret_cast<const double2*>(R + s * HW);
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+      const double2 v = rs[j / 2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (SHIFT && s + 1 == BSB) {
+          x[r][J0 + j - BSB] = fma(w[r][s], v.x, x[r][J0 + j]);
+          x[r][J0 + j + 1 - BSB] = fma(w[r][s], v.y, x[r][J0 + j + 1]);
+        } else {
+          x[r][J0 + j] = fma(w[r][s], v.x, x[r][J0 + j]);
+          x[r][J0 + j + 1] = fma(w[r][s], v.y, x[r][J0 + j + 1]);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void load_w(double (&w)[2][BSB], const double* W, int lane) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const double2* wd = reinterpret_cast<const double2*>(W + (lane + 32 * r) * BSB);
+#pragma unroll
+    for (int j = 0; j < BSB; j += 2) {
+      const double2 v = wd[j / 2];
+      w[r][j] = v.x;
+      w[r][j + 1] = v.y;
+    }
+  }
 }
 
 struct MapsB {
@@ -130,17 +181,17 @@ gj_batched64b_kernel(BatchedArgs a, const __grid_constant__ MapsB tm) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* stage = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* Wsm = reinterpret_cast<double*>(stage + SmemB::STAGE);
-  double* Ro = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(Wsm) + SmemB::W);
-  double* Rt = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(Ro) + SmemB::RO);
-  unsigned char* rec = reinterpret_cast<unsigned char*>(Rt) + SmemB::RT;
-  int* bsm = reinterpret_cast<int*>(rec + SmemB::REC);
-  int* posx = bsm + 2 * HW * 2;
+  int* bsm = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(Wsm) + SmemB::W);
+  double* Rsm = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(bsm) + SmemB::BSM);
+  unsigned char* rec = reinterpret_cast<unsigned char*>(Rsm) + SmemB::RO;
+  int* posx = reinterpret_cast<int*>(rec + SmemB::REC);
   int* perm = posx + NPB;
   uint32_t* ex = reinterpret_cast<uint32_t*>(perm + NPB);
   uint64_t* bar = reinterpret_cast<uint64_t*>(ex + 16);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  double* Rw = Rsm + warp * BSB * HW;   // this warp's pivot-row values
 
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -160,18 +211,19 @@ gj_batched64b_kernel(BatchedArgs a, const __grid_constant__ MapsB tm) {
     while (!mbar_try_wait(bar, it & 1)) {
     }
     __syncwarp();
+    // warp w: blocks w, w+2, w+4, w+6 -> registers [0,8), [8,16), [16,24), [24,32)
     double x[2][HW];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int row = lane + 32 * r;
 #pragma unroll
       for (int j = 0; j < HW; j += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(stage + st_addr(row, (uint32_t)(HW * warp + j) * 8u));
+        const int col = BSB * (2 * (j / BSB) + warp) + j % BSB;
+        const double2 v = *reinterpret_cast<const double2*>(stage + st_addr(row, (uint32_t)col * 8u));
         x[r][j] = v.x;
         x[r][j + 1] = v.y;
       }
     }
-    // zero threshold tau = tol * max|a_ij| (Obs. 2, reading G1)
     {
       double rm = 0.0;
 #pragma unroll
@@ -196,129 +248,85 @@ gj_batched64b_kernel(BatchedArgs a, const __grid_constant__ MapsB tm) {
 
     uint32_t kmask[2] = {0xffffffffu, 0xffffffffu};
     int pos[2] = {lane, lane + 32};
-    int blk = 0;
+    bool pending = false;   // E_{b-1} still to be applied to registers [BS, 32)
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      if (h == 1) {
-        // hand the positions over from warp 0 (owner of steps 0..31) to warp 1
-        if (warp == 0) {
-          posx[lane] = pos[0];
-          posx[lane + 32] = pos[1];
+    for (int b = 0; b < NPB / BSB; ++b) {
+      const int par = b & 1;
+      const int k0 = BSB * b;
+      double* W = Wsm + par * NPB * BSB;
+      int* bsb = bsm + par * HW * 2;
+      if ((b & 1) == warp) {
+        // ---------------- owner of block b: its front block has every earlier update
+        int bs[2] = {-1, -1};
+#pragma unroll
+        for (int s = 0; s < BSB; ++s) panel_step64(s, k0 + s, x, kmask, pos, bs, rec, lane);
+        if (b >= 2) nb_sync(kEmpty + par);   // the other warp is done with W_{b-2}
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          double2* wd = reinterpret_cast<double2*>(W + (lane + 32 * r) * BSB);
+#pragma unroll
+          for (int j = 0; j < BSB; j += 2) wd[j / 2] = make_double2(x[r][j], x[r][j + 1]);
+          bsb[lane * 2 + r] = bs[r];
         }
-        __syncthreads();
-        if (warp == 1) {
-          pos[0] = posx[lane];
-          pos[1] = posx[lane + 32];
-          kmask[0] = pos[0] < 32 ? 0u : 0xffffffffu;
-          kmask[1] = pos[1] < 32 ? 0u : 0xffffffffu;
+        nb_arrive(kFull + par);             // W_b, the block steps and the record are out
+        if (pending) {
+          // E_{b-1} on the columns outside the new panel (values R from this warp's copy)
+          double w[2][BSB];
+          load_w(w, Wsm + (par ^ 1) * NPB * BSB, lane);
+          apply_update<BSB, RWO, false>(x, w, Rw + BSB);
+          __syncwarp();
+          if (b + 1 < NPB / BSB) nb_arrive(kEmpty + (par ^ 1));   // done with W_{b-1} (reused at b+1)
+        }
+        // E_b on this warp's other columns, rotating the panel to the end
+        __syncwarp();
+        publish_rows<BSB, RWO>(x, bs, Rw);
+        __syncwarp();
+        double w[2][BSB];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int s = 0; s < BSB; ++s) w[r][s] = x[r][s];
+        apply_update<BSB, RWO, true>(x, w, Rw);
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int s = 0; s < BSB; ++s) x[r][RWO + s] = w[r][s];
+        pending = false;
+      } else {
+        // ---------------- the other warp: wait for W_b, replay the block's swaps, apply
+        // E_b to the front block now (look-ahead) and to the rest after its next panel
+        nb_sync(kFull + par);
+        int bs[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) bs[r] = bsb[lane * 2 + r];
+#pragma unroll
+        for (int s = 0; s < BSB; ++s) {
+          int q;
+          double pdd;
+          rec_load(rec, k0 + s, pdd, q);
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            pos[r] = (pos[r] == k0 + s) ? q : pos[r];
+            if (bs[r] == s) {
+              pos[r] = k0 + s;
+              kmask[r] = 0u;
+            }
+          }
+        }
+        publish_rows<0, HW>(x, bs, Rw);
+        __syncwarp();
+        double w[2][BSB];
+        load_w(w, W, lane);
+        apply_update<0, BSB, false>(x, w, Rw);
+        pending = true;
+        if (b + 1 == NPB / BSB) {   // no next panel: the rest now
+          apply_update<BSB, RWO, false>(x, w, Rw + BSB);
+          pending = false;
         }
       }
-#pragma unroll 1
-      for (int bb = 0; bb < HW / BSB; ++bb, ++blk) {
-        const int kb = HW * h + BSB * bb;
-        const int buf = blk & 1;
-        double* W = Wsm + buf * NPB * BSB;
-        double* RO_ = Ro + buf * BSB * RWO;
-        double* RT_ = Rt + buf * BSB * HW;
-        int* bsb = bsm + buf * HW * 2;
-        if (warp == h) {
-          // ---- owner: panel phase on registers 0..BS ----
-          int bs[2] = {-1, -1};
-#pragma unroll
-          for (int s = 0; s < BSB; ++s) panel_step64(s, kb + s, x, kmask, pos, bs, rec, lane);
-          // publish W - S, the pivot rows' owner part (registers BS..32), block steps
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            double2* wd = reinterpret_cast<double2*>(W + (lane + 32 * r) * BSB);
-#pragma unroll
-            for (int j = 0; j < BSB; j += 2) wd[j / 2] = make_double2(x[r][j], x[r][j + 1]);
-            if (bs[r] >= 0) {
-              double2* rd = reinterpret_cast<double2*>(RO_ + bs[r] * RWO);
-#pragma unroll
-              for (int j = 0; j < RWO; j += 2) rd[j / 2] = make_double2(x[r][BSB + j], x[r][BSB + j + 1]);
-            }
-            bsb[lane * 2 + r] = bs[r];
-          }
-          __syncthreads();   // (1)
-          __syncthreads();   // (2): the other warp's part of the pivot rows
-          // trailing update of registers BS..32, written BS to the left; W - S appended
-          double w[2][BSB];
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int s = 0; s < BSB; ++s) w[r][s] = x[r][s];
-#pragma unroll
-          for (int s = 0; s < BSB; ++s) {
-            const double2* rs = reinterpret_cast<const double2*>(RO_ + s * RWO);
-#pragma unroll
-            for (int j = 0; j < RWO; j += 2) {
-              const double2 v = rs[j / 2];
-#pragma unroll
-              for (int r = 0; r < 2; ++r) {
-                if (s + 1 < BSB) {
-                  x[r][BSB + j] = fma(w[r][s], v.x, x[r][BSB + j]);
-                  x[r][BSB + j + 1] = fma(w[r][s], v.y, x[r][BSB + j + 1]);
-                } else {
-                  x[r][j] = fma(w[r][s], v.x, x[r][BSB + j]);
-                  x[r][j + 1] = fma(w[r][s], v.y, x[r][BSB + j + 1]);
-                }
-              }
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int s = 0; s < BSB; ++s) x[r][RWO + s] = w[r][s];
-        } else {
-          __syncthreads();   // (1): W - S, the owner part, block steps
-          int bs[2];
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            bs[r] = bsb[lane * 2 + r];
-            if (bs[r] >= 0) {
-              double2* rd = reinterpret_cast<double2*>(RT_ + bs[r] * HW);
-#pragma unroll
-              for (int j = 0; j < HW; j += 2) rd[j / 2] = make_double2(x[r][j], x[r][j + 1]);
-            }
-          }
-          __syncthreads();   // (2)
-          double w[2][BSB];
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const double2* wd = reinterpret_cast<const double2*>(W + (lane + 32 * r) * BSB);
-#pragma unroll
-            for (int j = 0; j < BSB; j += 2) {
-              const double2 v = wd[j / 2];
-              w[r][j] = v.x;
-              w[r][j + 1] = v.y;
-            }
-          }
-#pragma unroll
-          for (int s = 0; s < BSB; ++s) {
-            const double2* rs = reinterpret_cast<const double2*>(RT_ + s * HW);
-#pragma unroll
-            for (int j = 0; j < HW; j += 2) {
-              const double2 v = rs[j / 2];
-#pragma unroll
-              for (int r = 0; r < 2; ++r) {
-                x[r][j] = fma(w[r][s], v.x, x[r][j]);
-                x[r][j + 1] = fma(w[r][s], v.y, x[r][j + 1]);
-              }
-            }
-          }
-        }
-      }
-    }
-    // positions back to both warps (warp 1 holds the final ones: pos = the row's pivot step)
-    if (warp == 1) {
-      posx[lane] = pos[0];
-      posx[lane + 32] = pos[1];
     }
     __syncthreads();
-    pos[0] = posx[lane];
-    pos[1] = posx[lane + 32];
-
-    // ---- a6: det / ipiv / singular flag from the per-step record (warp 0) ----
+    // positions: warp 1 owns the last block, both are consistent now
     double myrp[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
@@ -328,6 +336,7 @@ gj_batched64b_kernel(BatchedArgs a, const __grid_constant__ MapsB tm) {
       myrp[r] = rcp64(p_own);
       (void)q_own;
     }
+    // ---- a6: det / ipiv / singular flag from the per-step record (warp 0) ----
     if (warp == 0) {
       unsigned fb[2];
       int nsw = 0, nng = 0;
@@ -366,13 +375,12 @@ gj_batched64b_kernel(BatchedArgs a, const __grid_constant__ MapsB tm) {
       for (int r = 0; r < 2; ++r) {
         const int orow = pos[r];
 #pragma unroll
-        for (int j = 0; j < HW; j += 2) {
-          const int2 cb = *reinterpret_cast<const int2*>(perm + HW * warp + j);
-          *reinterpret_cast<double*>(stage + st_addr(orow, (uint32_t)cb.x)) = myrp[r] * x[r][j];
-          *reinterpret_cast<double*>(stage + st_addr(orow, (uint32_t)cb.y)) = myrp[r] * x[r][j + 1];
+        for (int j = 0; j < HW; ++j) {
+          const int c = BSB * (2 * (j / BSB) + warp) + j % BSB;   // compact column of register j
+          *reinterpret_cast<double*>(stage + st_addr(orow, (uint32_t)perm[c])) = myrp[r] * x[r][j];
         }
         // the row's own compact entry was held as W - 1: add the 1 back (owner of that column)
-        if (pos[r] / HW == warp) {
+        if ((pos[r] / BSB) % 2 == warp) {
           double* own = reinterpret_cast<double*>(stage + st_addr(orow, (uint32_t)((lane + 32 * r) * 8)));
           *own = *own + myrp[r];
         }
