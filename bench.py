@@ -388,6 +388,7 @@ def main():
             e2e_s = float(t.item())
         e2e = {"value": world * B / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Ah.numel() * 4),
                "d2h_bytes_per_step": int(Xh.numel() * 4 + B * 9), "ms_per_step": e2e_s * 1e3,
+               "ms_each": [round(t * 1e3, 2) for t in ts],
                "api": "gj_invert_batched_host (pinned host buffers, chunked H2D/compute/D2H pipeline)"}
 
     if rank == 0:

@@ -1,0 +1,7 @@
+# round-end style validation: all GPU tests, smoke, the bench line, the reference arm
+set -x
+timeout 1800 python -m pytest tests -q -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo bench_rc=$?
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
+cat gpurun_out/bench_ref.json
