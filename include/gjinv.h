@@ -98,8 +98,9 @@ gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logab
 
 /*
  * gj_invert — one n x n matrix, any n >= 1 (n <= 64 uses the batched kernels; larger n
- * the blocked Gauss–Jordan: panel factorisation + FP64 tensor-core trailing updates,
- * the aggregated form of Eqs. (14)-(15)).
+ * the blocked Gauss–Jordan: panel factorisation + tensor-core trailing updates, the
+ * aggregated form of Eqs. (14)-(15): FP64 DMMA for GJ_F64; for GJ_F32 tcgen05.mma
+ * kind::tf32 with the accumulator in TMEM and a 3xTF32 split for fp32 accuracy).
  *   A, lda       input (row stride lda >= n elements), read only.
  *   Ainv, ldainv output (row stride ldainv >= n); may equal A when lda == ldainv.
  *   ipiv, logabsdet, sign, info  as gj_invert_batched with batch = 1 (each may be NULL).

@@ -68,7 +68,8 @@ gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, vo
 size_t gj_workspace_size(gj_dtype dt, int n, int64_t batch, int entry) {
   (void)batch;
   if (n < 1) return 0;
-  if (n > GJ_BATCHED_MAX_N && (entry == 1 || entry == 2)) return dt == GJ_F64 ? large_workspace_size(n) : 0;
+  if (n > GJ_BATCHED_MAX_N && (entry == 1 || entry == 2))
+    return dt == GJ_F64 ? large_workspace_size(n) : large_workspace_size_f32(n);
   if (entry == 1) return (size_t)n * n * esize(dt);  // lda != n repack
   return 0;
 }
@@ -77,11 +78,15 @@ gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logab
                  int8_t* sign, void* det, int32_t* ipiv, int32_t* info, double tol,
                  void* workspace, size_t workspace_bytes, void* stream) {
   if (n > GJ_BATCHED_MAX_N) {
-    if (dt != GJ_F64 || batch != 1 || A == nullptr) return batch == 0 ? GJ_OK : GJ_ERR_UNSUPPORTED;
-    if (workspace == nullptr || workspace_bytes < large_workspace_size(n)) return GJ_ERR_WORKSPACE;
-    cudaError_t e = invert_large_f64(n, static_cast<const double*>(A), n, nullptr, 0, ipiv, logabsdet, sign,
-                                     static_cast<double*>(det), info, resolve_tol(dt, n, tol), workspace,
-                                     static_cast<cudaStream_t>(stream));
+    if ((dt != GJ_F64 && dt != GJ_F32) || batch != 1 || A == nullptr) return batch == 0 ? GJ_OK : GJ_ERR_UNSUPPORTED;
+    if (workspace == nullptr || workspace_bytes < gj_workspace_size(dt, n, 1, 2)) return GJ_ERR_WORKSPACE;
+    cudaError_t e = dt == GJ_F64
+        ? invert_large_f64(n, static_cast<const double*>(A), n, nullptr, 0, ipiv, logabsdet, sign,
+                           static_cast<double*>(det), info, resolve_tol(dt, n, tol), workspace,
+                           static_cast<cudaStream_t>(stream))
+        : invert_large_f32(n, static_cast<const float*>(A), n, nullptr, 0, ipiv, logabsdet, sign,
+                           static_cast<float*>(det), info, resolve_tol(dt, n, tol), workspace,
+                           static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
   }
   return gj_invert_batched(dt, n, batch, A, nullptr, ipiv, logabsdet, sign, det, info, tol, stream);
@@ -95,10 +100,13 @@ gj_status gj_invert(gj_dtype dt, int n, const void* A, int64_t lda, void* Ainv, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t es = esize(dt);
   if (n > GJ_BATCHED_MAX_N) {
-    if (dt != GJ_F64) return GJ_ERR_UNSUPPORTED;   // large-n fp32 (TF32 tensor path) is NEXT f1
-    if (workspace == nullptr || workspace_bytes < large_workspace_size(n)) return GJ_ERR_WORKSPACE;
-    cudaError_t e = invert_large_f64(n, static_cast<const double*>(A), lda, static_cast<double*>(Ainv), ldainv, ipiv,
-                                     logabsdet, sign, nullptr, info, resolve_tol(dt, n, tol), workspace, s);
+    if (workspace == nullptr || workspace_bytes < gj_workspace_size(dt, n, 1, 1)) return GJ_ERR_WORKSPACE;
+    cudaError_t e = dt == GJ_F64
+        ? invert_large_f64(n, static_cast<const double*>(A), lda, static_cast<double*>(Ainv), ldainv, ipiv,
+                           logabsdet, sign, nullptr, info, resolve_tol(dt, n, tol), workspace, s)
+        // fp32: the tcgen05 TF32 (3xTF32) trailing update
+        : invert_large_f32(n, static_cast<const float*>(A), lda, static_cast<float*>(Ainv), ldainv, ipiv,
+                           logabsdet, sign, nullptr, info, resolve_tol(dt, n, tol), workspace, s);
     return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
   }
   if (lda == n && ldainv == n)

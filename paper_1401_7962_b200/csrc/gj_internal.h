@@ -33,6 +33,25 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
                              double* logabsdet, int8_t* sign, double* det, int32_t* info, double tol, void* ws,
                              cudaStream_t s);
 
+// Large-n fp32 path (gj_large.cu) and its tcgen05 TF32 trailing update (gj_tcgemm.cu).
+cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, int64_t ldainv, int32_t* ipiv,
+                             double* logabsdet, int8_t* sign, float* det, int32_t* info, double tol, void* ws,
+                             cudaStream_t s);
+size_t large_workspace_size_f32(int n);
+struct TcUpdateArgs {
+  const float* Ah;   // M x 128, K-major: the panel W split, high TF32 part
+  const float* Al;   //                   low part
+  const float* Bh;   // Nrows x 128, K-major: R transposed (B[c][s] = R[s][c]), high part
+  const float* Bl;   //                   low part
+  float* C;          // C[i][c], row stride ldc (absolute column index c)
+  int64_t ldc;
+  int M, N, Nrows;   // N: columns updated (the skipped range excluded); Nrows: rows of Bh / Bl
+  const int* pivstep;
+  int rep_lo, rep_hi;   // rows with pivstep in [rep_lo, rep_hi) are replaced, not added to
+  int skip_lo, skip_hi; // columns [skip_lo, skip_hi) are not updated
+};
+cudaError_t launch_tc_update(const TcUpdateArgs& g, int grid_sms, bool pdl, cudaStream_t s);
+
 // Distributed large-n steps (gj_large.cu; column-block-cyclic, block 128).
 void dist_sizes(int n, int P, int rank, int* npad, int* nl, int* nl_real);
 cudaError_t dist_init(int n, int P, int rank, const double* A_local, int64_t lda, double* Xl, int* pos, int* pivstep,

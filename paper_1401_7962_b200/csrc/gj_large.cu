@@ -159,7 +159,7 @@ __device__ __forceinline__ void st_remote_v4(uint32_t raddr, uint4 v) {
 }
 
 struct LeafArgs {
-  double* X;         // npad rows, leading dimension ld (all columns, or one rank's local columns)
+  void* X;           // npad rows of T, leading dimension ld (all columns, or one rank's local columns)
   int64_t ld;        // row stride of X (elements)
   int npad;          // padded order (rows)
   int c0;            // first column of the panel in X
@@ -170,7 +170,7 @@ struct LeafArgs {
   double* rec_p;     // [npad] pivot value per step
   int* rec_q;        // [npad] pivot's physical position per step
   int* rec_row;      // [npad] pivot row per step
-  double* Wout;      // if non-null: the factored panel, npad x pw (ld pw), written at the end
+  void* Wout;        // if non-null: the factored panel (T), npad x pw (ld pw), written at the end
 };
 
 constexpr int kLeafThreads = 512;
@@ -225,16 +225,50 @@ __device__ __forceinline__ double rcp_f64(double p) {
   return fma(r, e, r);
 }
 
+__device__ __forceinline__ float rcp_t(float p) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
+  return fmaf(r, fmaf(-p, r, 1.0f), r);
+}
+__device__ __forceinline__ double rcp_t(double p) { return rcp_f64(p); }
+// the candidate key of |v|: (hi, lo) words of the IEEE bit pattern (monotone for |v|)
+__device__ __forceinline__ void abs_key(double v, uint32_t& hi, uint32_t& lo) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull;
+  hi = (uint32_t)(u >> 32);
+  lo = (uint32_t)u;
+}
+__device__ __forceinline__ void abs_key(float v, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(v) & 0x7fffffffu;
+  lo = 0u;
+}
+// two consecutive elements as one vector access
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+template <typename T>
+__device__ __forceinline__ void ld2(const T* p, T& a, T& b) {
+  const typename Vec2<T>::type v = *reinterpret_cast<const typename Vec2<T>::type*>(p);
+  a = v.x;
+  b = v.y;
+}
+template <typename T>
+__device__ __forceinline__ void st2(T* p, T a, T b) {
+  typename Vec2<T>::type v;
+  v.x = a;
+  v.y = b;
+  *reinterpret_cast<typename Vec2<T>::type*>(p) = v;
+}
+
 // Rotated leaf update (pivot column in register PC; the second step of a pair shifts the
 // registers two to the left and appends the two new D columns, as in K1).
-template <int W, int PC, bool SECOND>
-__device__ __forceinline__ void leaf_update(double (&x)[W], const double* y, double nf, double dcol) {
+template <typename T, int W, int PC, bool SECOND>
+__device__ __forceinline__ void leaf_update(T (&x)[W], const T* y, T nf, T dcol) {
   if constexpr (!SECOND) {
 #pragma unroll
     for (int j = 1; j < W; ++j) x[j] = fma(nf, y[j], x[j]);
     x[0] = dcol;
   } else {
-    const double c0 = fma(nf, y[0], x[0]);
+    const T c0 = fma(nf, y[0], x[0]);
 #pragma unroll
     for (int j = 0; j + 2 < W; ++j) x[j] = fma(nf, y[j + 2], x[j + 2]);
     x[W - 2] = c0;
@@ -242,15 +276,16 @@ __device__ __forceinline__ void leaf_update(double (&x)[W], const double* y, dou
   }
 }
 
-// Shared-memory layout of the leaf kernel (bytes)
-template <int W>
+// Shared-memory layout of the leaf kernel (bytes); T elements
+template <typename T, int W>
 struct LeafSmem {
-  static constexpr int EXW = W + 2;                       // entry: key (2 doubles) + W row values
+  static constexpr int KEYT = 16 / (int)sizeof(T);        // the 16-byte key in T units
+  static constexpr int EXW = W + KEYT;                    // entry: key + W row values (T units)
   static constexpr int RS = 0;                            // [W][PANEL_MAX] pivot rows of a leaf
-  static constexpr int PROW = RS + W * 128 * 8;           // [W] pivot row ids of the current leaf
-  static constexpr int WSLOT = PROW + W * 4;              // [kLeafThreads/32][EXW] doubles
-  static constexpr int EXCH = WSLOT + (kLeafThreads / 32) * EXW * 8;   // [2][CL][EXW]
-  static int bytes(int cl) { return EXCH + 2 * cl * EXW * 8 + 2 * 8 + 64; }
+  static constexpr int PROW = RS + W * 128 * (int)sizeof(T);   // [W] pivot row ids of the current leaf
+  static constexpr int WSLOT = (PROW + W * 4 + 15) / 16 * 16;  // [kLeafThreads/32][EXW]
+  static constexpr int EXCH = WSLOT + (kLeafThreads / 32) * EXW * (int)sizeof(T);   // [2][CL][EXW]
+  static int bytes(int cl) { return EXCH + 2 * cl * EXW * (int)sizeof(T) + 2 * 8 + 64; }
 };
 
 // K3 as one launch per PANEL: the panel's leaves one after another, each followed by its
@@ -259,29 +294,31 @@ struct LeafSmem {
 // programmatic dependents at once, so the trailing GEMM of the previous panel (launched
 // right after it with programmatic stream serialisation) runs on the other SMs while
 // this panel is factored (look-ahead).
-template <int W, int RPT>
+template <typename T, int W, int RPT>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  using LS = LeafSmem<W>;
+  using LS = LeafSmem<T, W>;
   constexpr int EXW = LS::EXW;
+  constexpr int KEYT = LS::KEYT;
+  T* const X = static_cast<T*>(a.X);
   extern __shared__ __align__(16) unsigned char smem[];
-  double* Rs = reinterpret_cast<double*>(smem + LS::RS);
+  T* Rs = reinterpret_cast<T*>(smem + LS::RS);
   int* prow = reinterpret_cast<int*>(smem + LS::PROW);
-  double* wslot = reinterpret_cast<double*>(smem + LS::WSLOT);
-  double* exch = reinterpret_cast<double*>(smem + LS::EXCH);
+  T* wslot = reinterpret_cast<T*>(smem + LS::WSLOT);
+  T* exch = reinterpret_cast<T*>(smem + LS::EXCH);
 
   const uint32_t rank = cluster_rank();
   const uint32_t CL = cluster_size();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LS::EXCH + 2 * CL * EXW * 8);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LS::EXCH + 2 * CL * EXW * (int)sizeof(T));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npad = a.npad, P0 = a.c0, pw = a.pw;
   const int64_t ld = a.ld;
-  const uint32_t entry_bytes = (uint32_t)(CL * EXW * 8);
+  const uint32_t entry_bytes = (uint32_t)(CL * EXW * (int)sizeof(T));
 
-  double x[RPT][W];
+  T x[RPT][W];
   int pos[RPT], pst[RPT], rowid[RPT];
   bool valid[RPT];
-  double myrp[RPT];
+  T myrp[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int r = (int)(rank * (kLeafThreads * RPT)) + i * kLeafThreads + tid;
@@ -305,18 +342,14 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     const int s0 = a.k0 + off;     // global step of the leaf's first column
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      myrp[i] = 1.0;
+      myrp[i] = T(1);
       if (valid[i]) {
-        const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)rowid[i] * ld + c0);
+        const T* src = X + (int64_t)rowid[i] * ld + c0;
 #pragma unroll
-        for (int j = 0; j < W; j += 2) {
-          const double2 v = src[j / 2];
-          x[i][j] = v.x;
-          x[i][j + 1] = v.y;
-        }
+        for (int j = 0; j < W; j += 2) ld2(src + j, x[i][j], x[i][j + 1]);
       } else {
 #pragma unroll
-        for (int j = 0; j < W; ++j) x[i][j] = 0.0;
+        for (int j = 0; j < W; ++j) x[i][j] = T(0);
       }
     }
     auto step = [&](int kk, auto pc_tag, auto second_tag) {
@@ -331,8 +364,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         if (valid[i] && pst[i] < 0) {
-          const unsigned long long u = (unsigned long long)__double_as_longlong(x[i][PC]) & 0x7fffffffffffffffull;
-          const Cand c{(uint32_t)(u >> 32), (uint32_t)u, (uint32_t)pos[i], (uint32_t)rowid[i]};
+          uint32_t kh, kl;
+          abs_key(x[i][PC], kh, kl);
+          const Cand c{kh, kl, (uint32_t)pos[i], (uint32_t)rowid[i]};
           if (bi < 0 || better(c, best)) { best = c; bi = i; }
         }
       }
@@ -343,7 +377,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
       // the warp winner writes key + row into its slot (then fences them into the async
       // proxy: warp 0 ships the CTA winner's slot with cp.async.bulk)
       const bool wwin = has && best.pos == pw_;
-      double* slot = wslot + warp * EXW;
+      T* slot = wslot + warp * EXW;
       if (pw_ == 0xffffffffu) {
         if (lane == 0) reinterpret_cast<uint4*>(slot)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
       } else {
@@ -352,7 +386,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
           if (wwin && bi == i) {
             reinterpret_cast<uint4*>(slot)[0] = make_uint4(best.hi, best.lo, best.pos, best.row);
 #pragma unroll
-            for (int j = 0; j < W; j += 2) reinterpret_cast<double2*>(slot + 2)[j / 2] = make_double2(x[i][j], x[i][j + 1]);
+            for (int j = 0; j < W; j += 2) st2(slot + KEYT + j, x[i][j], x[i][j + 1]);
           }
         }
       }
@@ -371,13 +405,13 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         const uint32_t src = smem_u32(wslot + src_warp * EXW);
         if (lane < (int)CL) {
           const uint32_t ldst = smem_u32(exch + (size_t)(b * CL + rank) * EXW);
-          bulk_s2c(map_remote(ldst, (uint32_t)lane), src, (uint32_t)(EXW * 8), map_remote(smem_u32(&bars[b]), (uint32_t)lane));
+          bulk_s2c(map_remote(ldst, (uint32_t)lane), src, (uint32_t)(EXW * (int)sizeof(T)), map_remote(smem_u32(&bars[b]), (uint32_t)lane));
         }
       }
       // ---- all: wait for the CL entries of this step, pick the cluster winner
       mbar_wait_all(&bars[b], (uint32_t)((gk >> 1) & 1));
       if (tid == 0) mbar_expect_tx(&bars[b], entry_bytes);   // arm the barrier for step gk + 2
-      const double* ex0 = exch + (size_t)(b * CL) * EXW;
+      const T* ex0 = exch + (size_t)(b * CL) * EXW;
       Cand cc{0u, 0u, 0xffffffffu, 0u};
       if (lane < (int)CL) {
         const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)lane * EXW);
@@ -388,18 +422,18 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         const uint4 k4 = *reinterpret_cast<const uint4*>(ex0 + (size_t)wr * EXW);
         return Cand{k4.x, k4.y, k4.z, k4.w};
       }();
-      const double* y = ex0 + (size_t)wr * EXW + 2;
-      const double p = y[PC];
+      const T* y = ex0 + (size_t)wr * EXW + KEYT;
+      const T p = y[PC];
       const int q = (int)wc.pos;
       if (tid == 0) {
         prow[kk] = (int)wc.row;
         if (rank == 0) {
-          a.rec_p[kg] = p;
+          a.rec_p[kg] = (double)p;
           a.rec_q[kg] = q;
           a.rec_row[kg] = (int)wc.row;
         }
       }
-      const double rp = rcp_f64(p);
+      const T rp = rcp_t(p);
       // ---- a3 + a5
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
@@ -410,9 +444,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
           pst[i] = kg;
           myrp[i] = rp;
         }
-        const double nf = is_piv ? 0.0 : -(x[i][PC] * rp);
-        const double dcol = is_piv ? 1.0 : nf;
-        leaf_update<W, PC, SECOND>(x[i], y, nf, dcol);
+        const T nf = is_piv ? T(0) : -(x[i][PC] * rp);
+        const T dcol = is_piv ? T(1) : nf;
+        leaf_update<T, W, PC, SECOND>(x[i], y, nf, dcol);
       }
     };
 #pragma unroll 1
@@ -423,13 +457,13 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     // deferred normalisation of this leaf's pivot rows; write back the leaf columns (W)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const double sc = (pst[i] >= s0 && pst[i] < s0 + W) ? myrp[i] : 1.0;
+      const T sc = (pst[i] >= s0 && pst[i] < s0 + W) ? myrp[i] : T(1);
 #pragma unroll
       for (int j = 0; j < W; ++j) x[i][j] *= sc;
       if (!valid[i]) continue;
-      double2* dst = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * ld + c0);
+      T* dst = X + (int64_t)rowid[i] * ld + c0;
 #pragma unroll
-      for (int j = 0; j < W; j += 2) dst[j / 2] = make_double2(x[i][j], x[i][j + 1]);
+      for (int j = 0; j < W; j += 2) st2(dst + j, x[i][j], x[i][j + 1]);
     }
     if (pw > W) {
       // the leaf's transformation on the panel's other columns (left: D columns of earlier
@@ -438,8 +472,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
       const int half = pw / 2;
       for (int e = tid; e < W * half; e += kLeafThreads) {
         const int sidx = e / half, cc2 = e - sidx * half;
-        reinterpret_cast<double2*>(Rs + sidx * 128)[cc2] =
-            reinterpret_cast<const double2*>(a.X + (int64_t)prow[sidx] * ld + P0)[cc2];
+        T u0, u1;
+        ld2(X + (int64_t)prow[sidx] * ld + P0 + 2 * cc2, u0, u1);
+        st2(Rs + sidx * 128 + 2 * cc2, u0, u1);
       }
       cluster_sync_all();   // every CTA has its copy before any CTA rewrites a pivot row
 #pragma unroll 1
@@ -449,26 +484,30 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         for (int i = 0; i < RPT; ++i) {
           if (!valid[i]) continue;
           const bool rep = pst[i] >= s0 && pst[i] < s0 + W;   // pivot row of this leaf: replaced
-          double2* row = reinterpret_cast<double2*>(a.X + (int64_t)rowid[i] * ld + P0 + t0);
-          double v[8];
+          T* row = X + (int64_t)rowid[i] * ld + P0 + t0;
+          T v[8];
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
-            const double2 u = rep ? make_double2(0.0, 0.0) : row[j / 2];
-            v[j] = u.x;
-            v[j + 1] = u.y;
-          }
-#pragma unroll
-          for (int sidx = 0; sidx < W; ++sidx) {
-            const double2* rr = reinterpret_cast<const double2*>(Rs + sidx * 128 + t0);
-#pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-              const double2 r2 = rr[j / 2];
-              v[j] = fma(x[i][sidx], r2.x, v[j]);
-              v[j + 1] = fma(x[i][sidx], r2.y, v[j + 1]);
+            if (rep) {
+              v[j] = T(0);
+              v[j + 1] = T(0);
+            } else {
+              ld2(row + j, v[j], v[j + 1]);
             }
           }
 #pragma unroll
-          for (int j = 0; j < 8; j += 2) row[j / 2] = make_double2(v[j], v[j + 1]);
+          for (int sidx = 0; sidx < W; ++sidx) {
+            const T* rr = Rs + sidx * 128 + t0;
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+              T r0, r1;
+              ld2(rr + j, r0, r1);
+              v[j] = fma(x[i][sidx], r0, v[j]);
+              v[j + 1] = fma(x[i][sidx], r1, v[j + 1]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) st2(row + j, v[j], v[j + 1]);
         }
       }
       __syncthreads();   // Rs / prow are rewritten by the next leaf
@@ -480,9 +519,13 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     a.pos[rowid[i]] = pos[i];
     a.pivstep[rowid[i]] = pst[i];
     if (a.Wout != nullptr) {   // this thread wrote every final panel value of its rows itself
-      const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)rowid[i] * ld + P0);
-      double2* dst = reinterpret_cast<double2*>(a.Wout + (int64_t)rowid[i] * pw);
-      for (int j = 0; j < pw / 2; ++j) dst[j] = src[j];
+      const T* src = X + (int64_t)rowid[i] * ld + P0;
+      T* dst = static_cast<T*>(a.Wout) + (int64_t)rowid[i] * pw;
+      for (int j = 0; j < pw; j += 2) {
+        T u0, u1;
+        ld2(src + j, u0, u1);
+        st2(dst + j, u0, u1);
+      }
     }
   }
   cluster_sync_all();   // no CTA leaves while a peer's bulk copy may still target it
@@ -689,13 +732,13 @@ static Workspace carve(void* ws, int npad) {
   return w;
 }
 
-template <int W, int RPT>
+template <int W, int RPT, typename T = double>
 static cudaError_t launch_leaf(const LeafArgs& la, int cl, cudaStream_t s) {
-  const size_t smem = (size_t)LeafSmem<W>::bytes(cl);
+  const size_t smem = (size_t)LeafSmem<T, W>::bytes(cl);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(leaf_kernel<W, RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(leaf_kernel<W, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(leaf_kernel<T, W, RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(leaf_kernel<T, W, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -710,7 +753,7 @@ static cudaError_t launch_leaf(const LeafArgs& la, int cl, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, leaf_kernel<W, RPT>, la);
+  return cudaLaunchKernelEx(&cfg, leaf_kernel<T, W, RPT>, la);
 }
 
 // grid_sms: SMs the persistent grid may use; pdl: launch as a programmatic dependent of the
@@ -770,6 +813,174 @@ static bool debug_sync() {
   } while (0)
 
 }  // namespace large
+
+// ============================================================================ fp32 (f1)
+// The same blocked Gauss-Jordan in fp32: the panel kernel instantiated for
+// float, the trailing update on tcgen05 TF32 tensor cores with a 3xTF32 split
+// (gj_tcgemm.cu).  npad is a multiple of 128 (whole tensor-core tiles of K = 128).
+namespace f32 {
+constexpr int PANEL = large::PANEL;
+
+__global__ void copy_pad_f32(const float* __restrict__ A, int64_t lda, int n, float* __restrict__ X, int npad,
+                             unsigned long long* smax) {
+  float m = 0.0f;
+  const int64_t tot = (int64_t)npad * npad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / npad), j = (int)(e - (int64_t)i * npad);
+    float v;
+    if (i < n && j < n) {
+      v = A[(int64_t)i * lda + j];
+      m = fmaxf(m, fabsf(v));
+    } else {
+      v = (i == j) ? 1.0f : 0.0f;
+    }
+    X[e] = v;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong((double)m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+    b = ob > b ? ob : b;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(smax, b);
+}
+
+// x = hi + lo with hi exactly representable in TF32 (low 13 mantissa bits cleared)
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+  lo = x - hi;
+}
+
+// Ah/Al (npad x 128) = split X[:, P0 .. P0 + 128)
+__global__ void split_panel_f32(const float* __restrict__ X, int npad, int P0, float* __restrict__ Ah,
+                                float* __restrict__ Al) {
+  const int64_t tot = (int64_t)npad * PANEL;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / PANEL), k = (int)(e - (int64_t)i * PANEL);
+    float h, l;
+    split_tf32(X[(int64_t)i * npad + P0 + k], h, l);
+    Ah[e] = h;
+    Al[e] = l;
+  }
+}
+
+// Bh/Bl (npad x 128): B[c][s] = split X[rows[s]][c]  (R transposed, through a 32 x 32 tile)
+__global__ void gather_split_T_f32(const float* __restrict__ X, int npad, const int* __restrict__ rows,
+                                   float* __restrict__ Bh, float* __restrict__ Bl) {
+  __shared__ float t[32][33];
+  const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  for (int j = ty; j < 32; j += 8) t[j][tx] = X[(int64_t)rows[s0 + j] * npad + c0 + tx];
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    float h, l;
+    split_tf32(t[tx][j], h, l);
+    Bh[(int64_t)(c0 + j) * PANEL + s0 + tx] = h;
+    Bl[(int64_t)(c0 + j) * PANEL + s0 + tx] = l;
+  }
+}
+
+__global__ void unpermute_f32(const float* __restrict__ X, int npad, const int* __restrict__ rec_row,
+                              const int* __restrict__ pivstep, int n, float* __restrict__ Y, int64_t ldy) {
+  const int k = blockIdx.y;
+  const float* src = X + (int64_t)rec_row[k] * npad;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    Y[(int64_t)k * ldy + j] = src[pivstep[j]];
+}
+
+__global__ void finalize_det_f32(const double* logabsdet, const int8_t* sign, float* det) {
+  *det = *sign == 0 ? 0.0f : (float)((double)*sign * exp(*logabsdet));
+}
+
+struct Workspace {
+  float *X, *Ah, *Al, *Bh, *Bl;
+  double* rec_p;
+  int *rec_q, *rec_row, *pos, *pivstep;
+  unsigned long long* smax;
+  double* lg;
+  int8_t* sg;
+};
+static int pad128(int n) { return (n + 127) / 128 * 128; }
+static size_t bytes(int n) {
+  const size_t np = (size_t)pad128(n);
+  return np * np * 4 + 4 * np * PANEL * 4 + np * 8 + 4 * np * 4 + 64 + 16 * 256 + 1024;
+}
+static Workspace carve(void* ws, int npad) {
+  Workspace w;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += (b + 255) / 256 * 256;
+    return r;
+  };
+  w.X = reinterpret_cast<float*>(take((size_t)npad * npad * 4));
+  w.Ah = reinterpret_cast<float*>(take((size_t)npad * PANEL * 4));
+  w.Al = reinterpret_cast<float*>(take((size_t)npad * PANEL * 4));
+  w.Bh = reinterpret_cast<float*>(take((size_t)npad * PANEL * 4));
+  w.Bl = reinterpret_cast<float*>(take((size_t)npad * PANEL * 4));
+  w.rec_p = reinterpret_cast<double*>(take((size_t)npad * 8));
+  w.rec_q = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.rec_row = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.pos = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.pivstep = reinterpret_cast<int*>(take((size_t)npad * 4));
+  w.smax = reinterpret_cast<unsigned long long*>(take(8));
+  w.lg = reinterpret_cast<double*>(take(8));
+  w.sg = reinterpret_cast<int8_t*>(take(8));
+  return w;
+}
+}  // namespace f32
+
+size_t large_workspace_size_f32(int n) { return f32::bytes(n); }
+
+cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, int64_t ldainv, int32_t* ipiv,
+                             double* logabsdet, int8_t* sign, float* det, int32_t* info, double tol, void* ws_ptr,
+                             cudaStream_t s) {
+  using large::LeafCfg;
+  using large::LeafArgs;
+  using large::leaf_cfg;
+  using large::launch_leaf;
+  constexpr int PANEL = f32::PANEL;
+  const int npad = f32::pad128(n);
+  LeafCfg lc;
+  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
+  f32::Workspace w = f32::carve(ws_ptr, npad);
+  cudaError_t e;
+  const int sms = device_sm_count();
+  large::init_perm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(npad, w.pos, w.pivstep);
+  cudaMemsetAsync(w.smax, 0, 8, s);
+  f32::copy_pad_f32<<<sms * 8, 256, 0, s>>>(A, lda, n, w.X, npad, w.smax);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  auto factor_panel = [&](int P0) -> cudaError_t {
+    LeafArgs la{w.X, npad, npad, P0, P0, PANEL, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
+    if (lc.w == 32) return launch_leaf<32, 1, float>(la, lc.cl, s);
+    if (lc.w == 16) return launch_leaf<16, 2, float>(la, lc.cl, s);
+    return launch_leaf<8, 4, float>(la, lc.cl, s);
+  };
+  if ((e = factor_panel(0)) != cudaSuccess) return e;
+  for (int P0 = 0; P0 < npad; P0 += PANEL) {
+    const int P1 = P0 + PANEL;
+    const bool nxt = P1 < npad;
+    f32::split_panel_f32<<<sms * 4, 256, 0, s>>>(w.X, npad, P0, w.Ah, w.Al);
+    f32::gather_split_T_f32<<<dim3(npad / 32, PANEL / 32), dim3(32, 8), 0, s>>>(w.X, npad, w.rec_row + P0, w.Bh, w.Bl);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (nxt) {
+      TcUpdateArgs ga{w.Ah, w.Al, w.Bh, w.Bl, w.X, npad, npad, PANEL, npad, w.pivstep, P0, P0 + PANEL, 0, P1};
+      if ((e = launch_tc_update(ga, 0, false, s)) != cudaSuccess) return e;
+      if ((e = factor_panel(P1)) != cudaSuccess) return e;
+    }
+    const int pw1 = nxt ? PANEL : 0;
+    TcUpdateArgs gb{w.Ah, w.Al, w.Bh, w.Bl, w.X, npad, npad, npad - PANEL - pw1, npad, w.pivstep, P0, P0 + PANEL,
+                    P0, P1 + pw1};
+    if ((e = launch_tc_update(gb, nxt ? sms - lc.cl : 0, nxt, s)) != cudaSuccess) return e;
+  }
+  if (Ainv != nullptr)
+    f32::unpermute_f32<<<dim3((n + 255) / 256, n), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
+  large::finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet ? logabsdet : w.lg,
+                                     sign ? sign : w.sg, nullptr, info);
+  if (det != nullptr)
+    f32::finalize_det_f32<<<1, 1, 0, s>>>(logabsdet ? logabsdet : w.lg, sign ? sign : w.sg, det);
+  return cudaGetLastError();
+}
 
 size_t large_workspace_size(int n) { return large::workspace_bytes(n); }
 
