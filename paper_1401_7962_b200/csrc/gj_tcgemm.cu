@@ -7,11 +7,13 @@
 // Wl Rl and the TF32 rounding of the low parts are ~2^-21 of |W||R|).
 // The operands arrive split and K-major (Ah/Al: M x 128, Bh/Bl: N x 128; B is R
 // transposed) — gj_large.cu's split / transposed-gather kernels write them per panel.
-// One CTA per SM (persistent over 128 x 64 tiles): TMA loads the whole K = 128 of both
-// operands (128-byte swizzle, 192 KB), one elected thread issues 48 tcgen05.mma
-// (4 k-blocks x 4 k-steps x 3 products) into a 128-lane x 64-column fp32 TMEM
-// accumulator, tcgen05.commit signals an mbarrier, and four warps read the accumulator
-// back with tcgen05.ld (warp w <-> TMEM lanes 32w..32w+31 = tile rows) and update C.
+// One CTA per SM, warp-specialised: warp 4 issues the TMA loads (the row block's Ah/Al,
+// 128 KB, resident for a whole work unit; B tiles of 128 x 32 through two 32 KB stages),
+// one thread of warp 5 issues 48 tcgen05.mma per tile (4 k-blocks x 4 k-steps x 3
+// products) into one of two 128-lane x 32-column fp32 TMEM accumulators and signals
+// mbarriers with tcgen05.commit, and warps 0-3 read the accumulator back with tcgen05.ld
+// (warp w <-> TMEM lanes 32w..32w+31 = tile rows) and update C while the next tile's
+// MMAs run.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -24,11 +26,13 @@ namespace tc {
 
 using namespace ptx;
 
-constexpr int TM = 128, TN = 64, TK = 128, KB = 32;
+constexpr int TM = 128, TN = 32, TK = 128, KB = 32, NKB = TK / KB;
 constexpr int A_BLK = TM * KB * 4;                  // 16 KB: one k-block of Ah (or Al)
-constexpr int B_BLK = TN * KB * 4;                  // 8 KB
-constexpr int SMEM = 2 * (TK / KB) * (A_BLK + B_BLK) + 1024 + 64;
-constexpr int kThreads = 128;
+constexpr int B_BLK = TN * KB * 4;                  // 4 KB
+constexpr int B_STAGE = 2 * NKB * B_BLK;            // Bh + Bl of one column tile: 32 KB
+constexpr int SMEM = 2 * NKB * A_BLK + 2 * B_STAGE + 1024;
+constexpr int kEpiWarps = 4;                        // warps 0-3: epilogue (TMEM lane quarters)
+constexpr int kThreads = (kEpiWarps + 2) * 32;      // warp 4: TMA producer, warp 5: MMA issuer
 
 // Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
@@ -47,28 +51,48 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t ad, uint64_t bd
   asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
                ::"r"(tmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
 }
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 struct Maps {
   CUtensorMap ah, al, bh, bl;
 };
 
+// Work unit = (row block, contiguous range of column tiles): A of the row block stays in
+// shared memory for the whole unit; B tiles stream through two stages; the accumulator is
+// double-buffered in TMEM so the epilogue of tile t overlaps the MMAs of tile t+1.
 __global__ void __launch_bounds__(kThreads, 1) tc_update_kernel(const __grid_constant__ Maps mp, TcUpdateArgs g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sAh = base;
-  unsigned char* sAl = sAh + (TK / KB) * A_BLK;
-  unsigned char* sBh = sAl + (TK / KB) * A_BLK;
-  unsigned char* sBl = sBh + (TK / KB) * B_BLK;
-  __shared__ uint64_t bar_tma, bar_mma;
+  unsigned char* sAl = sAh + NKB * A_BLK;
+  unsigned char* sB = sAl + NKB * A_BLK;   // [stage][h/l][kb][TN x KB]
+  __shared__ uint64_t a_full, a_empty, b_full[2], b_empty[2], t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(TN));
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "n"(2 * TN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 32) {
-    mbar_init(&bar_tma, 1);
-    mbar_init(&bar_mma, 1);
+  if (tid == 128) {
+    mbar_init(&a_full, 1);
+    mbar_init(&a_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], kEpiWarps);
+    }
     fence_mbar_init();
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -78,87 +102,136 @@ __global__ void __launch_bounds__(kThreads, 1) tc_update_kernel(const __grid_con
 
   const int ntn = (g.N + TN - 1) / TN, ntm = (g.M + TM - 1) / TM;
   const int shift = g.skip_hi - g.skip_lo;
-  int it = 0;
-  for (int tile = blockIdx.x; tile < ntn * ntm; tile += gridDim.x, ++it) {
-    const int m0 = (tile % ntm) * TM;
-    const int nc0 = (tile / ntm) * TN;                    // compact column of the tile
-    const int n0 = nc0 + (nc0 >= g.skip_lo ? shift : 0);  // real column
-    const int nlim = n0 + (g.N - nc0);
-    if (tid == 0) {
-      mbar_expect_tx(&bar_tma, 2 * (TK / KB) * (A_BLK + B_BLK));
-#pragma unroll
-      for (int kb = 0; kb < TK / KB; ++kb) {
-        tma_load_2d(sAh + kb * A_BLK, &mp.ah, kb * KB, m0, &bar_tma);
-        tma_load_2d(sAl + kb * A_BLK, &mp.al, kb * KB, m0, &bar_tma);
-        tma_load_2d(sBh + kb * B_BLK, &mp.bh, kb * KB, n0, &bar_tma);
-        tma_load_2d(sBl + kb * B_BLK, &mp.bl, kb * KB, n0, &bar_tma);
-      }
-    }
-    while (!mbar_try_wait(&bar_tma, it & 1)) {
-    }
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      uint32_t acc = 0;
-#pragma unroll
-      for (int kb = 0; kb < TK / KB; ++kb) {
-#pragma unroll
-        for (int kk = 0; kk < KB / 8; ++kk) {
-          const uint64_t ah = desc_k_sw128(smem_u32(sAh + kb * A_BLK) + kk * 32);
-          const uint64_t al = desc_k_sw128(smem_u32(sAl + kb * A_BLK) + kk * 32);
-          const uint64_t bh = desc_k_sw128(smem_u32(sBh + kb * B_BLK) + kk * 32);
-          const uint64_t bl = desc_k_sw128(smem_u32(sBl + kb * B_BLK) + kk * 32);
-          mma_tf32(tmem, al, bh, acc);   // small products first
-          acc = 1;
-          mma_tf32(tmem, ah, bl, 1);
-          mma_tf32(tmem, ah, bh, 1);
+  // units: each row block's column tiles split into `cpr` contiguous parts
+  const int cpr = gridDim.x >= ntm ? (int)gridDim.x / ntm : 1;
+  const int nunits = ntm * cpr;
+  auto unit_range = [&](int u, int& rb, int& t0, int& t1) {
+    rb = u / cpr;
+    const int part = u % cpr;
+    t0 = (int)((int64_t)ntn * part / cpr);
+    t1 = (int)((int64_t)ntn * (part + 1) / cpr);
+  };
+  auto real_col = [&](int ct) {
+    const int nc0 = ct * TN;
+    return nc0 + (nc0 >= g.skip_lo ? shift : 0);
+  };
+
+  if (warp == 4) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int ua = 0, tb = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ua) {
+        int rb, t0, t1;
+        unit_range(u, rb, t0, t1);
+        wait(&a_empty, (ua & 1) ^ 1);
+        mbar_expect_tx(&a_full, 2 * NKB * A_BLK);
+        for (int kb = 0; kb < NKB; ++kb) {
+          tma_load_2d(sAh + kb * A_BLK, &mp.ah, kb * KB, rb * TM, &a_full);
+          tma_load_2d(sAl + kb * A_BLK, &mp.al, kb * KB, rb * TM, &a_full);
         }
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar_mma))
-                   : "memory");
-    }
-    while (!mbar_try_wait(&bar_mma, it & 1)) {
-    }
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    // epilogue: warp w reads tile rows 32w..32w+31 (TMEM lanes), 64 columns
-    const int r = m0 + warp * 32 + lane;
-    bool keep = r < g.M;
-    if (keep) {
-      const int ps = g.pivstep[r];
-      keep = !(ps >= g.rep_lo && ps < g.rep_hi);
-    }
-#pragma unroll
-    for (int c = 0; c < TN; c += 16) {
-      uint32_t v[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-            "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
-      asm volatile("tcgen05.wait::ld.sync.aligned;");
-      if (r < g.M) {
-        float* crow = g.C + (int64_t)r * g.ldc + n0 + c;
-#pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-          if (n0 + c + j + 3 < nlim) {
-            float4 o = keep ? *reinterpret_cast<const float4*>(crow + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-            o.x += __uint_as_float(v[j]);
-            o.y += __uint_as_float(v[j + 1]);
-            o.z += __uint_as_float(v[j + 2]);
-            o.w += __uint_as_float(v[j + 3]);
-            *reinterpret_cast<float4*>(crow + j) = o;
-          } else {
-            for (int u = 0; u < 4; ++u)
-              if (n0 + c + j + u < nlim) crow[j + u] = (keep ? crow[j + u] : 0.f) + __uint_as_float(v[j + u]);
+        for (int t = t0; t < t1; ++t, ++tb) {
+          const int st = tb & 1;
+          wait(&b_empty[st], ((tb >> 1) & 1) ^ 1);
+          unsigned char* sb = sB + st * B_STAGE;
+          mbar_expect_tx(&b_full[st], B_STAGE);
+          const int n0 = real_col(t);
+          for (int kb = 0; kb < NKB; ++kb) {
+            tma_load_2d(sb + kb * B_BLK, &mp.bh, kb * KB, n0, &b_full[st]);
+            tma_load_2d(sb + (NKB + kb) * B_BLK, &mp.bl, kb * KB, n0, &b_full[st]);
           }
         }
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();   // TMEM read and smem consumed before the next tile's loads / MMAs
-    asm volatile("tcgen05.fence::after_thread_sync;");
+  } else if (warp == 5) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      int ua = 0, tb = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ua) {
+        int rb, t0, t1;
+        unit_range(u, rb, t0, t1);
+        wait(&a_full, ua & 1);
+        for (int t = t0; t < t1; ++t, ++tb) {
+          const int st = tb & 1, ac = tb & 1;
+          wait(&b_full[st], (tb >> 1) & 1);
+          wait(&t_empty[ac], ((tb >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t d = tmem + (uint32_t)(ac * TN);
+          const uint32_t sb = smem_u32(sB + st * B_STAGE);
+          uint32_t acc = 0;
+#pragma unroll
+          for (int kb = 0; kb < NKB; ++kb) {
+#pragma unroll
+            for (int kk = 0; kk < KB / 8; ++kk) {
+              const uint64_t ah = desc_k_sw128(smem_u32(sAh + kb * A_BLK) + kk * 32);
+              const uint64_t al = desc_k_sw128(smem_u32(sAl + kb * A_BLK) + kk * 32);
+              const uint64_t bh = desc_k_sw128(sb + kb * B_BLK + kk * 32);
+              const uint64_t bl = desc_k_sw128(sb + (NKB + kb) * B_BLK + kk * 32);
+              mma_tf32(d, al, bh, acc);   // the small products first
+              acc = 1;
+              mma_tf32(d, ah, bl, 1);
+              mma_tf32(d, ah, bh, 1);
+            }
+          }
+          mma_commit(&b_empty[st]);   // the B stage may be refilled
+          mma_commit(&t_full[ac]);    // the accumulator is ready
+        }
+        mma_commit(&a_empty);         // A of this unit no longer read
+      }
+    }
+  } else {
+    // ---------------- epilogue: warp w <-> TMEM lanes (rows) 32w..32w+31
+    int tb = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      int rb, t0, t1;
+      unit_range(u, rb, t0, t1);
+      const int r = rb * TM + warp * 32 + lane;
+      bool keep = r < g.M;
+      if (keep) {
+        const int ps = g.pivstep[r];
+        keep = !(ps >= g.rep_lo && ps < g.rep_hi);
+      }
+      for (int t = t0; t < t1; ++t, ++tb) {
+        const int ac = tb & 1;
+        wait(&t_full[ac], (tb >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint32_t v[TN];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ac * TN)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) arrive(&t_empty[ac]);   // the TMEM buffer may be overwritten
+        const int n0 = real_col(t);
+        const int nlim = n0 + (g.N - t * TN);
+        if (r < g.M) {
+          float* crow = g.C + (int64_t)r * g.ldc + n0;
+#pragma unroll
+          for (int j = 0; j < TN; j += 4) {
+            if (n0 + j + 3 < nlim) {
+              float4 o = keep ? *reinterpret_cast<const float4*>(crow + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+              o.x += __uint_as_float(v[j]);
+              o.y += __uint_as_float(v[j + 1]);
+              o.z += __uint_as_float(v[j + 2]);
+              o.w += __uint_as_float(v[j + 3]);
+              *reinterpret_cast<float4*>(crow + j) = o;
+            } else {
+              for (int q = 0; q < 4; ++q)
+                if (n0 + j + q < nlim) crow[j + q] = (keep ? crow[j + q] : 0.f) + __uint_as_float(v[j + q]);
+            }
+          }
+        }
+      }
+    }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TN));
+  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TN));
   // launched as a programmatic dependent of the panel kernel: complete only after it
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -181,9 +254,12 @@ cudaError_t launch_tc_update(const TcUpdateArgs& g, int grid_sms, bool pdl, cuda
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int tiles = ((g.N + TN - 1) / TN) * ((g.M + TM - 1) / TM);
+  const int ntm = (g.M + TM - 1) / TM, ntn = (g.N + TN - 1) / TN;
   const int sms = grid_sms > 0 ? grid_sms : device_sm_count();
-  const int grid = tiles < sms ? tiles : sms;
+  // units of (row block, column range): as many as SMs when there are fewer row blocks
+  const int cpr = ntm >= sms ? 1 : (sms / ntm < ntn ? sms / ntm : ntn);
+  const int units = ntm * cpr;
+  const int grid = units < sms ? units : sms;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
