@@ -188,6 +188,39 @@ def c4_measure(dev, reps: int = 3):
                          "kernel": "whole gj_invert (leaf_kernel panels overlapped with gemm_update_kernel DMMA)"}}
 
 
+def f1_measure(dev, reps: int = 3):
+    """SURVEY §8f f1 (NEXT row, not a BASELINE config): one fp32 8192 x 8192 N(0,1)/sqrt(n)
+    matrix through gj_invert — fp32 panel kernel + tcgen05 kind::tf32 trailing update
+    (3xTF32).  Peak: TF32 dense = measured bf16 x (1.1 / 2.25) nominal ratio, / 3 products."""
+    import torch
+    import paper_1401_7962_b200 as gj
+    import synth
+    n = 8192
+    A = torch.from_numpy(synth.gen_gaussian(n, seed=3).astype(np.float32)).to(dev)
+    X = torch.empty_like(A)
+    gj.invert(A, out=X)
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        gj.invert(A, out=X)
+        b.record()
+        torch.cuda.synchronize(dev)
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    tf = (2.0 * n ** 3 - n ** 2) / (ms / 1e3) / 1e12
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    bf16 = json.load(open(path))["bf16_tflops"] if os.path.exists(path) else 1590.0
+    peak = bf16 * 1.1 / 2.25 / 3.0
+    return {"workload": "f1: one fp32 8192x8192 N(0,1)/sqrt(n) (SURVEY §8f f1; not a BASELINE config)",
+            "metric": "fp32 GFLOP/s at n=8192", "value": tf * 1e3, "unit": "GFLOP/s", "ms": ms,
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                         "traffic": None,
+                         "peak_source": "measured bf16 (MEASURED_PEAKS.json) x nominal tf32/bf16 1.1/2.25, / 3 (3xTF32)",
+                         "note": "panel-latency bound: the pivot chain, not the tensor pipe, sets the time"}}
+
+
 def cpu_baseline(sample: int, A_host=None):
     """The oracle as it stands, on the host's cores, on the first `sample` items of C2."""
     import oracle
@@ -410,6 +443,7 @@ def main():
                 "roofline": roof, "gpu_launches": args.steps, "clocks": clk.summary(), "e2e": e2e}
         if not args.no_c4:
             line["secondary"] = c4_measure(dev)
+            line["next_f1"] = f1_measure(dev)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample, A_host)
         print(json.dumps(line), flush=True)

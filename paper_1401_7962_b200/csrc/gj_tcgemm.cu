@@ -31,8 +31,10 @@ constexpr int A_BLK = TM * KB * 4;                  // 16 KB: one k-block of Ah 
 constexpr int B_BLK = TN * KB * 4;                  // 4 KB
 constexpr int B_STAGE = 2 * NKB * B_BLK;            // Bh + Bl of one column tile: 32 KB
 constexpr int SMEM = 2 * NKB * A_BLK + 2 * B_STAGE + 1024;
-constexpr int kEpiWarps = 4;                        // warps 0-3: epilogue (TMEM lane quarters)
-constexpr int kThreads = (kEpiWarps + 2) * 32;      // warp 4: TMA producer, warp 5: MMA issuer
+constexpr int kEpiWarps = 8;                        // warps 0-7: epilogue (lane quarter w % 4, column half w / 4)
+constexpr int kPW = kEpiWarps, kMW = kEpiWarps + 1; // producer warp, MMA warp
+constexpr int kThreads = (kEpiWarps + 2) * 32;
+constexpr int EC = TN / 2;                          // columns per epilogue thread
 
 // Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
@@ -79,12 +81,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_update_kernel(const __grid_con
   __shared__ uint64_t a_full, a_empty, b_full[2], b_empty[2], t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 5) {
+  if (warp == kMW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "n"(2 * TN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 128) {
+  if (tid == kPW * 32) {
     mbar_init(&a_full, 1);
     mbar_init(&a_empty, 1);
     for (int i = 0; i < 2; ++i) {
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_update_kernel(const __grid_con
     return nc0 + (nc0 >= g.skip_lo ? shift : 0);
   };
 
-  if (warp == 4) {
+  if (warp == kPW) {
     // ---------------- TMA producer
     if (lane == 0) {
       int ua = 0, tb = 0;
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_update_kernel(const __grid_con
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMW) {
     // ---------------- MMA issuer (one thread)
     if (lane == 0) {
       int ua = 0, tb = 0;
@@ -179,12 +181,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_update_kernel(const __grid_con
       }
     }
   } else {
-    // ---------------- epilogue: warp w <-> TMEM lanes (rows) 32w..32w+31
+    // ---------------- epilogue: warp w <-> TMEM lanes (rows) 32(w%4).., columns 16(w/4)..
+    const int quarter = warp & 3, half = warp >> 2;
     int tb = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       int rb, t0, t1;
       unit_range(u, rb, t0, t1);
-      const int r = rb * TM + warp * 32 + lane;
+      const int r = rb * TM + quarter * 32 + lane;
       bool keep = r < g.M;
       if (keep) {
         const int ps = g.pivstep[r];
@@ -192,46 +195,47 @@ __global__ void __launch_bounds__(kThreads, 1) tc_update_kernel(const __grid_con
       }
       for (int t = t0; t < t1; ++t, ++tb) {
         const int ac = tb & 1;
+        const int n0 = real_col(t) + half * EC;
+        const int nlim = real_col(t) + (g.N - t * TN);
+        float* crow = g.C + (int64_t)r * g.ldc + n0;
+        const bool full = r < g.M && n0 + EC <= nlim;
+        // C of this tile while the MMAs run
+        float4 cv[EC / 4];
+#pragma unroll
+        for (int j = 0; j < EC / 4; ++j)
+          cv[j] = (full && keep) ? *reinterpret_cast<const float4*>(crow + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
         wait(&t_full[ac], (tb >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        uint32_t v[TN];
+        uint32_t v[EC];
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ac * TN)));
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ac * TN + half * EC)));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) arrive(&t_empty[ac]);   // the TMEM buffer may be overwritten
-        const int n0 = real_col(t);
-        const int nlim = n0 + (g.N - t * TN);
-        if (r < g.M) {
-          float* crow = g.C + (int64_t)r * g.ldc + n0;
+        if (full) {
 #pragma unroll
-          for (int j = 0; j < TN; j += 4) {
-            if (n0 + j + 3 < nlim) {
-              float4 o = keep ? *reinterpret_cast<const float4*>(crow + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-              o.x += __uint_as_float(v[j]);
-              o.y += __uint_as_float(v[j + 1]);
-              o.z += __uint_as_float(v[j + 2]);
-              o.w += __uint_as_float(v[j + 3]);
-              *reinterpret_cast<float4*>(crow + j) = o;
-            } else {
-              for (int q = 0; q < 4; ++q)
-                if (n0 + j + q < nlim) crow[j + q] = (keep ? crow[j + q] : 0.f) + __uint_as_float(v[j + q]);
-            }
+          for (int j = 0; j < EC / 4; ++j) {
+            float4 o = cv[j];
+            o.x += __uint_as_float(v[4 * j]);
+            o.y += __uint_as_float(v[4 * j + 1]);
+            o.z += __uint_as_float(v[4 * j + 2]);
+            o.w += __uint_as_float(v[4 * j + 3]);
+            *reinterpret_cast<float4*>(crow + 4 * j) = o;
           }
+        } else if (r < g.M) {
+          for (int q = 0; q < EC; ++q)
+            if (n0 + q < nlim) crow[q] = (keep ? crow[q] : 0.f) + __uint_as_float(v[q]);
         }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TN));
+  if (warp == kMW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TN));
   // launched as a programmatic dependent of the panel kernel: complete only after it
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
