@@ -648,21 +648,24 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g
     const double* as = As + (kb & 1) * BM * AST + (wm * 64) * AST;
     const double* bs = Bs + (kb & 1) * BK * BST + wn * 32;
     // m16n8k16 (8 DMMA.8x8x4 in SASS); measured faster here than k-outer m8n8k4 issue
-    double bf[4][4];
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int k16 = 0; k16 < BK; k16 += 16) {
+      double bf[4][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) bf[nt][i] = bs[(tq + 4 * i) * BST + nt * 8 + gq];
+      for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      double af[8];
+        for (int i = 0; i < 4; ++i) bf[nt][i] = bs[(k16 + tq + 4 * i) * BST + nt * 8 + gq];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        af[2 * i] = as[(mt * 16 + gq) * AST + tq + 4 * i];
-        af[2 * i + 1] = as[(mt * 16 + gq + 8) * AST + tq + 4 * i];
+      for (int mt = 0; mt < 4; ++mt) {
+        double af[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          af[2 * i] = as[(mt * 16 + gq) * AST + k16 + tq + 4 * i];
+          af[2 * i + 1] = as[(mt * 16 + gq + 8) * AST + k16 + tq + 4 * i];
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma16816(acc[mt][nt], af, bf[nt]);
       }
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) dmma16816(acc[mt][nt], af, bf[nt]);
     }
     __syncthreads();
   }
