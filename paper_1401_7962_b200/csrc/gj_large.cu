@@ -283,8 +283,12 @@ struct LeafSmem {
   static constexpr int EXW = W + KEYT;                    // entry: key + W row values (T units)
   static constexpr int RS = 0;                            // [W][PANEL_MAX] pivot rows of a leaf
   static constexpr int PROW = RS + W * 128 * (int)sizeof(T);   // [W] pivot row ids of the current leaf
-  static constexpr int WSLOT = (PROW + W * 4 + 15) / 16 * 16;  // [kLeafThreads/32][EXW]
-  static constexpr int EXCH = WSLOT + (kLeafThreads / 32) * EXW * (int)sizeof(T);   // [2][CL][EXW]
+  // [2][kLeafThreads/32][EXW] warp winners, double-buffered by step parity: the bulk copies
+  // of step k read their source asynchronously, and only the wait of step k+1 proves (via
+  // the peers' step-(k+1) entries) that every peer has received — so the copy has read —
+  // this CTA's step-k entry; step k+2 may then rewrite the buffer
+  static constexpr int WSLOT = (PROW + W * 4 + 15) / 16 * 16;
+  static constexpr int EXCH = WSLOT + 2 * (kLeafThreads / 32) * EXW * (int)sizeof(T);   // [2][CL][EXW]
   static int bytes(int cl) { return EXCH + 2 * cl * EXW * (int)sizeof(T) + 2 * 8 + 64; }
 };
 
@@ -377,7 +381,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
       // the warp winner writes key + row into its slot (then fences them into the async
       // proxy: warp 0 ships the CTA winner's slot with cp.async.bulk)
       const bool wwin = has && best.pos == pw_;
-      T* slot = wslot + warp * EXW;
+      T* const wsb = wslot + b * (kLeafThreads / 32) * EXW;
+      T* slot = wsb + warp * EXW;
       if (pw_ == 0xffffffffu) {
         if (lane == 0) reinterpret_cast<uint4*>(slot)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
       } else {
@@ -398,11 +403,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         const int nw = kLeafThreads / 32;
         Cand c{0u, 0u, 0xffffffffu, 0u};
         if (lane < nw) {
-          const uint4 k4 = reinterpret_cast<const uint4*>(wslot + lane * EXW)[0];
+          const uint4 k4 = reinterpret_cast<const uint4*>(wsb + lane * EXW)[0];
           c = Cand{k4.x, k4.y, k4.z, k4.w};
         }
         const int src_warp = warp_pick(c, lane < nw);
-        const uint32_t src = smem_u32(wslot + src_warp * EXW);
+        const uint32_t src = smem_u32(wsb + src_warp * EXW);
         if (lane < (int)CL) {
           const uint32_t ldst = smem_u32(exch + (size_t)(b * CL + rank) * EXW);
           bulk_s2c(map_remote(ldst, (uint32_t)lane), src, (uint32_t)(EXW * (int)sizeof(T)), map_remote(smem_u32(&bars[b]), (uint32_t)lane));
@@ -804,6 +809,13 @@ static bool debug_sync() {
   if (v < 0) v = getenv("GJ_DEBUG_SYNC") != nullptr ? 1 : 0;
   return v == 1;
 }
+// GJ_LARGE_NO_PDL: launch the trailing update after the next panel (no overlap) — a
+// diagnostic switch
+static bool no_pdl() {
+  static int v = -1;
+  if (v < 0) v = getenv("GJ_LARGE_NO_PDL") != nullptr ? 1 : 0;
+  return v == 1;
+}
 #define GJ_DBG(name)                                                                        \
   do {                                                                                      \
     if (debug_sync()) {                                                                     \
@@ -942,6 +954,7 @@ cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, in
   using large::LeafArgs;
   using large::leaf_cfg;
   using large::launch_leaf;
+  using large::debug_sync;
   constexpr int PANEL = f32::PANEL;
   const int npad = f32::pad128(n);
   LeafCfg lc;
@@ -953,6 +966,7 @@ cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, in
   cudaMemsetAsync(w.smax, 0, 8, s);
   f32::copy_pad_f32<<<sms * 8, 256, 0, s>>>(A, lda, n, w.X, npad, w.smax);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int det_only = Ainv == nullptr ? 1 : 0;   // gj_det: columns right of the panel only
   auto factor_panel = [&](int P0) -> cudaError_t {
     LeafArgs la{w.X, npad, npad, P0, P0, PANEL, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
     if (lc.w == 32) return launch_leaf<32, 1, float>(la, lc.cl, s);
@@ -974,7 +988,14 @@ cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, in
     const int pw1 = nxt ? PANEL : 0;
     TcUpdateArgs gb{w.Ah, w.Al, w.Bh, w.Bl, w.X, npad, npad, npad - PANEL - pw1, npad, w.pivstep, P0, P0 + PANEL,
                     P0, P1 + pw1};
-    if ((e = launch_tc_update(gb, nxt ? sms - lc.cl : 0, nxt, s)) != cudaSuccess) return e;
+    if (det_only) {
+      gb.N = npad - P1 - pw1;
+      gb.skip_lo = 0;
+      gb.skip_hi = P1 + pw1;
+    }
+    const bool pdl = nxt && !large::no_pdl();
+    if ((e = launch_tc_update(gb, pdl ? sms - lc.cl : 0, pdl, s)) != cudaSuccess) return e;
+    GJ_DBG("f32 panel");
   }
   if (Ainv != nullptr)
     f32::unpermute_f32<<<dim3((n + 255) / 256, n), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
@@ -1005,6 +1026,10 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   GJ_DBG("setup");
 
+  // determinant only (Ainv == NULL, gj_det): the pivots need every column right of the
+  // current panel, never the compact D columns on the left — about half the work (the
+  // panel itself is factored whole: its compact columns W drive the update)
+  const int det_only = Ainv == nullptr ? 1 : 0;
   // Look-ahead over panels: panel k+1 is updated by panel k first and factored by the
   // cluster kernel while the rest of panel k's update runs on the other SMs.
   auto factor_panel = [&](int P0, int pw) -> cudaError_t {
@@ -1029,6 +1054,11 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
     }
     // every column outside panels k and k+1 (the D columns on the left included)
     GemmArgs gb{w.X + P0, npad, w.R, npad, w.X, npad, npad, npad - pw - pw1, pw, w.pivstep, P0, P0 + pw, P0, P1 + pw1};
+    if (det_only) {   // only the columns right of panel k+1
+      gb.N = npad - P1 - pw1;
+      gb.skip_lo = 0;
+      gb.skip_hi = P1 + pw1;
+    }
     if ((e = launch_gemm(gb, s, pw1 > 0 ? sms - lc.cl : 0, pw1 > 0 && !debug_sync())) != cudaSuccess) return e;
     GJ_DBG("trailing gemm");
   }
