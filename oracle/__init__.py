@@ -61,6 +61,9 @@ def _load():
         lib.gjo_residual_rows.restype = ctypes.c_double
         lib.gjo_residual_batched.argtypes = [ctypes.c_int, ctypes.c_int64, dp, dp, dp, ctypes.c_int]
         lib.gjo_residual_batched.restype = ctypes.c_int
+        lib.gjo_invert_full_batched.argtypes = [ctypes.c_int, ctypes.c_int64, dp, ctypes.c_double, dp, ip, ip, dp,
+                                                dp, ip, dp, ip, dp, dp, ctypes.c_int]
+        lib.gjo_invert_full_batched.restype = ctypes.c_int
         lib.gjo_max_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -85,6 +88,7 @@ class OracleResult:
     info: np.ndarray         # [B] int32, 0 or first failing step (1-based)
     gap: np.ndarray          # [B, n] (c1 - c2) / c1 of the step-k candidates (rule R3)
     cmax_rel: np.ndarray     # [B, n] c1 / max|a_ij| (rule R7)
+    jpiv: np.ndarray = None  # [B, n] int32 column swap sequence (full pivoting only)
 
 
 def threads() -> int:
@@ -135,6 +139,34 @@ def invert(A, tol: float = 0.0, strategy: str = "partial", nthreads: int = 0) ->
                         _p(out.inverse, dp), _p(out.ipiv, ip), _p(out.pivots, dp),
                         _p(out.logabsdet, dp), _p(out.sign, ip), _p(out.det, dp), _p(out.info, ip),
                         _p(out.gap, dp), _p(out.cmax_rel, dp), nt)
+    if rc != 0:
+        raise MemoryError("oracle allocation failed")
+    return out
+
+
+def invert_full_batched(A, tol: float = 0.0, nthreads: int = 0) -> OracleResult:
+    """Full pivoting (Obs. 2–3; ``gjo_invert_full`` F1–F3): the pivot of
+    step k is the first maximum of |a_ij| over i, j = k..n in row-major scan of the
+    physically swapped array (reading G23); rows and columns are swapped and the column
+    swaps undone at the end.  ``ipiv`` / ``jpiv`` are the 1-based row / column swap
+    sequences; ``gap`` is over all candidates of a step."""
+    lib = _load()
+    A = np.asarray(A)
+    if A.ndim == 2:
+        A = A[None]
+    if not np.all(np.isfinite(A)):
+        raise ValueError("oracle rejects non-finite inputs (reading G20)")
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B, n, _ = A.shape
+    out = OracleResult(
+        inverse=np.empty((B, n, n)), ipiv=np.zeros((B, n), np.int32), pivots=np.zeros((B, n)),
+        logabsdet=np.empty(B), sign=np.zeros(B, np.int32), det=np.empty(B), info=np.zeros(B, np.int32),
+        gap=np.empty((B, n)), cmax_rel=np.empty((B, n)), jpiv=np.zeros((B, n), np.int32))
+    dp, ip = ctypes.c_double, ctypes.c_int32
+    rc = lib.gjo_invert_full_batched(n, B, _p(A, dp), float(tol), _p(out.inverse, dp), _p(out.ipiv, ip),
+                                     _p(out.jpiv, ip), _p(out.pivots, dp), _p(out.logabsdet, dp),
+                                     _p(out.sign, ip), _p(out.det, dp), _p(out.info, ip), _p(out.gap, dp),
+                                     _p(out.cmax_rel, dp), int(nthreads))
     if rc != 0:
         raise MemoryError("oracle allocation failed")
     return out

@@ -31,6 +31,8 @@
  *       swaps + un-permutation) is therefore checked against an independent route.
  *   O5  det = (-1)^swaps * prod p_k, logabsdet = sum log|p_k|, sign.
  *
+ * gjo_invert_full: full pivoting (Obs. 2-3, rows AND columns), see F1-F3 below.
+ *
  * Strategy 0 ("none", Eqs. (3)-(10) literally, pivot = a_kk) is kept
  * for tests of "a zero pivot does not imply singularity" (Obs. 2).
  *
@@ -167,6 +169,144 @@ int gjo_invert_batched(int n, int64_t batch, const double* A, double tol, int st
                           gap ? gap + b * n : NULL,
                           cmax_rel ? cmax_rel + b * n : NULL, 1);
     }
+    return err ? -1 : 0;
+}
+
+/* Full pivoting: Obs. 2-3 literally — at step k
+ * any a_ij, i, j = k..n, may be brought to the pivot position by swapping rows k and i
+ * and columns k and j; Obs. 3 takes the one of maximum |a_ij|; "at the end the row and
+ * column swaps must be undone".
+ *
+ *   F1  M = [A | I] (n x 2n), s = max |a_ij|, tau = tol * s            (as O1-O2)
+ *   F2  for k = 1..n:
+ *       a. (r, c) = first (i, j) in the row-major scan of i = k..n, j = k..n attaining
+ *          max |M[i][j]| (strict '>' as the listing's scan, L151-L153; reading G23)
+ *       b. |M[r][c]| <= tau => singular at step k (Obs. 2)
+ *       c. swap rows k and r over all 2n columns; swap columns k and c of the A half
+ *          (the D half's columns are the unknowns' right-hand sides, never swapped)
+ *       d. p = M[k][k]; Eq. (13) with the sign of BOTH swaps (det(A Q) = det(A) det(Q))
+ *       e. Eq. (14): row k /= p;  f. Eq. (15): rows i != k -= M[i][k] * row k
+ *   F3  the right half R = (A Q)^-1 = Q^T A^-1, Q = T_1 ... T_n the column swaps, so
+ *       A^-1 = Q R: apply the column swaps in reverse order to the ROWS of R
+ *       ("trebuie efectuate din nou schimbarea de linii și coloane", Obs. 3).
+ * ipiv[k] = r + 1, jpiv[k] = c + 1 (1-based positions, LAPACK getc2 convention).
+ * gap[k] = (c1 - c2) / c1 over all (n-k)^2 candidates of step k. */
+int gjo_invert_full(int n, const double* A, double tol, double* Ainv, int32_t* ipiv, int32_t* jpiv,
+                    double* pivots, double* logabsdet, int32_t* sign, double* det, int32_t* info, double* gap,
+                    double* cmax_rel)
+{
+    const int w = 2 * n;
+    ld* M = (ld*)malloc(sizeof(ld) * (size_t)n * (size_t)w);
+    int* cp = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    if ((!M || !cp) && n > 0) { free(M); free(cp); return -1; }
+    /* F1 */
+    ld s = 0.0L;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            ld a = (ld)A[(size_t)i * n + j];
+            M[(size_t)i * w + j] = a;
+            M[(size_t)i * w + n + j] = (i == j) ? 1.0L : 0.0L;
+            if (fabsl(a) > s) s = fabsl(a);
+        }
+    const ld tau = (ld)tol * s;
+    int swaps = 0, neg = 0, fail = 0;
+    ld logabs = 0.0L, prod = 1.0L;
+    for (int k = 0; k < n; ++k) {
+        /* F2a */
+        int r = k, c = k;
+        ld c1 = -1.0L, c2 = -1.0L;
+        for (int i = k; i < n; ++i)
+            for (int j = k; j < n; ++j) {
+                ld v = fabsl(M[(size_t)i * w + j]);
+                if (v > c1) { c2 = c1; c1 = v; r = i; c = j; }
+                else if (v > c2) { c2 = v; }
+            }
+        if (gap) gap[k] = (c2 < 0.0L) ? INFINITY : (c1 > 0.0L ? (double)((c1 - c2) / c1) : 0.0);
+        if (cmax_rel) cmax_rel[k] = (s > 0.0L) ? (double)(c1 / s) : 0.0;
+        if (ipiv) ipiv[k] = r + 1;
+        if (jpiv) jpiv[k] = c + 1;
+        cp[k] = c;
+        /* F2b */
+        if (c1 <= tau) { fail = k + 1; break; }
+        /* F2c */
+        if (r != k) {
+            for (int j = 0; j < w; ++j) {
+                ld t = M[(size_t)k * w + j]; M[(size_t)k * w + j] = M[(size_t)r * w + j]; M[(size_t)r * w + j] = t;
+            }
+            swaps ^= 1;
+        }
+        if (c != k) {
+            for (int i = 0; i < n; ++i) {
+                ld t = M[(size_t)i * w + k]; M[(size_t)i * w + k] = M[(size_t)i * w + c]; M[(size_t)i * w + c] = t;
+            }
+            swaps ^= 1;
+        }
+        /* F2d */
+        ld* Rk = M + (size_t)k * w;
+        const ld p = Rk[k];
+        if (pivots) pivots[k] = (double)p;
+        logabs += logl(fabsl(p));
+        if (p < 0.0L) neg ^= 1;
+        prod *= p;
+        /* F2e */
+        for (int j = 0; j < w; ++j) Rk[j] = Rk[j] / p;
+        /* F2f */
+        for (int i = 0; i < n; ++i) {
+            if (i == k) continue;
+            ld* Ri = M + (size_t)i * w;
+            const ld f = Ri[k];
+            if (f == 0.0L) continue;
+            for (int j = 0; j < w; ++j) Ri[j] = Ri[j] - f * Rk[j];
+        }
+    }
+    if (info) *info = fail;
+    if (fail) {
+        if (logabsdet) *logabsdet = -INFINITY;
+        if (sign) *sign = 0;
+        if (det) *det = 0.0;
+        if (Ainv) for (size_t t = 0; t < (size_t)n * n; ++t) Ainv[t] = NAN;
+        if (pivots) for (int k = fail - 1; k < n; ++k) pivots[k] = 0.0;
+        if (ipiv) for (int k = fail; k < n; ++k) ipiv[k] = 0;
+        if (jpiv) for (int k = fail; k < n; ++k) jpiv[k] = 0;
+        if (gap) for (int k = fail; k < n; ++k) gap[k] = NAN;
+        if (cmax_rel) for (int k = fail; k < n; ++k) cmax_rel[k] = NAN;
+    } else {
+        /* F3: undo the column swaps on the rows of the right half, last swap first */
+        for (int k = n - 1; k >= 0; --k) {
+            const int c = cp[k];
+            if (c == k) continue;
+            for (int j = n; j < w; ++j) {
+                ld t = M[(size_t)k * w + j]; M[(size_t)k * w + j] = M[(size_t)c * w + j]; M[(size_t)c * w + j] = t;
+            }
+        }
+        if (Ainv)
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j)
+                    Ainv[(size_t)i * n + j] = (double)M[(size_t)i * w + n + j];
+        if (logabsdet) *logabsdet = (double)logabs;
+        if (sign) *sign = ((swaps ^ neg) ? -1 : 1);
+        if (det) *det = (double)(swaps ? -prod : prod);
+    }
+    free(M);
+    free(cp);
+    return 0;
+}
+
+int gjo_invert_full_batched(int n, int64_t batch, const double* A, double tol, double* Ainv, int32_t* ipiv,
+                            int32_t* jpiv, double* pivots, double* logabsdet, int32_t* sign, double* det,
+                            int32_t* info, double* gap, double* cmax_rel, int nthreads)
+{
+    int err = 0;
+    const size_t nn = (size_t)n * n;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads > 0 ? nthreads : omp_get_max_threads()) reduction(|:err)
+#endif
+    for (int64_t b = 0; b < batch; ++b)
+        err |= gjo_invert_full(n, A + b * nn, tol, Ainv ? Ainv + b * nn : NULL, ipiv ? ipiv + b * n : NULL,
+                               jpiv ? jpiv + b * n : NULL, pivots ? pivots + b * n : NULL,
+                               logabsdet ? logabsdet + b : NULL, sign ? sign + b : NULL, det ? det + b : NULL,
+                               info ? info + b : NULL, gap ? gap + b * n : NULL,
+                               cmax_rel ? cmax_rel + b * n : NULL);
     return err ? -1 : 0;
 }
 
