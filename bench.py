@@ -221,6 +221,43 @@ def f1_measure(dev, reps: int = 3):
                          "note": "panel-latency bound: the pivot chain, not the tensor pipe, sets the time"}}
 
 
+def f2_measure(A, X, tol, stream, reps: int = 3):
+    """SURVEY §8f f2 (NEXT row): full pivoting (gj_invert_batched_full, Obs. 2-3) on the
+    same resident C2 batch; HBM roofline of the same algorithmic bytes as K1b."""
+    import torch
+    import paper_1401_7962_b200 as gj
+    B = A.shape[0]
+    ip = torch.empty((B, N), dtype=torch.int32, device=A.device)
+    jp = torch.empty_like(ip)
+    lg = torch.empty((B,), dtype=torch.float64, device=A.device)
+    sg = torch.empty((B,), dtype=torch.int8, device=A.device)
+
+    def run():
+        st = gj.lib.gj_invert_batched_full(0, N, B, A.data_ptr(), X.data_ptr(), ip.data_ptr(), jp.data_ptr(),
+                                           lg.data_ptr(), sg.data_ptr(), None, None, tol, stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    run()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    peak, src = measured_peaks()
+    gbs = B * (BYTES_PER_MATRIX + 2 * N * 4) / (ms / 1e3) / 1e9
+    return {"workload": "f2: C2 batch (1,048,576 x 32 x 32 fp32) with FULL pivoting (SURVEY §8f f2)",
+            "metric": "matrices/s", "value": B / (ms / 1e3), "unit": "matrices/s", "ms": ms, "reps": reps,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "peak_source": src, "kernel": "gj_full_kernel<float,32> (K6)",
+                         "note": "issue bound: per step a masked max over the 32 columns of every row"}}
+
+
 def cpu_baseline(sample: int, A_host=None):
     """The oracle as it stands, on the host's cores, on the first `sample` items of C2."""
     import oracle
@@ -396,6 +433,7 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * B / (ms_per_step / 1e3)
     avg_launch_ms = float(np.mean(launch_ms))
+    f2 = f2_measure(A, X, tol, stream) if (rank == 0 and not args.no_c4) else None
 
     # ---- end to end through the public API with HOST buffers (pinned), copies inside
     e2e = None
@@ -429,7 +467,7 @@ def main():
         achieved = B * BYTES_PER_MATRIX / (avg_launch_ms / 1e3) / 1e9
         traffic = profile_traffic()
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "gj_batched_warp_kernel<float,32,true> (K1)",
+                "traffic": traffic, "kernel": "gj_blk32_kernel<2,4,2> (K1b)",
                 "algorithmic_bytes_per_launch": B * BYTES_PER_MATRIX, "peak_source": peak_src,
                 "fp32_flops_per_launch": B * FLOPS_PER_MATRIX,
                 "achieved_fp32_tflops": B * FLOPS_PER_MATRIX / (avg_launch_ms / 1e3) / 1e12}
@@ -444,6 +482,7 @@ def main():
         if not args.no_c4:
             line["secondary"] = c4_measure(dev)
             line["next_f1"] = f1_measure(dev)
+            line["next_f2"] = f2
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample, A_host)
         print(json.dumps(line), flush=True)

@@ -87,6 +87,24 @@ gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, vo
                             int32_t* info, double tol, void* stream);
 
 /*
+ * gj_invert_batched_full — as gj_invert_batched with FULL pivoting:
+ * Obs. 2-3 — the pivot of step k is the element of maximum |a_ij|
+ * over all rows AND columns not yet pivoted (ties: the first in the row-major scan of the
+ * physically swapped array, i.e. smallest row position, then smallest column position —
+ * reading G23 of DESIGN.md), rows k <-> i and columns k <-> j are swapped, and the swaps
+ * are undone at the end.  n <= GJ_FULLPIV_MAX_N (32); any batch.
+ *   ipiv, jpiv  [batch][n] int32, 1-based row / column swap sequences (LAPACK getc2
+ *               convention: at step k rows k and ipiv[k], columns k and jpiv[k]); may be NULL.
+ *   sign        includes the parity of both swap sequences (det A = det(A Q) det Q).
+ * Other arguments, layouts, ownership and errors exactly as gj_invert_batched
+ * (Ainv NULL: determinants only).
+ */
+#define GJ_FULLPIV_MAX_N 32
+gj_status gj_invert_batched_full(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
+                                 int32_t* ipiv, int32_t* jpiv, double* logabsdet, int8_t* sign, void* det,
+                                 int32_t* info, double tol, void* stream);
+
+/*
  * gj_det — determinants only (Eq. (13); §4 "without laborious extra computation"):
  * the same elimination as gj_invert_batched without storing A^-1.
  * Arguments as gj_invert_batched; `workspace`/`workspace_bytes` are used for n > 64

@@ -5,8 +5,8 @@ Argument marshalling only: torch supplies device memory and the current CUDA str
 every step of the method runs in the library's sm_100a kernels.  There is no CPU
 fallback: if the library cannot be loaded, importing this package raises.
 
-Entry points mirror the C names: :func:`invert_batched`, :func:`invert`, :func:`det`,
-:func:`invert_batched_host`.
+Entry points mirror the C names: :func:`invert_batched`, :func:`invert_batched_full`,
+:func:`invert`, :func:`det`, :func:`invert_batched_host`.
 """
 from __future__ import annotations
 
@@ -17,7 +17,7 @@ from typing import Optional
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["invert_batched", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
+__all__ = ["invert_batched", "invert_batched_full", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
            "TOL_DEFAULT", "Result"]
 
 TOL_DEFAULT = -1.0
@@ -37,6 +37,8 @@ def _load():
     vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     L.gj_invert_batched.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, dbl, vp]
     L.gj_invert_batched.restype = i32
+    L.gj_invert_batched_full.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, dbl, vp]
+    L.gj_invert_batched_full.restype = i32
     L.gj_det.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
     L.gj_det.restype = i32
     L.gj_invert.argtypes = [i32, i32, vp, i64, vp, i64, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
@@ -55,6 +57,7 @@ lib = _load()
 library_path = _LIB_PATH
 
 Result = namedtuple("Result", ["inverse", "logabsdet", "sign", "det", "ipiv", "info"])
+FullResult = namedtuple("FullResult", ["inverse", "logabsdet", "sign", "det", "ipiv", "jpiv", "info"])
 
 
 def _check(st: int):
@@ -121,6 +124,38 @@ def invert_batched(A, tol: Optional[float] = None, *, out=None, inverse: bool = 
         sq = lambda t: None if t is None else t[0]
         return Result(sq(X), sq(o_lg), sq(o_sg), sq(o_det), sq(o_ipiv), sq(o_info))
     return Result(X, o_lg, o_sg, o_det, o_ipiv, o_info)
+
+
+def invert_batched_full(A, tol: Optional[float] = None, *, out=None, inverse: bool = True,
+                        stream=None) -> "FullResult":
+    """Full pivoting (``gj_invert_batched_full``, Obs. 2–3; n ≤ 32): as
+    :func:`invert_batched` plus ``jpiv``, the 1-based column swap sequence."""
+    torch = _torch()
+    if not A.is_cuda:
+        raise ValueError("A must be a CUDA tensor")
+    squeeze = A.dim() == 2
+    if squeeze:
+        A = A.unsqueeze(0)
+    if A.dim() != 3 or A.shape[1] != A.shape[2] or not A.is_contiguous():
+        raise ValueError("A must be a contiguous [B, n, n]")
+    B, n = A.shape[0], A.shape[1]
+    dev = A.device
+    X = (out if out is not None else torch.empty_like(A)) if inverse else None
+    o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev)
+    o_jpiv = torch.empty((B, n), dtype=torch.int32, device=dev)
+    o_lg = torch.empty((B,), dtype=torch.float64, device=dev)
+    o_sg = torch.empty((B,), dtype=torch.int8, device=dev)
+    o_det = torch.empty((B,), dtype=A.dtype, device=dev)
+    o_info = torch.empty((B,), dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        st = lib.gj_invert_batched_full(_dt(A), n, B, A.data_ptr(), _ptr(X), o_ipiv.data_ptr(), o_jpiv.data_ptr(),
+                                        o_lg.data_ptr(), o_sg.data_ptr(), o_det.data_ptr(), o_info.data_ptr(),
+                                        TOL_DEFAULT if tol is None else float(tol), _stream_ptr(stream))
+    _check(st)
+    if squeeze:
+        sq = lambda t: None if t is None else t[0]
+        return FullResult(sq(X), o_lg[0], o_sg[0], o_det[0], o_ipiv[0], o_jpiv[0], o_info[0])
+    return FullResult(X, o_lg, o_sg, o_det, o_ipiv, o_jpiv, o_info)
 
 
 def det(A, tol: Optional[float] = None, *, stream=None) -> Result:

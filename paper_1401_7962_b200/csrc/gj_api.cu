@@ -65,6 +65,19 @@ gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, vo
   return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
+gj_status gj_invert_batched_full(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
+                                 int32_t* ipiv, int32_t* jpiv, double* logabsdet, int8_t* sign, void* det,
+                                 int32_t* info, double tol, void* stream) {
+  if (dt != GJ_F32 && dt != GJ_F64) return GJ_ERR_ARG;
+  if (n < 1 || batch < 0) return GJ_ERR_ARG;
+  if (batch == 0) return GJ_OK;
+  if (A == nullptr) return GJ_ERR_ARG;
+  if (n > GJ_FULLPIV_MAX_N) return GJ_ERR_UNSUPPORTED;
+  BatchedArgs a{n, batch, A, Ainv, ipiv, logabsdet, sign, det, info, resolve_tol(dt, n, tol)};
+  cudaError_t e = launch_batched_full(dt, a, jpiv, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
 size_t gj_workspace_size(gj_dtype dt, int n, int64_t batch, int entry) {
   (void)batch;
   if (n < 1) return 0;

@@ -39,10 +39,14 @@ class Report:
                 f"max_dlogdet={self.max_logdet_err:.3e}")
 
 
-def ipiv_match(ipiv_gpu, ipiv_ref, gap_ref):
+def ipiv_match(ipiv_gpu, ipiv_ref, gap_ref, jpiv_gpu=None, jpiv_ref=None):
     """R3: equal step by step; at the first mismatch the oracle's gap_k must be <= 1e-6
-    and later steps are not compared.  Returns (ok, exempted)."""
-    neq = np.nonzero(ipiv_gpu != ipiv_ref)[0]
+    and later steps are not compared.  Full pivoting: a step matches when both its row
+    and its column swap match.  Returns (ok, exempted)."""
+    diff = ipiv_gpu != ipiv_ref
+    if jpiv_gpu is not None:
+        diff = diff | (jpiv_gpu != jpiv_ref)
+    neq = np.nonzero(diff)[0]
     if len(neq) == 0:
         return True, False
     k = neq[0]
@@ -86,8 +90,10 @@ def compare(A, gpu, ref, dtype, tol, kappa=None, check_ipiv=True, check_det=Fals
         if flat_only:
             rep.inv_kappa_fail = rep.inv_flat_fail
     if check_ipiv and "ipiv" in gpu:
+        full = "jpiv" in gpu and getattr(ref, "jpiv", None) is not None
         for b in idx:
-            ok, ex = ipiv_match(gpu["ipiv"][b], ref.ipiv[b], ref.gap[b])
+            ok, ex = ipiv_match(gpu["ipiv"][b], ref.ipiv[b], ref.gap[b],
+                                gpu["jpiv"][b] if full else None, ref.jpiv[b] if full else None)
             rep.ipiv_tie_exempt += int(ex and ok)
             if not ok:
                 rep.ipiv_fail.append(int(b))
