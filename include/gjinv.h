@@ -105,6 +105,26 @@ gj_status gj_invert_batched_full(gj_dtype dt, int n, int64_t batch, const void* 
                                  int32_t* info, double tol, void* stream);
 
 /*
+ * gj_invert_batched_pivoting — the K6 kernel under a chosen pivoting strategy, for the
+ * strategy / rounding-error comparison of the paper's §4 claim (Obs. 3
+ * L60 "to reduce rounding errors"):
+ *   GJ_PIVOT_NONE    (0)  pivot a_kk as in Eqs. (3)-(10) (L32-L46); info = first step with
+ *                         |a_kk| <= tau (a zero pivot, Obs. 2 — not necessarily singular)
+ *   GJ_PIVOT_PARTIAL (1)  the listing's row search in column k (L151-L162)
+ *   GJ_PIVOT_FULL    (2)  as gj_invert_batched_full
+ * Same arguments and outputs as gj_invert_batched_full (jpiv = 1..n for none/partial,
+ * ipiv = 1..n for none).  n <= GJ_FULLPIV_MAX_N.  GJ_ERR_ARG for another strategy.
+ * The production partial-pivoting path is gj_invert_batched (K1/K1b/K2); this entry exists
+ * so that the three strategies run with identical arithmetic.
+ */
+#define GJ_PIVOT_NONE 0
+#define GJ_PIVOT_PARTIAL 1
+#define GJ_PIVOT_FULL 2
+gj_status gj_invert_batched_pivoting(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
+                                     int32_t* ipiv, int32_t* jpiv, double* logabsdet, int8_t* sign, void* det,
+                                     int32_t* info, double tol, int strategy, void* stream);
+
+/*
  * gj_det — determinants only (Eq. (13); §4 "without laborious extra computation"):
  * the same elimination as gj_invert_batched without storing A^-1.
  * Arguments as gj_invert_batched; `workspace`/`workspace_bytes` are used for n > 64

@@ -17,7 +17,7 @@ from typing import Optional
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["invert_batched", "invert_batched_full", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
+__all__ = ["invert_batched", "invert_batched_full", "invert_batched_pivoting", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
            "TOL_DEFAULT", "Result"]
 
 TOL_DEFAULT = -1.0
@@ -39,6 +39,8 @@ def _load():
     L.gj_invert_batched.restype = i32
     L.gj_invert_batched_full.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, dbl, vp]
     L.gj_invert_batched_full.restype = i32
+    L.gj_invert_batched_pivoting.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, dbl, i32, vp]
+    L.gj_invert_batched_pivoting.restype = i32
     L.gj_det.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
     L.gj_det.restype = i32
     L.gj_invert.argtypes = [i32, i32, vp, i64, vp, i64, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
@@ -126,10 +128,14 @@ def invert_batched(A, tol: Optional[float] = None, *, out=None, inverse: bool = 
     return Result(X, o_lg, o_sg, o_det, o_ipiv, o_info)
 
 
-def invert_batched_full(A, tol: Optional[float] = None, *, out=None, inverse: bool = True,
-                        stream=None) -> "FullResult":
-    """Full pivoting (``gj_invert_batched_full``, Obs. 2–3; n ≤ 32): as
-    :func:`invert_batched` plus ``jpiv``, the 1-based column swap sequence."""
+PIVOTING = {"none": 0, "partial": 1, "full": 2}
+
+
+def invert_batched_pivoting(A, strategy: str = "full", tol: Optional[float] = None, *, out=None,
+                            inverse: bool = True, stream=None) -> "FullResult":
+    """``gj_invert_batched_pivoting`` (n ≤ 32): the K6 kernel with ``strategy`` "none"
+    (pivot a_kk, Eqs. (3)–(10)), "partial" (the listing's row search) or "full"
+    (Obs. 2–3); as :func:`invert_batched` plus ``jpiv``, the column swap sequence."""
     torch = _torch()
     if not A.is_cuda:
         raise ValueError("A must be a CUDA tensor")
@@ -148,14 +154,22 @@ def invert_batched_full(A, tol: Optional[float] = None, *, out=None, inverse: bo
     o_det = torch.empty((B,), dtype=A.dtype, device=dev)
     o_info = torch.empty((B,), dtype=torch.int32, device=dev)
     with torch.cuda.device(dev):
-        st = lib.gj_invert_batched_full(_dt(A), n, B, A.data_ptr(), _ptr(X), o_ipiv.data_ptr(), o_jpiv.data_ptr(),
-                                        o_lg.data_ptr(), o_sg.data_ptr(), o_det.data_ptr(), o_info.data_ptr(),
-                                        TOL_DEFAULT if tol is None else float(tol), _stream_ptr(stream))
+        st = lib.gj_invert_batched_pivoting(_dt(A), n, B, A.data_ptr(), _ptr(X), o_ipiv.data_ptr(),
+                                            o_jpiv.data_ptr(), o_lg.data_ptr(), o_sg.data_ptr(), o_det.data_ptr(),
+                                            o_info.data_ptr(), TOL_DEFAULT if tol is None else float(tol),
+                                            PIVOTING[strategy], _stream_ptr(stream))
     _check(st)
     if squeeze:
         sq = lambda t: None if t is None else t[0]
         return FullResult(sq(X), o_lg[0], o_sg[0], o_det[0], o_ipiv[0], o_jpiv[0], o_info[0])
     return FullResult(X, o_lg, o_sg, o_det, o_ipiv, o_jpiv, o_info)
+
+
+def invert_batched_full(A, tol: Optional[float] = None, *, out=None, inverse: bool = True,
+                        stream=None) -> "FullResult":
+    """Full pivoting (``gj_invert_batched_full``, Obs. 2–3; n ≤ 32): as
+    :func:`invert_batched` plus ``jpiv``, the 1-based column swap sequence."""
+    return invert_batched_pivoting(A, "full", tol, out=out, inverse=inverse, stream=stream)
 
 
 def det(A, tol: Optional[float] = None, *, stream=None) -> Result:

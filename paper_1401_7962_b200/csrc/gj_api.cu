@@ -65,17 +65,25 @@ gj_status gj_invert_batched(gj_dtype dt, int n, int64_t batch, const void* A, vo
   return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_invert_batched_full(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
-                                 int32_t* ipiv, int32_t* jpiv, double* logabsdet, int8_t* sign, void* det,
-                                 int32_t* info, double tol, void* stream) {
+gj_status gj_invert_batched_pivoting(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
+                                     int32_t* ipiv, int32_t* jpiv, double* logabsdet, int8_t* sign, void* det,
+                                     int32_t* info, double tol, int strategy, void* stream) {
   if (dt != GJ_F32 && dt != GJ_F64) return GJ_ERR_ARG;
   if (n < 1 || batch < 0) return GJ_ERR_ARG;
+  if (strategy != GJ_PIVOT_NONE && strategy != GJ_PIVOT_PARTIAL && strategy != GJ_PIVOT_FULL) return GJ_ERR_ARG;
   if (batch == 0) return GJ_OK;
   if (A == nullptr) return GJ_ERR_ARG;
   if (n > GJ_FULLPIV_MAX_N) return GJ_ERR_UNSUPPORTED;
   BatchedArgs a{n, batch, A, Ainv, ipiv, logabsdet, sign, det, info, resolve_tol(dt, n, tol)};
-  cudaError_t e = launch_batched_full(dt, a, jpiv, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_batched_strategy(dt, a, jpiv, strategy, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
+gj_status gj_invert_batched_full(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
+                                 int32_t* ipiv, int32_t* jpiv, double* logabsdet, int8_t* sign, void* det,
+                                 int32_t* info, double tol, void* stream) {
+  return gj_invert_batched_pivoting(dt, n, batch, A, Ainv, ipiv, jpiv, logabsdet, sign, det, info, tol,
+                                    GJ_PIVOT_FULL, stream);
 }
 
 size_t gj_workspace_size(gj_dtype dt, int n, int64_t batch, int entry) {

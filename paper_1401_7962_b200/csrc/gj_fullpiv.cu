@@ -127,7 +127,11 @@ struct FullSmem {
   static constexpr int per_warp = (STAGE + PROW + RECP + RECQ + PERM + MVEC + 15) / 16 * 16;
 };
 
-template <typename T, int NP>
+// STRAT: 2 = full pivoting (Obs. 2-3), 1 = partial (the listing: rows only, column k),
+// 0 = none (Eqs. (3)-(10) literally: pivot a_kk).  0 and 1 exist for the strategy /
+// rounding-error harness — the same arithmetic under each strategy;
+// the product partial-pivoting path is K1/K1b.
+template <typename T, int NP, int STRAT>
 __global__ void __launch_bounds__(kFullWarps * 32) gj_full_kernel(BatchedArgs a, int32_t* jpiv) {
   using S = FullSmem<T, NP>;
   constexpr int L = NP, MPW = S::MPW;
@@ -219,27 +223,56 @@ __global__ void __launch_bounds__(kFullWarps * 32) gj_full_kernel(BatchedArgs a,
 #pragma unroll 1
     for (int k = 0; k < n; ++k) {
       // ---- a2: the row's best key over its un-pivoted columns, group max
-      uint32_t cm[NP];
-      ld_masks<NP>(cm, mvec_g);
-      K km = 0;
+      int qr, rsrc, qc, c;
+      bool piv;
+      if constexpr (STRAT == 2) {
+        uint32_t cm[NP];
+        ld_masks<NP>(cm, mvec_g);
+        K km = 0;
 #pragma unroll
-      for (int j = 0; j < NP; ++j) {
-        const K kj = mkey(x[j], cm[j]);
-        km = kj > km ? kj : km;
+        for (int j = 0; j < NP; ++j) {
+          const K kj = mkey(x[j], cm[j]);
+          km = kj > km ? kj : km;
+        }
+        const K m = gmax_key<L>(rdone ? K(0) : km);
+        // smallest physical row position among the rows attaining m
+        const uint32_t rc = (!rdone && km == m) ? ((uint32_t)pos << 8 | (uint32_t)li) : 0xffffffu;
+        const uint32_t rw = gmin_u32<L>(rc);
+        qr = (int)(rw >> 8);
+        rsrc = (int)(rw & 0xffu);
+        piv = li == rsrc;
+        st_row_if<T, NP>(piv, prow_g, x);
+        __syncwarp();
+        // smallest physical column position among the pivot row's columns attaining m
+        const T yl = prow_g[li];
+        const uint32_t cc = (!cdone_l && akey(yl) == m) ? ((uint32_t)cpos << 8 | (uint32_t)li) : 0xffffffu;
+        const uint32_t cw = gmin_u32<L>(cc);
+        qc = (int)(cw >> 8);
+        c = (int)(cw & 0xffu);
+      } else if constexpr (STRAT == 1) {
+        // the listing's search (L151-L153): column k, max |x_ik| over the un-pivoted rows,
+        // ties -> smallest physical row position (G3); columns never move
+        c = k;
+        qc = k;
+        const K key = akey(sel_col<T, NP>(x, k));
+        const K m = gmax_key<L>(rdone ? K(0) : key);
+        const uint32_t rc = (!rdone && key == m) ? ((uint32_t)pos << 8 | (uint32_t)li) : 0xffffffu;
+        const uint32_t rw = gmin_u32<L>(rc);
+        qr = (int)(rw >> 8);
+        rsrc = (int)(rw & 0xffu);
+        piv = li == rsrc;
+        st_row_if<T, NP>(piv, prow_g, x);
+        __syncwarp();
+      } else {
+        // no pivoting: the pivot is a_kk (Eqs. (3)-(10)); nothing ever moves
+        c = k;
+        qc = k;
+        qr = k;
+        rsrc = k;
+        piv = li == k;
+        st_row_if<T, NP>(piv, prow_g, x);
+        __syncwarp();
       }
-      const K m = gmax_key<L>(rdone ? K(0) : km);
-      // smallest physical row position among the rows attaining m
-      const uint32_t rc = (!rdone && km == m) ? ((uint32_t)pos << 8 | (uint32_t)li) : 0xffffffu;
-      const uint32_t rw = gmin_u32<L>(rc);
-      const int qr = (int)(rw >> 8), rsrc = (int)(rw & 0xffu);
-      const bool piv = li == rsrc;
-      st_row_if<T, NP>(piv, prow_g, x);
-      __syncwarp();
-      // smallest physical column position among the pivot row's columns attaining m
-      const T yl = prow_g[li];
-      const uint32_t cc = (!cdone_l && akey(yl) == m) ? ((uint32_t)cpos << 8 | (uint32_t)li) : 0xffffffu;
-      const uint32_t cw = gmin_u32<L>(cc);
-      const int qc = (int)(cw >> 8), c = (int)(cw & 0xffu);
       const T p = prow_g[c];
       __syncwarp();
       // the pivot column's entry of the broadcast row is 0: the update leaves column c alone
@@ -268,7 +301,7 @@ __global__ void __launch_bounds__(kFullWarps * 32) gj_full_kernel(BatchedArgs a,
 #pragma unroll
         for (int j = 0; j < NP; ++j) x[j] = fma(nf, y[j], x[j]);
       }
-      if (li == c) mvec_g[li] = 0u;
+      if (STRAT == 2 && li == c) mvec_g[li] = 0u;
       // ---- a3: positions of the swapped rows and columns
       if (pos == k) pos = qr;
       if (piv) { pos = k; rdone = true; }
@@ -338,35 +371,42 @@ __global__ void __launch_bounds__(kFullWarps * 32) gj_full_kernel(BatchedArgs a,
   }
 }
 
-template <typename T, int NP>
+template <typename T, int NP, int STRAT>
 cudaError_t launch_full_t(const BatchedArgs& a, int32_t* jpiv, cudaStream_t s) {
   using S = FullSmem<T, NP>;
   const int smem = kFullWarps * S::per_warp;
   const int64_t ntasks = (a.batch + S::MPW - 1) / S::MPW;
   const int64_t need = (ntasks + kFullWarps - 1) / kFullWarps;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_full_kernel<T, NP>, kFullWarps * 32, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_full_kernel<T, NP, STRAT>, kFullWarps * 32, smem);
   if (e != cudaSuccess) return e;
   const int64_t cap = (int64_t)device_sm_count() * (per_sm > 0 ? per_sm : 1);
   const int grid = (int)(need < cap ? need : cap);
-  gj_full_kernel<T, NP><<<grid, kFullWarps * 32, smem, s>>>(a, jpiv);
+  gj_full_kernel<T, NP, STRAT><<<grid, kFullWarps * 32, smem, s>>>(a, jpiv);
   return cudaGetLastError();
 }
 
-template <typename T>
+template <typename T, int STRAT>
 cudaError_t launch_full_dt(const BatchedArgs& a, int32_t* jpiv, cudaStream_t s) {
-  if (a.n <= 2) return launch_full_t<T, 2>(a, jpiv, s);
-  if (a.n <= 4) return launch_full_t<T, 4>(a, jpiv, s);
-  if (a.n <= 8) return launch_full_t<T, 8>(a, jpiv, s);
-  if (a.n <= 16) return launch_full_t<T, 16>(a, jpiv, s);
-  return launch_full_t<T, 32>(a, jpiv, s);
+  if (a.n <= 2) return launch_full_t<T, 2, STRAT>(a, jpiv, s);
+  if (a.n <= 4) return launch_full_t<T, 4, STRAT>(a, jpiv, s);
+  if (a.n <= 8) return launch_full_t<T, 8, STRAT>(a, jpiv, s);
+  if (a.n <= 16) return launch_full_t<T, 16, STRAT>(a, jpiv, s);
+  return launch_full_t<T, 32, STRAT>(a, jpiv, s);
+}
+
+template <typename T>
+cudaError_t launch_strat(const BatchedArgs& a, int32_t* jpiv, int strategy, cudaStream_t s) {
+  if (strategy == 0) return launch_full_dt<T, 0>(a, jpiv, s);
+  if (strategy == 1) return launch_full_dt<T, 1>(a, jpiv, s);
+  return launch_full_dt<T, 2>(a, jpiv, s);
 }
 
 }  // namespace
 
-cudaError_t launch_batched_full(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, cudaStream_t s) {
-  if (a.n < 1 || a.n > 32) return cudaErrorInvalidValue;
-  return dt == GJ_F32 ? launch_full_dt<float>(a, jpiv, s) : launch_full_dt<double>(a, jpiv, s);
+cudaError_t launch_batched_strategy(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, int strategy, cudaStream_t s) {
+  if (a.n < 1 || a.n > 32 || strategy < 0 || strategy > 2) return cudaErrorInvalidValue;
+  return dt == GJ_F32 ? launch_strat<float>(a, jpiv, strategy, s) : launch_strat<double>(a, jpiv, strategy, s);
 }
 
 }  // namespace gj

@@ -26,8 +26,8 @@ cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 // K2b, fp64 n = 64 (gj_batched64b.cu); cudaErrorNotSupported if the buffers do not suit it.
 cudaError_t launch_batched64b(const BatchedArgs& a, cudaStream_t s);
-// K6, full pivoting, n <= 32 (gj_fullpiv.cu); jpiv may be null.
-cudaError_t launch_batched_full(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, cudaStream_t s);
+// K6, n <= 32 (gj_fullpiv.cu): strategy 2 = full pivoting, 1 = partial, 0 = none; jpiv may be null.
+cudaError_t launch_batched_strategy(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, int strategy, cudaStream_t s);
 
 // Large-n blocked path (gj_large.cu), fp64, one matrix; Ainv may be null (det only).
 size_t large_workspace_size(int n);
