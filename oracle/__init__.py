@@ -64,6 +64,9 @@ def _load():
         lib.gjo_invert_full_batched.argtypes = [ctypes.c_int, ctypes.c_int64, dp, ctypes.c_double, dp, ip, ip, dp,
                                                 dp, ip, dp, ip, dp, dp, ctypes.c_int]
         lib.gjo_invert_full_batched.restype = ctypes.c_int
+        lib.gjo_solve_batched.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, dp, dp, ctypes.c_double, dp,
+                                          ip, dp, ip, ip, dp, ctypes.c_int]
+        lib.gjo_solve_batched.restype = ctypes.c_int
         lib.gjo_max_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -167,6 +170,41 @@ def invert_full_batched(A, tol: float = 0.0, nthreads: int = 0) -> OracleResult:
                                      _p(out.jpiv, ip), _p(out.pivots, dp), _p(out.logabsdet, dp),
                                      _p(out.sign, ip), _p(out.det, dp), _p(out.info, ip), _p(out.gap, dp),
                                      _p(out.cmax_rel, dp), int(nthreads))
+    if rc != 0:
+        raise MemoryError("oracle allocation failed")
+    return out
+
+
+@dataclass
+class SolveResult:
+    X: np.ndarray            # [B, n, m] float64 (NaN for failed items)
+    ipiv: np.ndarray         # [B, n] int32
+    logabsdet: np.ndarray    # [B]
+    sign: np.ndarray         # [B] int32
+    info: np.ndarray         # [B] int32
+    gap: np.ndarray          # [B, n]
+
+
+def solve_batched(A, B, tol: float = 0.0, nthreads: int = 0) -> SolveResult:
+    """Gauss–Jordan on [A | B] (``gjo_solve``; Eqs. (14)–(15) with B in place of I, the
+    listing's partial pivoting): X = A^-1 B per item.  A [Bt, n, n], B [Bt, n, m]."""
+    lib = _load()
+    A = np.asarray(A)
+    Bm = np.asarray(B)
+    if A.ndim == 2:
+        A, Bm = A[None], Bm[None]
+    if not (np.all(np.isfinite(A)) and np.all(np.isfinite(Bm))):
+        raise ValueError("oracle rejects non-finite inputs (reading G20)")
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    Bm = np.ascontiguousarray(Bm, dtype=np.float64)
+    Bt, n, _ = A.shape
+    m = Bm.shape[2]
+    out = SolveResult(X=np.empty((Bt, n, m)), ipiv=np.zeros((Bt, n), np.int32), logabsdet=np.empty(Bt),
+                      sign=np.zeros(Bt, np.int32), info=np.zeros(Bt, np.int32), gap=np.empty((Bt, n)))
+    dp, ip = ctypes.c_double, ctypes.c_int32
+    rc = lib.gjo_solve_batched(n, m, Bt, _p(A, dp), _p(Bm, dp), float(tol), _p(out.X, dp), _p(out.ipiv, ip),
+                               _p(out.logabsdet, dp), _p(out.sign, ip), _p(out.info, ip), _p(out.gap, dp),
+                               int(nthreads))
     if rc != 0:
         raise MemoryError("oracle allocation failed")
     return out

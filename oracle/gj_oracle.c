@@ -32,6 +32,7 @@
  *   O5  det = (-1)^swaps * prod p_k, logabsdet = sum log|p_k|, sign.
  *
  * gjo_invert_full: full pivoting (Obs. 2-3, rows AND columns), see F1-F3 below.
+ * gjo_solve: the same elimination on [A | B] (multi-RHS solve, Eq. (12) with B for I).
  *
  * Strategy 0 ("none", Eqs. (3)-(10) literally, pivot = a_kk) is kept
  * for tests of "a zero pivot does not imply singularity" (Obs. 2).
@@ -307,6 +308,90 @@ int gjo_invert_full_batched(int n, int64_t batch, const double* A, double tol, d
                                logabsdet ? logabsdet + b : NULL, sign ? sign + b : NULL, det ? det + b : NULL,
                                info ? info + b : NULL, gap ? gap + b * n : NULL,
                                cmax_rel ? cmax_rel + b * n : NULL);
+    return err ? -1 : 0;
+}
+
+/* Multi-RHS solve: the same Gauss–Jordan with the right-hand sides B
+ * (n x m) in place of the identity — M = [A | B], Eqs. (14)-(15) on all n + m columns, the
+ * listing's partial pivoting (O3a-O3c); at the end M = [I | A^-1 B] (Eq. (12) with B for I).
+ * X: n x m row-major.  ipiv / logabsdet / sign / info as gjo_invert. */
+int gjo_solve(int n, int m, const double* A, const double* B, double tol, double* X, int32_t* ipiv,
+              double* logabsdet, int32_t* sign, int32_t* info, double* gap)
+{
+    const int w = n + m;
+    ld* M = (ld*)malloc(sizeof(ld) * (size_t)n * (size_t)(w > 0 ? w : 1));
+    if (!M && n > 0) return -1;
+    ld s = 0.0L;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) {
+            ld a = (ld)A[(size_t)i * n + j];
+            M[(size_t)i * w + j] = a;
+            if (fabsl(a) > s) s = fabsl(a);
+        }
+        for (int j = 0; j < m; ++j) M[(size_t)i * w + n + j] = (ld)B[(size_t)i * m + j];
+    }
+    const ld tau = (ld)tol * s;
+    int swaps = 0, neg = 0, fail = 0;
+    ld logabs = 0.0L;
+    for (int k = 0; k < n; ++k) {
+        int r = k;
+        ld c1 = fabsl(M[(size_t)k * w + k]), c2 = -1.0L;
+        for (int i = k + 1; i < n; ++i) {
+            ld c = fabsl(M[(size_t)i * w + k]);
+            if (c > c1) { c2 = c1; c1 = c; r = i; }
+            else if (c > c2) { c2 = c; }
+        }
+        if (gap) gap[k] = (c2 < 0.0L) ? INFINITY : (c1 > 0.0L ? (double)((c1 - c2) / c1) : 0.0);
+        if (ipiv) ipiv[k] = r + 1;
+        if (c1 <= tau) { fail = k + 1; break; }
+        if (r != k) {
+            for (int j = 0; j < w; ++j) {
+                ld t = M[(size_t)k * w + j]; M[(size_t)k * w + j] = M[(size_t)r * w + j]; M[(size_t)r * w + j] = t;
+            }
+            swaps ^= 1;
+        }
+        ld* Rk = M + (size_t)k * w;
+        const ld p = Rk[k];
+        logabs += logl(fabsl(p));
+        if (p < 0.0L) neg ^= 1;
+        for (int j = 0; j < w; ++j) Rk[j] = Rk[j] / p;
+        for (int i = 0; i < n; ++i) {
+            if (i == k) continue;
+            ld* Ri = M + (size_t)i * w;
+            const ld f = Ri[k];
+            if (f == 0.0L) continue;
+            for (int j = 0; j < w; ++j) Ri[j] = Ri[j] - f * Rk[j];
+        }
+    }
+    if (info) *info = fail;
+    if (fail) {
+        if (logabsdet) *logabsdet = -INFINITY;
+        if (sign) *sign = 0;
+        if (X) for (size_t t = 0; t < (size_t)n * m; ++t) X[t] = NAN;
+        if (ipiv) for (int k = fail; k < n; ++k) ipiv[k] = 0;
+        if (gap) for (int k = fail; k < n; ++k) gap[k] = NAN;
+    } else {
+        if (X)
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < m; ++j) X[(size_t)i * m + j] = (double)M[(size_t)i * w + n + j];
+        if (logabsdet) *logabsdet = (double)logabs;
+        if (sign) *sign = ((swaps ^ neg) ? -1 : 1);
+    }
+    free(M);
+    return 0;
+}
+
+int gjo_solve_batched(int n, int m, int64_t batch, const double* A, const double* B, double tol, double* X,
+                      int32_t* ipiv, double* logabsdet, int32_t* sign, int32_t* info, double* gap, int nthreads)
+{
+    int err = 0;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads > 0 ? nthreads : omp_get_max_threads()) reduction(|:err)
+#endif
+    for (int64_t b = 0; b < batch; ++b)
+        err |= gjo_solve(n, m, A + b * (size_t)n * n, B + b * (size_t)n * m, tol, X ? X + b * (size_t)n * m : NULL,
+                         ipiv ? ipiv + b * n : NULL, logabsdet ? logabsdet + b : NULL, sign ? sign + b : NULL,
+                         info ? info + b : NULL, gap ? gap + b * n : NULL);
     return err ? -1 : 0;
 }
 
