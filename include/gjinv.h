@@ -125,6 +125,25 @@ gj_status gj_invert_batched_pivoting(gj_dtype dt, int n, int64_t batch, const vo
                                      int32_t* info, double tol, int strategy, void* stream);
 
 /*
+ * gj_solve_batched — X = A^-1 B for a batch of systems with nrhs right-hand sides by
+ * Gauss–Jordan on the augmented [A | B] (Eq. (12) with B in place of the identity, the
+ * elimination of Eqs. (14)-(15); the listing's partial pivoting, ties to
+ * the smallest physical position, G3) — SURVEY.md §8f f4.  n <= GJ_SOLVE_MAX_N (32),
+ * nrhs <= GJ_SOLVE_MAX_NRHS (32).
+ *   A     [batch][n][n] row-major dt, read only.
+ *   B     [batch][n][nrhs] row-major dt, read only (unless X aliases it).
+ *   X     [batch][n][nrhs] row-major dt, written; may equal B (in place).
+ *   ipiv, logabsdet, sign, info, tol, stream as gj_invert_batched (each output may be NULL);
+ *   X of an item with info != 0 is unspecified.
+ * Returns GJ_OK, GJ_ERR_ARG (null A/B/X, n < 1, nrhs < 1), GJ_ERR_UNSUPPORTED, GJ_ERR_CUDA.
+ */
+#define GJ_SOLVE_MAX_N 32
+#define GJ_SOLVE_MAX_NRHS 32
+gj_status gj_solve_batched(gj_dtype dt, int n, int nrhs, int64_t batch, const void* A, const void* B, void* X,
+                           int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                           void* stream);
+
+/*
  * gj_det — determinants only (Eq. (13); §4 "without laborious extra computation"):
  * the same elimination as gj_invert_batched without storing A^-1.
  * Arguments as gj_invert_batched; `workspace`/`workspace_bytes` are used for n > 64

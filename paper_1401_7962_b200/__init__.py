@@ -17,7 +17,7 @@ from typing import Optional
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["invert_batched", "invert_batched_full", "invert_batched_pivoting", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
+__all__ = ["invert_batched", "invert_batched_full", "invert_batched_pivoting", "solve_batched", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
            "TOL_DEFAULT", "Result"]
 
 TOL_DEFAULT = -1.0
@@ -41,6 +41,8 @@ def _load():
     L.gj_invert_batched_full.restype = i32
     L.gj_invert_batched_pivoting.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, dbl, i32, vp]
     L.gj_invert_batched_pivoting.restype = i32
+    L.gj_solve_batched.argtypes = [i32, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, dbl, vp]
+    L.gj_solve_batched.restype = i32
     L.gj_det.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
     L.gj_det.restype = i32
     L.gj_invert.argtypes = [i32, i32, vp, i64, vp, i64, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
@@ -126,6 +128,39 @@ def invert_batched(A, tol: Optional[float] = None, *, out=None, inverse: bool = 
         sq = lambda t: None if t is None else t[0]
         return Result(sq(X), sq(o_lg), sq(o_sg), sq(o_det), sq(o_ipiv), sq(o_info))
     return Result(X, o_lg, o_sg, o_det, o_ipiv, o_info)
+
+
+SolveResult = namedtuple("SolveResult", ["X", "logabsdet", "sign", "ipiv", "info"])
+
+
+def solve_batched(A, B, tol: Optional[float] = None, *, out=None, stream=None) -> "SolveResult":
+    """``gj_solve_batched``: X = A^-1 B by Gauss–Jordan on [A | B] (n, nrhs ≤ 32).
+    A [batch, n, n], B [batch, n, nrhs] (or [n, n], [n, nrhs]); ``out`` may be B."""
+    torch = _torch()
+    if not (A.is_cuda and B.is_cuda):
+        raise ValueError("A and B must be CUDA tensors")
+    squeeze = A.dim() == 2
+    if squeeze:
+        A, B = A.unsqueeze(0), B.unsqueeze(0)
+    if A.dim() != 3 or A.shape[1] != A.shape[2] or B.dim() != 3 or B.shape[:2] != A.shape[:2]:
+        raise ValueError("A must be [batch, n, n] and B [batch, n, nrhs]")
+    if not (A.is_contiguous() and B.is_contiguous()) or A.dtype != B.dtype:
+        raise ValueError("A and B must be contiguous and of one dtype")
+    bt, n, m = A.shape[0], A.shape[1], B.shape[2]
+    dev = A.device
+    X = out if out is not None else torch.empty_like(B)
+    o_ipiv = torch.empty((bt, n), dtype=torch.int32, device=dev)
+    o_lg = torch.empty((bt,), dtype=torch.float64, device=dev)
+    o_sg = torch.empty((bt,), dtype=torch.int8, device=dev)
+    o_info = torch.empty((bt,), dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        st = lib.gj_solve_batched(_dt(A), n, m, bt, A.data_ptr(), B.data_ptr(), X.data_ptr(), o_ipiv.data_ptr(),
+                                  o_lg.data_ptr(), o_sg.data_ptr(), o_info.data_ptr(),
+                                  TOL_DEFAULT if tol is None else float(tol), _stream_ptr(stream))
+    _check(st)
+    if squeeze:
+        return SolveResult(X[0], o_lg[0], o_sg[0], o_ipiv[0], o_info[0])
+    return SolveResult(X, o_lg, o_sg, o_ipiv, o_info)
 
 
 PIVOTING = {"none": 0, "partial": 1, "full": 2}

@@ -79,6 +79,19 @@ gj_status gj_invert_batched_pivoting(gj_dtype dt, int n, int64_t batch, const vo
   return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
+gj_status gj_solve_batched(gj_dtype dt, int n, int nrhs, int64_t batch, const void* A, const void* B, void* X,
+                           int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                           void* stream) {
+  if (dt != GJ_F32 && dt != GJ_F64) return GJ_ERR_ARG;
+  if (n < 1 || nrhs < 1 || batch < 0) return GJ_ERR_ARG;
+  if (batch == 0) return GJ_OK;
+  if (A == nullptr || B == nullptr || X == nullptr) return GJ_ERR_ARG;
+  if (n > GJ_SOLVE_MAX_N || nrhs > GJ_SOLVE_MAX_NRHS) return GJ_ERR_UNSUPPORTED;
+  SolveArgs a{n, nrhs, batch, A, B, X, ipiv, logabsdet, sign, info, resolve_tol(dt, n, tol)};
+  cudaError_t e = launch_solve_batched(dt, a, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
+}
+
 gj_status gj_invert_batched_full(gj_dtype dt, int n, int64_t batch, const void* A, void* Ainv,
                                  int32_t* ipiv, int32_t* jpiv, double* logabsdet, int8_t* sign, void* det,
                                  int32_t* info, double tol, void* stream) {

@@ -26,6 +26,20 @@ cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 // K2b, fp64 n = 64 (gj_batched64b.cu); cudaErrorNotSupported if the buffers do not suit it.
 cudaError_t launch_batched64b(const BatchedArgs& a, cudaStream_t s);
+// K7, multi-RHS solve X = A^-1 B, n <= 32, m <= 32 (gj_solve.cu).
+struct SolveArgs {
+  int n, m;             // order, right-hand sides
+  int64_t batch;
+  const void* A;        // [batch][n][n]
+  const void* B;        // [batch][n][m]
+  void* X;              // [batch][n][m], may alias B
+  int32_t* ipiv;        // may be null
+  double* logabsdet;    // may be null
+  int8_t* sign;         // may be null
+  int32_t* info;        // may be null
+  double tol;
+};
+cudaError_t launch_solve_batched(gj_dtype dt, const SolveArgs& a, cudaStream_t s);
 // K6, n <= 32 (gj_fullpiv.cu): strategy 2 = full pivoting, 1 = partial, 0 = none; jpiv may be null.
 cudaError_t launch_batched_strategy(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, int strategy, cudaStream_t s);
 
