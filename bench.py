@@ -258,6 +258,44 @@ def f2_measure(A, X, tol, stream, reps: int = 3):
                          "note": "issue bound: per step a masked max over the 32 columns of every row"}}
 
 
+def f4_measure(A, stream, nrhs: int = 1, reps: int = 3):
+    """SURVEY §8f f4 (NEXT row): X = A^-1 B by GJ on [A | B] (gj_solve_batched) for the
+    resident C2 batch with one right-hand side per system; HBM roofline of A + B + X."""
+    import torch
+    import paper_1401_7962_b200 as gj
+    Bn = A.shape[0]
+    g = torch.Generator(device=A.device)
+    g.manual_seed(5)
+    R = torch.randn((Bn, N, nrhs), dtype=A.dtype, device=A.device, generator=g)
+    X = torch.empty_like(R)
+    ip = torch.empty((Bn, N), dtype=torch.int32, device=A.device)
+
+    def run():
+        st = gj.lib.gj_solve_batched(0, N, nrhs, Bn, A.data_ptr(), R.data_ptr(), X.data_ptr(), ip.data_ptr(),
+                                     None, None, None, N * 2.0 ** -23, stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    run()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    peak, src = measured_peaks()
+    gbs = Bn * (N * N + 2 * N * nrhs + N) * 4 / (ms / 1e3) / 1e9
+    return {"workload": f"f4: C2 batch (1,048,576 x 32 x 32 fp32) solved for {nrhs} right-hand side(s) (SURVEY §8f f4)",
+            "metric": "systems/s", "value": Bn / (ms / 1e3), "unit": "systems/s", "ms": ms, "reps": reps,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "peak_source": src, "kernel": f"gj_solve_kernel<float,32,{1 if nrhs == 1 else nrhs}> (K7)",
+                         "note": "unblocked (one row per lane, pivot row through shared memory every step)"}}
+
+
 def cpu_baseline(sample: int, A_host=None):
     """The oracle as it stands, on the host's cores, on the first `sample` items of C2."""
     import oracle
@@ -434,6 +472,7 @@ def main():
     value = world * B / (ms_per_step / 1e3)
     avg_launch_ms = float(np.mean(launch_ms))
     f2 = f2_measure(A, X, tol, stream) if (rank == 0 and not args.no_c4) else None
+    f4 = f4_measure(A, stream) if (rank == 0 and not args.no_c4) else None
 
     # ---- end to end through the public API with HOST buffers (pinned), copies inside
     e2e = None
@@ -483,6 +522,7 @@ def main():
             line["secondary"] = c4_measure(dev)
             line["next_f1"] = f1_measure(dev)
             line["next_f2"] = f2
+            line["next_f4"] = f4
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample, A_host)
         print(json.dumps(line), flush=True)
