@@ -18,9 +18,10 @@ sg = torch.empty(B, dtype=torch.int8).pin_memory()
 for chunk in [int(c) for c in sys.argv[1:]] or [0, 32768, 65536, 131072, 262144]:
     gj.invert_batched_host(Ah, out=Xh, logabsdet=lg, sign=sg, tol=32 * 2.0 ** -23, chunk=chunk)
     ts = []
-    for _ in range(3):
+    for _ in range(8):
         t0 = time.perf_counter()
         gj.invert_batched_host(Ah, out=Xh, logabsdet=lg, sign=sg, tol=32 * 2.0 ** -23, chunk=chunk)
         ts.append(time.perf_counter() - t0)
+    print("  each ms:", [round(x * 1e3, 1) for x in ts])
     t = min(ts)
     print(f"chunk={chunk}: {t * 1e3:.1f} ms  {B / t:.3e} mat/s  {2 * B * 4096 / t / 1e9:.1f} GB/s (H2D+D2H)", flush=True)
