@@ -154,3 +154,39 @@ def test_c5_gaussian_distributed(gj, torch):
         del A, LU
     finally:
         tdist.destroy_process_group()
+
+
+def test_c2_full_pivoting_sampled(gj, torch):
+    """bench.py's next_f2 launch: the whole C2 batch through gj_invert_batched_full, the
+    full-pivoting oracle on a sample spread over the batch incl. its ragged end."""
+    A = synth.gen_c2()
+    r = gj.invert_batched_full(torch.from_numpy(A).cuda(), tol=32 * 2.0 ** -23)
+    torch.cuda.synchronize()
+    idx = _sample(A.shape[0], 1500, 14)
+    it = torch.from_numpy(idx).cuda()
+    g = {k: (None if v is None else v[it].cpu().numpy()) for k, v in r._asdict().items()}
+    ref = oracle.invert_full_batched(A[idx], tol=32 * 2.0 ** -23)
+    rep = compare(A[idx], g, ref, np.float32, 32 * 2.0 ** -23)
+    print(rep.summary())
+    assert_report(rep)
+
+
+def test_c2_solve_sampled(gj, torch):
+    """bench.py's next_f4 launch: the whole C2 batch with one right-hand side through
+    gj_solve_batched, the [A | B] oracle on a sample."""
+    A = synth.gen_c2()
+    B = np.random.default_rng(5).standard_normal((A.shape[0], 32, 1)).astype(np.float32)
+    r = gj.solve_batched(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), tol=32 * 2.0 ** -23)
+    torch.cuda.synchronize()
+    idx = _sample(A.shape[0], 1500, 15)
+    it = torch.from_numpy(idx).cuda()
+    X = r.X[it].cpu().numpy().astype(np.float64)
+    info = r.info[it].cpu().numpy()
+    ref = oracle.solve_batched(A[idx], B[idx], tol=32 * 2.0 ** -23)
+    assert np.array_equal(info != 0, ref.info != 0)
+    ok = ref.info == 0
+    Ai = oracle.invert_batched(A[idx][ok]).inverse
+    kappa = np.abs(A[idx][ok].astype(np.float64)).sum(2).max(1) * np.abs(Ai).sum(2).max(1)
+    e = np.abs(X[ok] - ref.X[ok]).max(axis=(1, 2)) / np.abs(ref.X[ok]).max(axis=(1, 2))
+    print(f"C2 solve sample: max e/(kappa eps) {np.max(e / (kappa * 2.0 ** -23)):.3e}")
+    assert np.all(e <= np.maximum(2e-4, kappa * 2.0 ** -23))
