@@ -4,10 +4,10 @@
 //
 // K1's layout and step (lane = row, partial pivoting on the listing's rule with ties to the
 // smallest physical position (G3), logical row swaps, deferred pivot-row normalisation),
-// but the A part is not kept in compact form: the eliminated column is dropped and the
-// registers rotate left, so the pivot column is always register 0 (1 on the second step
-// of a pair) and no column is ever selected at run time.  The B part (m registers) takes
-// every step's update.  At the end the row pivoted at step k holds p_k x_k, so
+// but the A part is not kept in compact form: the k loop is fully unrolled, step k's pivot
+// column is register k and only the columns right of it are published, loaded and
+// updated (the A part shrinks: ~n^3/2 + n^2 m FMAs instead of the inverse's n^3).  The B
+// part (m registers) takes every step's update.  At the end the row pivoted at step k holds p_k x_k, so
 // X[k][:] = b_row / p_k — a row gather, no column permutation (B's columns never move).
 #include <cuda_runtime.h>
 #include <cmath>
@@ -74,13 +74,19 @@ __device__ __forceinline__ int s_pivot(T v, bool ok, int pos) {
   return (int)smin_u32<L>(cand ? (uint32_t)pos : 0xffffu);
 }
 
+// cp.async.bulk.prefetch of the 16-byte aligned interior of [lo, hi)
+__device__ __forceinline__ void prefetch_l2_range(const void* lo, const void* hi) {
+  const uintptr_t a = ((uintptr_t)lo + 15) & ~(uintptr_t)15, b = (uintptr_t)hi & ~(uintptr_t)15;
+  if (b > a) bulk_prefetch_l2(reinterpret_cast<const void*>(a), (uint32_t)(b - a));
+}
+
 template <typename T, int NP, int NR>
 struct SolveSmem {
   static constexpr int MPW = 32 / NP;
   static constexpr int ROWS = 32;
   static constexpr int SA = ROWS * (NP + 1) * (int)sizeof(T);     // A staging (padded rows)
   static constexpr int SB = ROWS * (NR + 1) * (int)sizeof(T);     // B / X staging
-  static constexpr int PA = 2 * MPW * NP * (int)sizeof(T);        // pivot row, A part (2 buffers)
+  static constexpr int PA = 2 * MPW * (NP + 4) * (int)sizeof(T);  // pivot row, A part + pivot (2 buffers)
   static constexpr int PB = 2 * MPW * NR * (int)sizeof(T);        // pivot row, B part
   static constexpr int REC = ROWS * 16;
   static constexpr int per_warp = ((SA + SB + PA + PB + REC) + 15) / 16 * 16;
@@ -119,39 +125,75 @@ __device__ __forceinline__ void move_rows(T* g, T* stage, int nrows, int len, in
   }
 }
 
-// One step k; the pivot column is register PC (0: first step of a pair, 1: second).
-template <typename T, int NP, int NR, int PC>
-__device__ __forceinline__ void solve_step(int k, T (&x)[NP], T (&b)[NR], bool& done, int& pos, T* pa, T* pb,
+// One step K (static: the k loop is fully unrolled, so the pivot column is register K and
+// only the columns right of it are live — the A part shrinks as the elimination proceeds).
+template <typename T, int NP, int NR, int K>
+__device__ __forceinline__ void solve_step(T (&x)[NP], T (&b)[NR], bool& done, int& pos, T* pa, T* pb,
                                            unsigned char* rec_g, int li) {
   constexpr int L = NP;
-  const int q = s_pivot<T, L>(x[PC], !done, pos);
+  constexpr int J0 = (K + 1) & ~3;   // first published / loaded column (16-byte aligned)
+  const int q = s_pivot<T, L>(x[K], !done, pos);
   const bool piv = !done && pos == q;
-  if (pos == k) pos = q;   // a3: the listing's swap of positions k and q (L156-L162)
-  if (piv) pos = k;
-  st_row_if<T, NP>(piv, pa, x);
-  st_row_if<T, NR>(piv, pb, b);
-  __syncwarp();
-  T y[NP], yb[NR];
-  ld_row<T, NP>(y, pa);
-  ld_row<T, NR>(yb, pb);
-  const T p = y[PC];
-  if (li == 0) rec_store(rec_g, k, p, q);
-  const T nf = piv ? T(0) : -(x[PC] * rcp(p));
-  done = done || piv;
-  // A part: eliminate column PC, rotate (the dropped column's slot gets 0)
-  if constexpr (PC == 0) {
-    update_first<NP>(x, y, nf);
-    x[0] = T(0);
-  } else {
-    update_second_rot<NP>(x, y, nf, T(0));
+  if (pos == K) pos = q;   // a3: the listing's swap of positions k and q (L156-L162)
+  if (piv) pos = K;
+  // a4: publish the pivot row's live A columns and its B part
+  if constexpr (J0 < NP) {
+    const uint32_t a0 = smem_u32(pa);
+#pragma unroll
+    for (int j = J0; j < NP; j += 16 / (int)sizeof(T)) {
+      if constexpr (sizeof(T) == 4) {
+        st_shared_v4_if(piv, a0 + 4u * j, x[j], x[j + 1], x[j + 2], x[j + 3]);
+      } else {
+        st_shared_v2_if(piv, a0 + 8u * j, x[j], x[j + 1]);
+      }
+    }
   }
-  // B part: every column
+  st_row_if<T, NR>(piv, pb, b);
+  if (piv) pa[NP] = x[K];   // the pivot itself (slot NP)
+  __syncwarp();
+  const T pk = pa[NP];
+  if (li == 0) rec_store(rec_g, K, pk, q);
+  const T nf = piv ? T(0) : -(x[K] * rcp(pk));
+  done = done || piv;
+  // a5: A columns right of K (16-byte loads from J0), then every B column
+  if constexpr (J0 < NP) {
+    T y[NP];
+#pragma unroll
+    for (int j = J0; j < NP; j += 16 / (int)sizeof(T)) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(pa + j);
+        y[j] = v.x; y[j + 1] = v.y; y[j + 2] = v.z; y[j + 3] = v.w;
+      } else {
+        const double2 v = *reinterpret_cast<const double2*>(pa + j);
+        y[j] = v.x; y[j + 1] = v.y;
+      }
+    }
+#pragma unroll
+    for (int j = K + 1; j < NP; ++j) x[j] = fma(nf, y[j], x[j]);
+  }
+  T yb[NR];
+  ld_row<T, NR>(yb, pb);
   if constexpr (sizeof(T) == 4 && NR % 2 == 0) {
 #pragma unroll
     for (int j = 0; j < NR; j += 2) ffma2(b[j], b[j + 1], nf, yb[j], yb[j + 1]);
   } else {
 #pragma unroll
     for (int j = 0; j < NR; ++j) b[j] = fma(nf, yb[j], b[j]);
+  }
+}
+
+template <typename T, int NP, int NR, int K>
+__device__ __forceinline__ void solve_steps(T (&x)[NP], T (&b)[NR], bool& done, int& pos, T* pa0, T* pb0,
+                                            unsigned char* rec_g, int li, int g) {
+  if constexpr (K < NP) {
+    constexpr int MPW = 32 / NP;
+    constexpr int PAW = NP + 4;   // pivot-row buffer width (A columns + the pivot, 16-byte rows)
+    // two buffers alternate, so step K+1's publish cannot overwrite what a slow lane of
+    // step K still reads
+    T* pa = pa0 + (K & 1) * MPW * PAW + g * PAW;
+    T* pb = pb0 + (K & 1) * MPW * NR + g * NR;
+    solve_step<T, NP, NR, K>(x, b, done, pos, pa, pb, rec_g, li);
+    solve_steps<T, NP, NR, K + 1>(x, b, done, pos, pa0, pb0, rec_g, li, g);
   }
 }
 
@@ -184,6 +226,13 @@ __global__ void __launch_bounds__(kSolveWarps * 32) gj_solve_kernel(SolveArgs a)
     const int64_t left = a.batch - item0;
     const int vi = left < MPW ? (int)left : MPW;
     const bool item_ok = g < vi;
+    // the next task's A and B into L2 while this one runs (the 16-byte aligned interior)
+    if (lane == 0 && task + (int64_t)gridDim.x * kSolveWarps < ntasks) {
+      const int64_t nx0 = (task + (int64_t)gridDim.x * kSolveWarps) * MPW;
+      const int64_t nx1 = nx0 + MPW < a.batch ? nx0 + MPW : a.batch;
+      prefetch_l2_range(Ag + nx0 * n * n, Ag + nx1 * n * n);
+      prefetch_l2_range(Bg + nx0 * n * m, Bg + nx1 * n * m);
+    }
     // ---- a1: A and B rows of the task into the padded staging rows
     move_rows<T, NP + 1, true>(const_cast<T*>(Ag) + item0 * n * n, sa, vi * n, n, n, NP, lane);
     move_rows<T, NR + 1, true>(const_cast<T*>(Bg) + item0 * n * m, sb, vi * n, m, n, NP, lane);
@@ -213,12 +262,8 @@ __global__ void __launch_bounds__(kSolveWarps * 32) gj_solve_kernel(SolveArgs a)
     bool done = false;
     int pos = li;
     // padded steps k >= n pick the identity padding rows and change nothing real
-#pragma unroll 1
-    for (int k = 0; k < NP; k += 2) {
-      solve_step<T, NP, NR, 0>(k, x, b, done, pos, pa0 + g * NP, pb0 + g * NR, rec_g, li);
-      solve_step<T, NP, NR, 1>(k + 1, x, b, done, pos, pa0 + MPW * NP + g * NP, pb0 + MPW * NR + g * NR, rec_g, li);
-      __syncwarp();
-    }
+    solve_steps<T, NP, NR, 0>(x, b, done, pos, pa0, pb0, rec_g, li, g);
+    __syncwarp();
 
     // ---- a6: det / ipiv / singular flag (lane li <-> step li)
     T p_own, p_k;
