@@ -127,12 +127,16 @@ struct FullSmem {
   static constexpr int per_warp = (STAGE + PROW + RECP + RECQ + PERM + MVEC + 15) / 16 * 16;
 };
 
+// resident CTAs per SM the register budget is sized for (fp64 n = 32 needs the most)
+template <typename T, int NP>
+constexpr int full_min_blocks() { return NP < 32 ? 4 : (sizeof(T) == 8 ? 2 : 3); }
+
 // STRAT: 2 = full pivoting (Obs. 2-3), 1 = partial (the listing: rows only, column k),
 // 0 = none (Eqs. (3)-(10) literally: pivot a_kk).  0 and 1 exist for the strategy /
 // rounding-error harness — the same arithmetic under each strategy;
 // the product partial-pivoting path is K1/K1b.
 template <typename T, int NP, int STRAT>
-__global__ void __launch_bounds__(kFullWarps * 32) gj_full_kernel(BatchedArgs a, int32_t* jpiv) {
+__global__ void __launch_bounds__(kFullWarps * 32, full_min_blocks<T, NP>()) gj_full_kernel(BatchedArgs a, int32_t* jpiv) {
   using S = FullSmem<T, NP>;
   constexpr int L = NP, MPW = S::MPW;
   using K = decltype(akey(T(0)));
