@@ -17,7 +17,8 @@ from typing import Optional
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["invert_batched", "invert_batched_full", "invert_batched_pivoting", "solve_batched", "invert", "det", "invert_batched_host", "GJError", "lib", "library_path",
+__all__ = ["invert_batched", "invert_batched_full", "invert_batched_pivoting", "solve_batched", "solve", "invert",
+           "det", "invert_batched_host", "GJError", "lib", "library_path",
            "TOL_DEFAULT", "Result"]
 
 TOL_DEFAULT = -1.0
@@ -43,6 +44,10 @@ def _load():
     L.gj_invert_batched_pivoting.restype = i32
     L.gj_solve_batched.argtypes = [i32, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, dbl, vp]
     L.gj_solve_batched.restype = i32
+    L.gj_solve.argtypes = [i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
+    L.gj_solve.restype = i32
+    L.gj_solve_workspace_size.argtypes = [i32, i32, i32]
+    L.gj_solve_workspace_size.restype = ctypes.c_size_t
     L.gj_det.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
     L.gj_det.restype = i32
     L.gj_invert.argtypes = [i32, i32, vp, i64, vp, i64, vp, vp, vp, vp, dbl, vp, ctypes.c_size_t, vp]
@@ -161,6 +166,31 @@ def solve_batched(A, B, tol: Optional[float] = None, *, out=None, stream=None) -
     if squeeze:
         return SolveResult(X[0], o_lg[0], o_sg[0], o_ipiv[0], o_info[0])
     return SolveResult(X, o_lg, o_sg, o_ipiv, o_info)
+
+
+def solve(A, B, tol: Optional[float] = None, *, out=None, stream=None) -> "SolveResult":
+    """``gj_solve``: one system X = A^-1 B of any order (strided rows allowed on the large
+    path; fp64 beyond n, nrhs <= 32)."""
+    torch = _torch()
+    if A.dim() != 2 or A.shape[0] != A.shape[1] or B.dim() != 2 or B.shape[0] != A.shape[0]:
+        raise ValueError("A must be [n, n] and B [n, nrhs]")
+    if A.stride(1) != 1 or B.stride(1) != 1 or A.dtype != B.dtype:
+        raise ValueError("unit column stride and one dtype required")
+    n, m = A.shape[0], B.shape[1]
+    dev = A.device
+    X = out if out is not None else torch.empty((n, m), dtype=A.dtype, device=dev)
+    o_ipiv = torch.empty((n,), dtype=torch.int32, device=dev)
+    o_lg = torch.empty((1,), dtype=torch.float64, device=dev)
+    o_sg = torch.empty((1,), dtype=torch.int8, device=dev)
+    o_info = torch.empty((1,), dtype=torch.int32, device=dev)
+    ws_bytes = lib.gj_solve_workspace_size(_dt(A), n, m)
+    ws = torch.empty((max(ws_bytes, 1),), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        st = lib.gj_solve(_dt(A), n, m, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), X.data_ptr(),
+                          X.stride(0), o_ipiv.data_ptr(), o_lg.data_ptr(), o_sg.data_ptr(), o_info.data_ptr(),
+                          TOL_DEFAULT if tol is None else float(tol), ws.data_ptr(), ws_bytes, _stream_ptr(stream))
+    _check(st)
+    return SolveResult(X, o_lg[0], o_sg[0], o_ipiv, o_info[0])
 
 
 PIVOTING = {"none": 0, "partial": 1, "full": 2}

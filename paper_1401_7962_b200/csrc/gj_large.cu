@@ -1068,6 +1068,105 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
   return cudaGetLastError();
 }
 
+// ============================================================================ large-n solve (f4)
+// X = A^-1 B for one fp64 matrix: the working array is [A | B] (npad x (npad + mpad)); the
+// panels and pivots are gj_invert's, and — as in the determinant-only mode — the trailing
+// update of panel k touches only the columns right of panel k+1: the rest of A and the
+// right-hand sides (the compact D columns on the left are never needed).  The pivot rows
+// end normalised, so the solution row k is the B part of the row pivoted at step k.
+namespace large {
+static int solve_ld(int npad, int m) { return npad + pad_to(m, 32); }
+size_t solve_workspace_bytes(int n, int m) {
+  const int npad = pad_to(n, 32), ld = solve_ld(npad, m);
+  return (size_t)npad * ld * 8 + (size_t)PANEL * ld * 8 + (size_t)npad * 8 + (size_t)npad * 4 * 4 + 256 + 1024 +
+         6 * 256;
+}
+// X[:, :npad] = blockdiag(A, I); X[:, npad:] = [B | 0; 0]
+__global__ void copy_pad_solve_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                                      int64_t ldb, int n, int m, double* __restrict__ X, int npad, int ld) {
+  const int64_t tot = (int64_t)npad * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / ld), j = (int)(e - (int64_t)i * ld);
+    double v;
+    if (j < npad) {
+      v = (i < n && j < n) ? A[(int64_t)i * lda + j] : (i == j ? 1.0 : 0.0);
+    } else {
+      const int c = j - npad;
+      v = (i < n && c < m) ? B[(int64_t)i * ldb + c] : 0.0;
+    }
+    X[e] = v;
+  }
+}
+// Xs[k][j] = X[rec_row[k]][npad + j]
+__global__ void solve_gather_kernel(const double* __restrict__ X, int ld, int npad, const int* __restrict__ rec_row,
+                                    int n, int m, double* __restrict__ Xs, int64_t ldx) {
+  const int k = blockIdx.y;
+  const double* src = X + (int64_t)rec_row[k] * ld + npad;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) Xs[(int64_t)k * ldx + j] = src[j];
+}
+}  // namespace large
+
+size_t large_solve_workspace_size(int n, int m) { return large::solve_workspace_bytes(n, m); }
+
+cudaError_t solve_large_f64(int n, int m, const double* A, int64_t lda, const double* B, int64_t ldb, double* Xs,
+                            int64_t ldx, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                            void* ws_ptr, cudaStream_t s) {
+  using namespace large;
+  const int npad = pad_to(n, 32);
+  const int ld = solve_ld(npad, m);
+  LeafCfg lc;
+  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
+  Workspace w;
+  {
+    char* p = static_cast<char*>(ws_ptr);
+    auto take = [&](size_t bytes) {
+      char* r = p;
+      p += (bytes + 255) / 256 * 256;
+      return r;
+    };
+    w.X = reinterpret_cast<double*>(take((size_t)npad * ld * 8));
+    w.R = reinterpret_cast<double*>(take((size_t)PANEL * ld * 8));
+    w.rec_p = reinterpret_cast<double*>(take((size_t)npad * 8));
+    w.rec_q = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.rec_row = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.pos = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.pivstep = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.smax = reinterpret_cast<unsigned long long*>(take(8));
+  }
+  cudaError_t e;
+  const int sms = device_sm_count();
+  init_perm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(npad, w.pos, w.pivstep);
+  copy_pad_solve_kernel<<<sms * 8, 256, 0, s>>>(A, lda, B, ldb, n, m, w.X, npad, ld);
+  cudaMemsetAsync(w.smax, 0, 8, s);
+  absmax_kernel<<<sms * 8, 256, 0, s>>>(A, lda, n, w.smax);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  auto factor_panel = [&](int P0, int pw) -> cudaError_t {
+    LeafArgs la{w.X, ld, npad, P0, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
+    if (lc.w == 32) return launch_leaf<32, 1>(la, lc.cl, s);
+    if (lc.w == 16) return launch_leaf<16, 2>(la, lc.cl, s);
+    return launch_leaf<8, 4>(la, lc.cl, s);
+  };
+  auto width = [&](int P0) { return (npad - P0) < PANEL ? (npad - P0) : PANEL; };
+  if ((e = factor_panel(0, width(0))) != cudaSuccess) return e;
+  for (int P0 = 0; P0 < npad; P0 += PANEL) {
+    const int pw = width(P0);
+    const int P1 = P0 + pw;
+    const int pw1 = P1 < npad ? width(P1) : 0;
+    // the panel's pivot rows, columns from P1 on (the right part of A and all of B)
+    gather_rows_kernel<<<dim3((ld / 2 + 255) / 256, pw), 256, 0, s>>>(w.X, ld, w.rec_row + P0, pw, w.R, P1, ld);
+    if (pw1 > 0) {
+      GemmArgs ga{w.X + P0, ld, w.R + P1, ld, w.X + P1, ld, npad, pw1, pw, w.pivstep, P0, P0 + pw, 0, 0};
+      if ((e = launch_gemm(ga, s)) != cudaSuccess) return e;
+      if ((e = factor_panel(P1, pw1)) != cudaSuccess) return e;
+    }
+    GemmArgs gb{w.X + P0, ld, w.R, ld, w.X, ld, npad, ld - P1 - pw1, pw, w.pivstep, P0, P0 + pw, 0, P1 + pw1};
+    if ((e = launch_gemm(gb, s, pw1 > 0 ? sms - lc.cl : 0, pw1 > 0 && !debug_sync())) != cudaSuccess) return e;
+  }
+  solve_gather_kernel<<<dim3((m + 127) / 128, n), 128, 0, s>>>(w.X, ld, npad, w.rec_row, n, m, Xs, ldx);
+  finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet, sign, nullptr, info);
+  return cudaGetLastError();
+}
+
 // ============================================================================ distributed
 // Column-block-cyclic large-n inversion over P ranks: global column block j
 // (DB = 128 columns, the panel width) lives on rank j % P.  Rows are complete on every

@@ -103,3 +103,65 @@ def test_identity_rhs_matches_inverse_path(gj, torch):
         e = np.abs(X - Xr).max(axis=(1, 2)) / np.abs(Xr).max(axis=(1, 2))
         assert np.all(e <= np.maximum(1e-10, kappa * 2.0 ** -52))
     assert np.array_equal(g["ipiv"], inv.ipiv.cpu().numpy())
+
+
+# ------------------------------------------------------------------ large n (gj_solve, fp64)
+def run_single(gj, torch, A, B, tol=None, strided=False):
+    At = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    Bt = torch.from_numpy(np.ascontiguousarray(B)).cuda()
+    if strided:   # views with padded rows
+        Ap = torch.zeros((A.shape[0], A.shape[1] + 7), dtype=At.dtype, device="cuda")
+        Ap[:, :A.shape[1]] = At
+        Bp = torch.zeros((B.shape[0], B.shape[1] + 3), dtype=Bt.dtype, device="cuda")
+        Bp[:, :B.shape[1]] = Bt
+        At, Bt = Ap[:, :A.shape[1]], Bp[:, :B.shape[1]]
+    r = gj.solve(At, Bt, tol)
+    torch.cuda.synchronize()
+    return r.X.cpu().numpy(), int(r.info), int(r.sign), float(r.logabsdet), r.ipiv.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,m", [(33, 1), (64, 5), (100, 40), (300, 7), (777, 3), (1024, 33)])
+def test_large_solve_vs_oracle(gj, torch, n, m):
+    A = synth.gen_gaussian(n, seed=900 + n)
+    B = np.random.default_rng(n).standard_normal((n, m))
+    X, info, sg, lg, ipiv = run_single(gj, torch, A, B, strided=(n % 2 == 1))
+    ref = oracle.solve_batched(A, B)
+    Ai = oracle.invert(A).inverse[0]
+    kappa = np.abs(A).sum(1).max() * np.abs(Ai).sum(1).max()
+    e = np.abs(X - ref.X[0]).max() / np.abs(ref.X[0]).max()
+    print(f"n={n} m={m}: rel err {e:.3e} kappa {kappa:.3e}")
+    assert info == 0
+    assert e <= max(1e-10, kappa * 2.0 ** -52)
+    assert ipiv_match(ipiv, ref.ipiv[0], ref.gap[0])[0]
+    assert sg == ref.sign[0] and abs(lg - ref.logabsdet[0]) <= max(1e-10, kappa * 2.0 ** -52)
+
+
+def test_large_solve_hadamard_exact(gj, torch):
+    """P6-style pin: every pivot a power of two and every value a small dyadic number, so
+    X = A^T B / n exactly for an integer B."""
+    n = 512
+    A = synth.hadamard_pd(n, seed=5)[0]
+    B = np.random.default_rng(3).integers(-4, 5, (n, 6)).astype(np.float64)
+    X, info, _, lg, _ = run_single(gj, torch, A, B)
+    assert info == 0
+    assert np.array_equal(X, A.T @ B / n)
+
+
+def test_large_solve_identity_rhs_matches_invert(gj, torch):
+    n = 700
+    A = synth.gen_gaussian(n, seed=77)
+    X, info, sg, lg, ipiv = run_single(gj, torch, A, np.eye(n))
+    r = gj.invert(torch.from_numpy(A).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(ipiv, r.ipiv.cpu().numpy())
+    assert lg == float(r.logabsdet) and sg == int(r.sign)
+    Xi = r.inverse.cpu().numpy()
+    assert np.abs(X - Xi).max() / np.abs(Xi).max() <= 1e-11
+
+
+def test_large_solve_singular(gj, torch):
+    A = synth.gen_gaussian(200, seed=78)
+    A[150] = A[20]
+    _, info, sg, lg, _ = run_single(gj, torch, A, np.ones((200, 2)), tol=1e-10)
+    ref = oracle.solve_batched(A, np.ones((200, 2)), tol=1e-10)
+    assert info == ref.info[0] > 0 and sg == 0 and lg == -np.inf
