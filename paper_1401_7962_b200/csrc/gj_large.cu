@@ -298,6 +298,21 @@ struct LeafSmem {
 // programmatic dependents at once, so the trailing GEMM of the previous panel (launched
 // right after it with programmatic stream serialisation) runs on the other SMs while
 // this panel is factored (look-ahead).
+#ifdef GJ_LEAF_PROF
+// diagnostic build only (tools/leaf_prof.sh): per-phase cycle sums of the leaf step, thread 0 of CTA 0
+__device__ unsigned long long g_leaf_prof[8];
+#define LEAF_T(i)                                                        \
+  do {                                                                   \
+    if (tid == 0 && rank == 0) {                                         \
+      const long long t_ = clock64();                                    \
+      if ((i) > 0) atomicAdd(&g_leaf_prof[(i)], (unsigned long long)(t_ - t_prev)); \
+      t_prev = t_;                                                       \
+    }                                                                    \
+  } while (0)
+#else
+#define LEAF_T(i) do { } while (0)
+#endif
+
 template <typename T, int W, int RPT>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -359,6 +374,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     auto step = [&](int kk, auto pc_tag, auto second_tag) {
       constexpr int PC = decltype(pc_tag)::value;
       constexpr bool SECOND = decltype(second_tag)::value;
+#ifdef GJ_LEAF_PROF
+      long long t_prev = 0;
+#endif
+      LEAF_T(0);
       const int kg = s0 + kk;
       const int gk = leaf * W + kk;   // step count within this launch: mbarrier phase
       const int b = gk & 1;
@@ -378,43 +397,51 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
       const uint32_t mh = __reduce_max_sync(0xffffffffu, has ? best.hi : 0u);
       const uint32_t ml = __reduce_max_sync(0xffffffffu, (has && best.hi == mh) ? best.lo : 0u);
       const uint32_t pw_ = __reduce_min_sync(0xffffffffu, (has && best.hi == mh && best.lo == ml) ? best.pos : 0xffffffffu);
-      // the warp winner writes key + row into its slot (then fences them into the async
-      // proxy: warp 0 ships the CTA winner's slot with cp.async.bulk)
+      // the warp winner writes its KEY into the warp's slot; only the CTA winner (picked by
+      // every warp from the keys after the barrier) writes its row values — one lane's
+      // 16-byte stores cost the shared pipe the same as a full warp's, so 16 warps writing
+      // whole rows every step was the largest part of the step
+      LEAF_T(1);
       const bool wwin = has && best.pos == pw_;
       T* const wsb = wslot + b * (kLeafThreads / 32) * EXW;
-      T* slot = wsb + warp * EXW;
-      if (pw_ == 0xffffffffu) {
-        if (lane == 0) reinterpret_cast<uint4*>(slot)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
-      } else {
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          if (wwin && bi == i) {
-            reinterpret_cast<uint4*>(slot)[0] = make_uint4(best.hi, best.lo, best.pos, best.row);
-#pragma unroll
-            for (int j = 0; j < W; j += 2) st2(slot + KEYT + j, x[i][j], x[i][j + 1]);
-          }
-        }
-      }
-      fence_async_smem();
+      if (lane == 0 && pw_ == 0xffffffffu) reinterpret_cast<uint4*>(wsb + warp * EXW)[0] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+      if (wwin) reinterpret_cast<uint4*>(wsb + warp * EXW)[0] = make_uint4(best.hi, best.lo, best.pos, best.row);
       __syncthreads();
-      // ---- warp 0: CTA winner; one bulk DSMEM copy per destination CTA (lane r -> CTA r),
-      // completing on the destination's mbarrier
-      if (warp == 0) {
-        const int nw = kLeafThreads / 32;
+      LEAF_T(2);
+      // ---- CTA winner (every warp picks it redundantly); its lane writes the row; warp d
+      // then ships the entry to CTA d with one bulk DSMEM copy completing on the
+      // destination's mbarrier — the CL copies issue in parallel from CL warps (a bulk copy
+      // takes warp-uniform operands, so one warp issuing all of them would serialise them)
+      {
+        constexpr int nw = kLeafThreads / 32;
         Cand c{0u, 0u, 0xffffffffu, 0u};
         if (lane < nw) {
           const uint4 k4 = reinterpret_cast<const uint4*>(wsb + lane * EXW)[0];
           c = Cand{k4.x, k4.y, k4.z, k4.w};
         }
         const int src_warp = warp_pick(c, lane < nw);
-        const uint32_t src = smem_u32(wsb + src_warp * EXW);
-        if (lane < (int)CL) {
-          const uint32_t ldst = smem_u32(exch + (size_t)(b * CL + rank) * EXW);
-          bulk_s2c(map_remote(ldst, (uint32_t)lane), src, (uint32_t)(EXW * (int)sizeof(T)), map_remote(smem_u32(&bars[b]), (uint32_t)lane));
+        if (warp == src_warp && wwin) {
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            if (bi == i) {
+              T* slot = wsb + warp * EXW;
+#pragma unroll
+              for (int j = 0; j < W; j += 2) st2(slot + KEYT + j, x[i][j], x[i][j + 1]);
+            }
+          }
+          fence_async_smem();
         }
+        __syncthreads();
+        const uint32_t src = smem_u32(wsb + src_warp * EXW);
+        const uint32_t ldst = smem_u32(exch + (size_t)(b * CL + rank) * EXW);
+        for (uint32_t d = (uint32_t)warp; d < CL; d += nw)
+          if (lane == 0)
+            bulk_s2c(map_remote(ldst, d), src, (uint32_t)(EXW * (int)sizeof(T)), map_remote(smem_u32(&bars[b]), d));
       }
+      LEAF_T(3);
       // ---- all: wait for the CL entries of this step, pick the cluster winner
       mbar_wait_all(&bars[b], (uint32_t)((gk >> 1) & 1));
+      LEAF_T(4);
       if (tid == 0) mbar_expect_tx(&bars[b], entry_bytes);   // arm the barrier for step gk + 2
       const T* ex0 = exch + (size_t)(b * CL) * EXW;
       Cand cc{0u, 0u, 0xffffffffu, 0u};
@@ -439,6 +466,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         }
       }
       const T rp = rcp_t(p);
+      LEAF_T(5);
       // ---- a3 + a5
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
@@ -453,6 +481,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         const T dcol = is_piv ? T(1) : nf;
         leaf_update<T, W, PC, SECOND>(x[i], y, nf, dcol);
       }
+      LEAF_T(6);
     };
 #pragma unroll 1
     for (int kk = 0; kk < W; kk += 2) {
@@ -1414,3 +1443,15 @@ cudaError_t dist_unpermute_unpack(int n, const double* recvbuf, const int* recv_
 }
 
 }  // namespace gj
+
+#ifdef GJ_LEAF_PROF
+extern "C" int gj_debug_leaf_prof(unsigned long long* out8, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out8, gj::large::g_leaf_prof, 8 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(gj::large::g_leaf_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
