@@ -147,17 +147,18 @@ gj_status gj_solve_batched(gj_dtype dt, int n, int nrhs, int64_t batch, const vo
  * gj_solve — X = A^-1 B for ONE system of any order n >= 1 with nrhs right-hand sides, by
  * Gauss–Jordan on [A | B] (Eq. (12) with B for I; Eqs. (14)-(15)) — SURVEY.md §8f f4.
  * n <= 32 and nrhs <= 32 with dense rows (lda == n, ldb == ldx == nrhs): the batched K7
- * kernel (batch 1).  Otherwise GJ_F64 only: the blocked large-n path on the working array
- * [A | B] — gj_invert's panels and pivots, with each panel's trailing update restricted to
- * the columns right of the next panel (the rest of A and all of B): ~2/3 n^3 + 2 n^2 nrhs.
+ * kernel (batch 1).  Otherwise the blocked large-n path on the working array [A | B] —
+ * gj_invert's panels and pivots (FP64 DMMA updates for GJ_F64, tcgen05 3xTF32 for GJ_F32),
+ * with each panel's trailing update restricted to the columns right of the next panel (the
+ * rest of A and all of B): ~2/3 n^3 + 2 n^2 nrhs.
  *   A, lda   input (row stride lda >= n), read only.
  *   B, ldb   right-hand sides, n x nrhs (row stride ldb >= nrhs), read only.
  *   X, ldx   solution, n x nrhs (row stride ldx >= nrhs); must not overlap A or B on the
  *            large path (may equal B on the batched path).
  *   ipiv, logabsdet, sign, info, tol  as gj_invert (each output may be NULL).
  *   workspace  device buffer of gj_solve_workspace_size(dt, n, nrhs) bytes (0: may be NULL).
- * Returns GJ_OK, GJ_ERR_ARG, GJ_ERR_UNSUPPORTED (GJ_F32 beyond the batched limits, or a
- * strided small system), GJ_ERR_WORKSPACE or GJ_ERR_CUDA.
+ * Returns GJ_OK, GJ_ERR_ARG, GJ_ERR_UNSUPPORTED (a strided system within the batched
+ * limits), GJ_ERR_WORKSPACE or GJ_ERR_CUDA.
  */
 gj_status gj_solve(gj_dtype dt, int n, int nrhs, const void* A, int64_t lda, const void* B, int64_t ldb, void* X,
                    int64_t ldx, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,

@@ -95,7 +95,7 @@ gj_status gj_solve_batched(gj_dtype dt, int n, int nrhs, int64_t batch, const vo
 size_t gj_solve_workspace_size(gj_dtype dt, int n, int nrhs) {
   if (n < 1 || nrhs < 1) return 0;
   if (n <= GJ_SOLVE_MAX_N && nrhs <= GJ_SOLVE_MAX_NRHS) return 0;
-  return dt == GJ_F64 ? large_solve_workspace_size(n, nrhs) : 0;
+  return dt == GJ_F64 ? large_solve_workspace_size(n, nrhs) : large_solve_workspace_size_f32(n, nrhs);
 }
 
 gj_status gj_solve(gj_dtype dt, int n, int nrhs, const void* A, int64_t lda, const void* B, int64_t ldb, void* X,
@@ -108,11 +108,14 @@ gj_status gj_solve(gj_dtype dt, int n, int nrhs, const void* A, int64_t lda, con
     if (lda != n || ldb != nrhs || ldx != nrhs) return GJ_ERR_UNSUPPORTED;   // the batched kernel is dense
     return gj_solve_batched(dt, n, nrhs, 1, A, B, X, ipiv, logabsdet, sign, info, tol, stream);
   }
-  if (dt != GJ_F64) return GJ_ERR_UNSUPPORTED;
   if (workspace == nullptr || workspace_bytes < gj_solve_workspace_size(dt, n, nrhs)) return GJ_ERR_WORKSPACE;
-  cudaError_t e = solve_large_f64(n, nrhs, static_cast<const double*>(A), lda, static_cast<const double*>(B), ldb,
-                                  static_cast<double*>(X), ldx, ipiv, logabsdet, sign, info, resolve_tol(dt, n, tol),
-                                  workspace, static_cast<cudaStream_t>(stream));
+  cudaError_t e = dt == GJ_F64
+      ? solve_large_f64(n, nrhs, static_cast<const double*>(A), lda, static_cast<const double*>(B), ldb,
+                        static_cast<double*>(X), ldx, ipiv, logabsdet, sign, info, resolve_tol(dt, n, tol), workspace,
+                        static_cast<cudaStream_t>(stream))
+      : solve_large_f32(n, nrhs, static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb,
+                        static_cast<float*>(X), ldx, ipiv, logabsdet, sign, info, resolve_tol(dt, n, tol), workspace,
+                        static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 

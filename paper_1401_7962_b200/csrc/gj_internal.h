@@ -42,6 +42,10 @@ struct SolveArgs {
 cudaError_t launch_solve_batched(gj_dtype dt, const SolveArgs& a, cudaStream_t s);
 // Large-n solve, fp64, one matrix (gj_large.cu): [A | B] with the det-only trailing update.
 size_t large_solve_workspace_size(int n, int m);
+size_t large_solve_workspace_size_f32(int n, int m);
+cudaError_t solve_large_f32(int n, int m, const float* A, int64_t lda, const float* B, int64_t ldb, float* Xs,
+                            int64_t ldx, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                            void* ws, cudaStream_t s);
 cudaError_t solve_large_f64(int n, int m, const double* A, int64_t lda, const double* B, int64_t ldb, double* Xs,
                             int64_t ldx, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
                             void* ws, cudaStream_t s);

@@ -895,26 +895,27 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
-// Ah/Al (npad x 128) = split X[:, P0 .. P0 + 128)
-__global__ void split_panel_f32(const float* __restrict__ X, int npad, int P0, float* __restrict__ Ah,
+// Ah/Al (npad x 128) = split X[:, P0 .. P0 + 128)  (X rows of stride ld)
+__global__ void split_panel_f32(const float* __restrict__ X, int64_t ld, int npad, int P0, float* __restrict__ Ah,
                                 float* __restrict__ Al) {
   const int64_t tot = (int64_t)npad * PANEL;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / PANEL), k = (int)(e - (int64_t)i * PANEL);
     float h, l;
-    split_tf32(X[(int64_t)i * npad + P0 + k], h, l);
+    split_tf32(X[(int64_t)i * ld + P0 + k], h, l);
     Ah[e] = h;
     Al[e] = l;
   }
 }
 
-// Bh/Bl (npad x 128): B[c][s] = split X[rows[s]][c]  (R transposed, through a 32 x 32 tile)
-__global__ void gather_split_T_f32(const float* __restrict__ X, int npad, const int* __restrict__ rows,
+// Bh/Bl (ncols x 128): B[c][s] = split X[rows[s]][c]  (R transposed, through a 32 x 32
+// tile; one block column per 32 columns of X, rows of stride ld)
+__global__ void gather_split_T_f32(const float* __restrict__ X, int64_t ld, const int* __restrict__ rows,
                                    float* __restrict__ Bh, float* __restrict__ Bl) {
   __shared__ float t[32][33];
   const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
-  for (int j = ty; j < 32; j += 8) t[j][tx] = X[(int64_t)rows[s0 + j] * npad + c0 + tx];
+  for (int j = ty; j < 32; j += 8) t[j][tx] = X[(int64_t)rows[s0 + j] * ld + c0 + tx];
   __syncthreads();
   for (int j = ty; j < 32; j += 8) {
     float h, l;
@@ -1006,7 +1007,7 @@ cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, in
   for (int P0 = 0; P0 < npad; P0 += PANEL) {
     const int P1 = P0 + PANEL;
     const bool nxt = P1 < npad;
-    f32::split_panel_f32<<<sms * 4, 256, 0, s>>>(w.X, npad, P0, w.Ah, w.Al);
+    f32::split_panel_f32<<<sms * 4, 256, 0, s>>>(w.X, npad, npad, P0, w.Ah, w.Al);
     f32::gather_split_T_f32<<<dim3(npad / 32, PANEL / 32), dim3(32, 8), 0, s>>>(w.X, npad, w.rec_row + P0, w.Bh, w.Bl);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (nxt) {
@@ -1032,6 +1033,123 @@ cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, in
                                      sign ? sign : w.sg, nullptr, info);
   if (det != nullptr)
     f32::finalize_det_f32<<<1, 1, 0, s>>>(logabsdet ? logabsdet : w.lg, sign ? sign : w.sg, det);
+  return cudaGetLastError();
+}
+
+// Large-n solve in fp32 (f4): invert_large_f32's panels on the working array [A | B]
+// (npad x (npad + mpad)), each trailing tcgen05 update restricted to the columns right of
+// the next panel (as gj_det) — the rest of A and all of B.
+namespace f32 {
+static int solve_mpad(int m) { return (m + 31) / 32 * 32; }
+static size_t solve_bytes(int n, int m) {
+  const size_t np = (size_t)pad128(n), ld = np + (size_t)solve_mpad(m);
+  return np * ld * 4 + 2 * np * PANEL * 4 + 2 * ld * PANEL * 4 + np * 8 + 4 * np * 4 + 64 + 16 * 256 + 1024;
+}
+__global__ void copy_pad_solve_f32(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+                                   int n, int m, float* __restrict__ X, int npad, int ld, unsigned long long* smax) {
+  float mx = 0.0f;
+  const int64_t tot = (int64_t)npad * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / ld), j = (int)(e - (int64_t)i * ld);
+    float v;
+    if (j < npad) {
+      if (i < n && j < n) {
+        v = A[(int64_t)i * lda + j];
+        mx = fmaxf(mx, fabsf(v));
+      } else {
+        v = (i == j) ? 1.0f : 0.0f;
+      }
+    } else {
+      const int c = j - npad;
+      v = (i < n && c < m) ? B[(int64_t)i * ldb + c] : 0.0f;
+    }
+    X[e] = v;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong((double)mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+    b = ob > b ? ob : b;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(smax, b);
+}
+__global__ void solve_gather_f32(const float* __restrict__ X, int ld, int npad, const int* __restrict__ rec_row, int n,
+                                 int m, float* __restrict__ Xs, int64_t ldx) {
+  const int k = blockIdx.y;
+  const float* src = X + (int64_t)rec_row[k] * ld + npad;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) Xs[(int64_t)k * ldx + j] = src[j];
+}
+}  // namespace f32
+
+size_t large_solve_workspace_size_f32(int n, int m) { return f32::solve_bytes(n, m); }
+
+cudaError_t solve_large_f32(int n, int m, const float* A, int64_t lda, const float* B, int64_t ldb, float* Xs,
+                            int64_t ldx, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                            void* ws_ptr, cudaStream_t s) {
+  using large::LeafCfg;
+  using large::LeafArgs;
+  using large::leaf_cfg;
+  using large::launch_leaf;
+  using large::debug_sync;
+  constexpr int PANEL = f32::PANEL;
+  const int npad = f32::pad128(n);
+  const int ld = npad + f32::solve_mpad(m);
+  LeafCfg lc;
+  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
+  f32::Workspace w;
+  {
+    char* p = static_cast<char*>(ws_ptr);
+    auto take = [&](size_t b) {
+      char* r = p;
+      p += (b + 255) / 256 * 256;
+      return r;
+    };
+    w.X = reinterpret_cast<float*>(take((size_t)npad * ld * 4));
+    w.Ah = reinterpret_cast<float*>(take((size_t)npad * PANEL * 4));
+    w.Al = reinterpret_cast<float*>(take((size_t)npad * PANEL * 4));
+    w.Bh = reinterpret_cast<float*>(take((size_t)ld * PANEL * 4));
+    w.Bl = reinterpret_cast<float*>(take((size_t)ld * PANEL * 4));
+    w.rec_p = reinterpret_cast<double*>(take((size_t)npad * 8));
+    w.rec_q = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.rec_row = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.pos = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.pivstep = reinterpret_cast<int*>(take((size_t)npad * 4));
+    w.smax = reinterpret_cast<unsigned long long*>(take(8));
+    w.lg = reinterpret_cast<double*>(take(8));
+    w.sg = reinterpret_cast<int8_t*>(take(8));
+  }
+  cudaError_t e;
+  const int sms = device_sm_count();
+  large::init_perm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(npad, w.pos, w.pivstep);
+  cudaMemsetAsync(w.smax, 0, 8, s);
+  f32::copy_pad_solve_f32<<<sms * 8, 256, 0, s>>>(A, lda, B, ldb, n, m, w.X, npad, ld, w.smax);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  auto factor_panel = [&](int P0) -> cudaError_t {
+    LeafArgs la{w.X, ld, npad, P0, P0, PANEL, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
+    if (lc.w == 32) return launch_leaf<32, 1, float>(la, lc.cl, s);
+    if (lc.w == 16) return launch_leaf<16, 2, float>(la, lc.cl, s);
+    return launch_leaf<8, 4, float>(la, lc.cl, s);
+  };
+  if ((e = factor_panel(0)) != cudaSuccess) return e;
+  for (int P0 = 0; P0 < npad; P0 += PANEL) {
+    const int P1 = P0 + PANEL;
+    const bool nxt = P1 < npad;
+    f32::split_panel_f32<<<sms * 4, 256, 0, s>>>(w.X, ld, npad, P0, w.Ah, w.Al);
+    f32::gather_split_T_f32<<<dim3(ld / 32, PANEL / 32), dim3(32, 8), 0, s>>>(w.X, ld, w.rec_row + P0, w.Bh, w.Bl);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (nxt) {
+      TcUpdateArgs ga{w.Ah, w.Al, w.Bh, w.Bl, w.X, ld, npad, PANEL, ld, w.pivstep, P0, P0 + PANEL, 0, P1};
+      if ((e = launch_tc_update(ga, 0, false, s)) != cudaSuccess) return e;
+      if ((e = factor_panel(P1)) != cudaSuccess) return e;
+    }
+    const int pw1 = nxt ? PANEL : 0;
+    TcUpdateArgs gb{w.Ah, w.Al, w.Bh, w.Bl, w.X, ld, npad, ld - P1 - pw1, ld, w.pivstep, P0, P0 + PANEL, 0, P1 + pw1};
+    const bool pdl = nxt && !large::no_pdl();
+    if ((e = launch_tc_update(gb, pdl ? sms - lc.cl : 0, pdl, s)) != cudaSuccess) return e;
+  }
+  f32::solve_gather_f32<<<dim3((m + 127) / 128, n), 128, 0, s>>>(w.X, ld, npad, w.rec_row, n, m, Xs, ldx);
+  large::finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet ? logabsdet : w.lg,
+                                     sign ? sign : w.sg, nullptr, info);
   return cudaGetLastError();
 }
 

@@ -165,3 +165,28 @@ def test_large_solve_singular(gj, torch):
     _, info, sg, lg, _ = run_single(gj, torch, A, np.ones((200, 2)), tol=1e-10)
     ref = oracle.solve_batched(A, np.ones((200, 2)), tol=1e-10)
     assert info == ref.info[0] > 0 and sg == 0 and lg == -np.inf
+
+
+@pytest.mark.parametrize("n,m", [(33, 2), (65, 1), (300, 40), (1024, 5)])
+def test_large_solve_f32_vs_oracle(gj, torch, n, m):
+    """fp32 beyond the batched limits: the tcgen05 (3xTF32) blocked path on [A | B]."""
+    A = synth.gen_gaussian(n, seed=950 + n).astype(np.float32)
+    B = np.random.default_rng(n + 1).standard_normal((n, m)).astype(np.float32)
+    X, info, sg, lg, ipiv = run_single(gj, torch, A, B)
+    ref = oracle.solve_batched(A, B)
+    Ai = oracle.invert(A).inverse[0]
+    kappa = np.abs(A.astype(np.float64)).sum(1).max() * np.abs(Ai).sum(1).max()
+    e = np.abs(X - ref.X[0]).max() / np.abs(ref.X[0]).max()
+    print(f"fp32 n={n} m={m}: rel err {e:.3e} kappa {kappa:.3e}")
+    assert info == 0
+    assert e <= max(TOL_INV[np.float32], kappa * 2.0 ** -23)
+    assert ipiv_match(ipiv, ref.ipiv[0], ref.gap[0])[0]
+    assert sg == ref.sign[0]
+
+
+def test_large_solve_f32_hadamard_exact(gj, torch):
+    n = 256
+    A = synth.hadamard_pd(n, seed=5)[0].astype(np.float32)
+    B = np.random.default_rng(4).integers(-4, 5, (n, 3)).astype(np.float32)
+    X, info, _, _, _ = run_single(gj, torch, A, B)
+    assert info == 0 and np.array_equal(X, (A.T.astype(np.float64) @ B / n).astype(np.float32))
