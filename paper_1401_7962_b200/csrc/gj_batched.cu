@@ -56,6 +56,11 @@ constexpr int kWarpsPerBlock = 4;
 // K1b: ballot fast path for the (usual) unique maximum; measured no faster on C2 (kept
 // as a build-time option, -DGJ_K1_FAST_PIVOT=1)
 constexpr bool kFastPivot = GJ_K1_FAST_PIVOT != 0;
+// K1b block loop unrolling (build option -DGJ_K1B_UNROLL=n, A/B measurements)
+#ifndef GJ_K1B_UNROLL
+#define GJ_K1B_UNROLL 1
+#endif
+constexpr int kK1bUnroll = GJ_K1B_UNROLL;
 
 // R rows per lane: two rows share every pivot-row load (halving the shared-memory
 // traffic of the broadcast, which bounds the fp32 n = 32 case); L = NP/R lanes per matrix.
@@ -796,7 +801,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     for (int s = 0; s < BS; ++s) blk_panel_step<R, BS>(s, s, P, kmask, pos, bs, rec_g, li, g, lane);
     // look-ahead: per iteration, publish block kb's pivot rows, apply its update to the
     // next panel first, then factor that panel while the rest of block kb's update runs
-#pragma unroll 1
+#pragma unroll kK1bUnroll
     for (int kb = 0; kb + BS < 32; kb += BS) {
       blk_publish<R, BS>(T, bs, rbuf_g);
       __syncwarp();

@@ -1,0 +1,11 @@
+# Build a variant of the library with extra nvcc flags into $1 (e.g. /tmp/ab1/libgjinv.so):
+#   bash tools/ab_build.sh /tmp/ab1 -DGJ_K1B_UNROLL=2
+set -e
+out=$1; shift
+mkdir -p $out
+cd paper_1401_7962_b200/csrc
+for f in gj_api gj_batched gj_batched64 gj_batched64b gj_fullpiv gj_solve gj_large gj_tcgemm gj_tma; do
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -I ../../include -c $f.cu -o $out/$f.o &
+done
+wait
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $out/libgjinv.so $out/*.o -lcuda
