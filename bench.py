@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=655360, help="oracle sample size (items, ~10 s of host work)")
     p.add_argument("--no-c4", action="store_true", help="skip the secondary n=8192 fp64 measurement")
-    p.add_argument("--workload", default="c2", choices=["c2", "c5"],
+    p.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
                    help="c2: the headline batched line; c5: one fp64 32768^2 matrix, column-block-cyclic over the ranks")
     p.add_argument("--n", type=int, default=32768, help="order for --workload c5")
     return p.parse_args()
@@ -400,6 +400,86 @@ def run_c5(args, rank, world, local):
     tdist.destroy_process_group()
 
 
+def run_c3(args, rank, world, local):
+    """BASELINE configs[2]: 262,144 x 64 x 64 fp64 (A = P L diag(u), 1% of the items with a
+    duplicated row, seed 2), tol 1e-10 (reading G1), K2b.  Each rank inverts its own batch
+    (weak scaling, no collective).  Roofline: the FP64 pipe (DFMA; 2n^3 - n^2 flops per item)
+    and HBM (inputs + inverse + ipiv + det outputs)."""
+    import torch
+    import paper_1401_7962_b200 as gj
+    import synth
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=dev)
+    A_host = synth.gen_c3(seed=2 + rank)
+    B, n = A_host.shape[0], A_host.shape[1]
+    A = torch.from_numpy(A_host).to(dev)
+    del A_host
+    X = torch.empty_like(A)
+    ip = torch.empty((B, n), dtype=torch.int32, device=dev)
+    lg = torch.empty(B, dtype=torch.float64, device=dev)
+    sg = torch.empty(B, dtype=torch.int8, device=dev)
+    dt_ = torch.empty(B, dtype=torch.float64, device=dev)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        st = gj.lib.gj_invert_batched(1, n, B, A.data_ptr(), X.data_ptr(), ip.data_ptr(), lg.data_ptr(),
+                                      sg.data_ptr(), dt_.data_ptr(), info.data_ptr(), synth.C3_TOL,
+                                      stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    with ClockSampler(local) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record(stream)
+        for _ in range(args.steps):
+            step()
+        b.record(stream)
+        barrier()
+    ms = a.elapsed_time(b) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        fl = B * (2.0 * n ** 3 - n ** 2)
+        tf = fl / (ms / 1e3) / 1e12
+        dfma_peak = 148 * 64 * 2 * 1.965e9 / 1e12   # FP64 FMA lanes x 2 flops x boost clock
+        hbm, hsrc = measured_peaks()
+        byts = B * (2 * n * n * 8 + n * 4 + 8 + 1 + 8 + 4)
+        print(json.dumps({
+            "metric": "matrices inverted/s (batched n=64 fp64)", "value": world * B / (ms / 1e3),
+            "unit": "matrices/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C3: batch 262144 x 64x64 fp64, A = P L diag(u), 1% duplicated-row items, "
+                                   "seed 2, tol 1e-10 (BASELINE.json configs[2])", "global_batch": B * world,
+                       "n": n, "parallelism": f"dp{world} (independent shards, no collective)",
+                       "l2": "inputs (8 GiB/GPU) larger than L2 (126 MB); no flush needed"},
+            "roofline": {"bound": "fp64", "achieved": tf, "peak": dfma_peak, "unit": "TFLOP/s",
+                         "frac": tf / dfma_peak, "traffic": None, "kernel": "gj_batched64b_kernel (K2b)",
+                         "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md unit counts)",
+                         "hbm_achieved_gbs": byts / (ms / 1e3) / 1e9, "hbm_peak_gbs": hbm},
+            "singular_items": int((info != 0).sum().item()), "gpu_launches": args.steps, "clocks": clk.summary()}),
+            flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -408,6 +488,9 @@ def main():
         return
     if args.workload == "c5":
         run_c5(args, rank, world, local)
+        return
+    if args.workload == "c3":
+        run_c3(args, rank, world, local)
         return
     import torch
     import paper_1401_7962_b200 as gj
