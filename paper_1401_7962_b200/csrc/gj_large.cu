@@ -575,7 +575,11 @@ constexpr int BM = 128, BN = 64, BK = 16;   // 2 CTAs per SM: one streams C whil
 constexpr int AST = BK + 4;    // A smem row stride (doubles): conflict-free fragment loads
 constexpr int BST = BN + 4;    // B smem row stride
 constexpr int kGemmThreads = 128;
-constexpr int GEMM_SMEM = 2 * (BM * AST + BK * BST) * (int)sizeof(double);
+#ifndef GJ_GEMM_NST
+#define GJ_GEMM_NST 2
+#endif
+constexpr int GEMM_NST = GJ_GEMM_NST;   // cp.async stages (build option, A/B)
+constexpr int GEMM_SMEM = GEMM_NST * (BM * AST + BK * BST) * (int)sizeof(double);
 
 struct GemmArgs {
   const double* A;
@@ -614,8 +618,8 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
 
 __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g) {
   extern __shared__ __align__(16) double gsm[];
-  double* As = gsm;                       // [2][BM][AST]
-  double* Bs = gsm + 2 * BM * AST;        // [2][BK][BST]
+  double* As = gsm;                       // [GEMM_NST][BM][AST]
+  double* Bs = gsm + GEMM_NST * BM * AST; // [GEMM_NST][BK][BST]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;       // 2 x 2 warps, warp tile 64 x 32
   const int gq = lane >> 2, tq = lane & 3;
@@ -672,15 +676,19 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g
   }
 
   const int nk = (g.K + BK - 1) / BK;   // K % 16 == 8 (8-wide leaves): zero-filled tail
-  load_stage(0, 0);
-  cp_async_commit();
-  for (int kb = 0; kb < nk; ++kb) {
-    if (kb + 1 < nk) load_stage((kb + 1) & 1, (kb + 1) * BK);
+#pragma unroll
+  for (int st = 0; st < GEMM_NST - 1; ++st) {
+    if (st < nk) load_stage(st, st * BK);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int kb = 0; kb < nk; ++kb) {
+    if (kb + GEMM_NST - 1 < nk) load_stage((kb + GEMM_NST - 1) % GEMM_NST, (kb + GEMM_NST - 1) * BK);
+    cp_async_commit();
+    cp_async_wait<GEMM_NST - 1>();
     __syncthreads();
-    const double* as = As + (kb & 1) * BM * AST + (wm * 64) * AST;
-    const double* bs = Bs + (kb & 1) * BK * BST + wn * 32;
+    const int cs = kb % GEMM_NST;
+    const double* as = As + cs * BM * AST + (wm * 64) * AST;
+    const double* bs = Bs + cs * BK * BST + wn * 32;
     // m16n8k16 (8 DMMA.8x8x4 in SASS); measured faster here than k-outer m8n8k4 issue
 #pragma unroll
     for (int k16 = 0; k16 < BK; k16 += 16) {
