@@ -67,3 +67,31 @@ def test_no_oracle_in_product_path():
             if fn.endswith((".py", ".cu", ".h", ".cpp", ".cuh")):
                 txt = open(os.path.join(dp, fn)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "gjo_" not in txt, fn
+
+
+def test_argument_errors_new_entries(gj):
+    """f2-f4 entry points: the same argument contract, answered without a GPU."""
+    L = gj.lib
+    # full / strategy kernels: n < 1, n > 32, bad strategy, NULL A, empty batch
+    assert L.gj_invert_batched_full(0, 0, 4, 1, None, None, None, None, None, None, None, -1.0, None) == 1
+    assert L.gj_invert_batched_full(0, 33, 4, 1, None, None, None, None, None, None, None, -1.0, None) == 2
+    assert L.gj_invert_batched_full(0, 8, 0, None, None, None, None, None, None, None, None, -1.0, None) == 0
+    assert L.gj_invert_batched_pivoting(0, 8, 4, 1, None, None, None, None, None, None, None, -1.0, 3, None) == 1
+    assert L.gj_invert_batched_pivoting(0, 8, 4, None, None, None, None, None, None, None, None, -1.0, 2, None) == 1
+    # batched solve: nrhs < 1, NULL B / X, limits
+    assert L.gj_solve_batched(0, 8, 0, 4, 1, 1, 1, None, None, None, None, -1.0, None) == 1
+    assert L.gj_solve_batched(0, 8, 2, 4, 1, None, 1, None, None, None, None, -1.0, None) == 1
+    assert L.gj_solve_batched(0, 8, 33, 4, 1, 1, 1, None, None, None, None, -1.0, None) == 2
+    assert L.gj_solve_batched(0, 8, 2, 0, None, None, None, None, None, None, None, -1.0, None) == 0
+    # single solve: bad leading dimensions, strided small system, missing workspace
+    assert L.gj_solve(1, 8, 2, 1, 7, 1, 2, 1, 2, None, None, None, None, -1.0, None, 0, None) == 1
+    assert L.gj_solve(1, 8, 2, 1, 9, 1, 2, 1, 2, None, None, None, None, -1.0, None, 0, None) == 2
+    assert L.gj_solve(1, 100, 2, 1, 100, 1, 2, 1, 2, None, None, None, None, -1.0, None, 0, None) == 3
+
+
+def test_solve_workspace_sizes(gj):
+    L = gj.lib
+    assert L.gj_solve_workspace_size(0, 32, 32) == 0     # the batched kernel: none
+    for dt in (0, 1):
+        small, big = L.gj_solve_workspace_size(dt, 100, 1), L.gj_solve_workspace_size(dt, 1000, 64)
+        assert 0 < small < big
