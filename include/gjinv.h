@@ -177,7 +177,7 @@ gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logab
                  void* workspace, size_t workspace_bytes, void* stream);
 
 /*
- * gj_invert — one n x n matrix, any n >= 1 (n <= 64 uses the batched kernels; larger n
+ * gj_invert — one n x n matrix, 1 <= n <= GJ_LARGE_MAX_N (n <= 64 uses the batched kernels; larger n
  * the blocked Gauss–Jordan: panel factorisation + tensor-core trailing updates, the
  * aggregated form of Eqs. (14)-(15): FP64 DMMA for GJ_F64; for GJ_F32 tcgen05.mma
  * kind::tf32 with the accumulator in TMEM and a 3xTF32 split for fp32 accuracy).
@@ -187,6 +187,7 @@ gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logab
  *   workspace    device buffer of at least gj_workspace_size(dt, n, 1, 1) bytes (may be
  *                NULL when that size is 0).
  */
+#define GJ_LARGE_MAX_N 65536   /* rows of one thread-block cluster's panel kernel (16 CTAs x 512 threads x 8) */
 gj_status gj_invert(gj_dtype dt, int n, const void* A, int64_t lda, void* Ainv, int64_t ldainv,
                     int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
                     void* workspace, size_t workspace_bytes, void* stream);

@@ -108,6 +108,7 @@ gj_status gj_solve(gj_dtype dt, int n, int nrhs, const void* A, int64_t lda, con
     if (lda != n || ldb != nrhs || ldx != nrhs) return GJ_ERR_UNSUPPORTED;   // the batched kernel is dense
     return gj_solve_batched(dt, n, nrhs, 1, A, B, X, ipiv, logabsdet, sign, info, tol, stream);
   }
+  if (n > GJ_LARGE_MAX_N) return GJ_ERR_UNSUPPORTED;
   if (workspace == nullptr || workspace_bytes < gj_solve_workspace_size(dt, n, nrhs)) return GJ_ERR_WORKSPACE;
   cudaError_t e = dt == GJ_F64
       ? solve_large_f64(n, nrhs, static_cast<const double*>(A), lda, static_cast<const double*>(B), ldb,
@@ -140,6 +141,7 @@ gj_status gj_det(gj_dtype dt, int n, int64_t batch, const void* A, double* logab
                  void* workspace, size_t workspace_bytes, void* stream) {
   if (n > GJ_BATCHED_MAX_N) {
     if ((dt != GJ_F64 && dt != GJ_F32) || batch != 1 || A == nullptr) return batch == 0 ? GJ_OK : GJ_ERR_UNSUPPORTED;
+    if (n > GJ_LARGE_MAX_N) return GJ_ERR_UNSUPPORTED;
     if (workspace == nullptr || workspace_bytes < gj_workspace_size(dt, n, 1, 2)) return GJ_ERR_WORKSPACE;
     cudaError_t e = dt == GJ_F64
         ? invert_large_f64(n, static_cast<const double*>(A), n, nullptr, 0, ipiv, logabsdet, sign,
@@ -161,6 +163,7 @@ gj_status gj_invert(gj_dtype dt, int n, const void* A, int64_t lda, void* Ainv, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t es = esize(dt);
   if (n > GJ_BATCHED_MAX_N) {
+    if (n > GJ_LARGE_MAX_N) return GJ_ERR_UNSUPPORTED;
     if (workspace == nullptr || workspace_bytes < gj_workspace_size(dt, n, 1, 1)) return GJ_ERR_WORKSPACE;
     cudaError_t e = dt == GJ_F64
         ? invert_large_f64(n, static_cast<const double*>(A), lda, static_cast<double*>(Ainv), ldainv, ipiv,

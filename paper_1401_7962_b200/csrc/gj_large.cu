@@ -511,17 +511,18 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         st2(Rs + sidx * 128 + 2 * cc2, u0, u1);
       }
       cluster_sync_all();   // every CTA has its copy before any CTA rewrites a pivot row
+      constexpr int CH = W < 8 ? W : 8;   // columns per chunk: never straddles the leaf
 #pragma unroll 1
-      for (int t0 = 0; t0 < pw; t0 += 8) {
+      for (int t0 = 0; t0 < pw; t0 += CH) {
         if (t0 >= c0 - P0 && t0 < c0 - P0 + W) continue;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           if (!valid[i]) continue;
           const bool rep = pst[i] >= s0 && pst[i] < s0 + W;   // pivot row of this leaf: replaced
           T* row = X + (int64_t)rowid[i] * ld + P0 + t0;
-          T v[8];
+          T v[CH];
 #pragma unroll
-          for (int j = 0; j < 8; j += 2) {
+          for (int j = 0; j < CH; j += 2) {
             if (rep) {
               v[j] = T(0);
               v[j + 1] = T(0);
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
           for (int sidx = 0; sidx < W; ++sidx) {
             const T* rr = Rs + sidx * 128 + t0;
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
+            for (int j = 0; j < CH; j += 2) {
               T r0, r1;
               ld2(rr + j, r0, r1);
               v[j] = fma(x[i][sidx], r0, v[j]);
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
             }
           }
 #pragma unroll
-          for (int j = 0; j < 8; j += 2) st2(row + j, v[j], v[j + 1]);
+          for (int j = 0; j < CH; j += 2) st2(row + j, v[j], v[j + 1]);
         }
       }
       __syncthreads();   // Rs / prow are rewritten by the next leaf
@@ -838,6 +839,7 @@ static bool leaf_cfg(int npad, LeafCfg* c) {
   if (npad <= 16 * kLeafThreads) { *c = {16, 1, 32}; return true; }
   if (npad <= 16 * kLeafThreads * 2) { *c = {16, 2, 16}; return true; }
   if (npad <= 16 * kLeafThreads * 4) { *c = {16, 4, 8}; return true; }
+  if (npad <= 16 * kLeafThreads * 8) { *c = {16, 8, 4}; return true; }
   return false;
 }
 
@@ -1009,7 +1011,8 @@ cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, in
     LeafArgs la{w.X, npad, npad, P0, P0, PANEL, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
     if (lc.w == 32) return launch_leaf<32, 1, float>(la, lc.cl, s);
     if (lc.w == 16) return launch_leaf<16, 2, float>(la, lc.cl, s);
-    return launch_leaf<8, 4, float>(la, lc.cl, s);
+    if (lc.w == 8) return launch_leaf<8, 4, float>(la, lc.cl, s);
+    return launch_leaf<4, 8, float>(la, lc.cl, s);
   };
   if ((e = factor_panel(0)) != cudaSuccess) return e;
   for (int P0 = 0; P0 < npad; P0 += PANEL) {
@@ -1136,7 +1139,8 @@ cudaError_t solve_large_f32(int n, int m, const float* A, int64_t lda, const flo
     LeafArgs la{w.X, ld, npad, P0, P0, PANEL, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
     if (lc.w == 32) return launch_leaf<32, 1, float>(la, lc.cl, s);
     if (lc.w == 16) return launch_leaf<16, 2, float>(la, lc.cl, s);
-    return launch_leaf<8, 4, float>(la, lc.cl, s);
+    if (lc.w == 8) return launch_leaf<8, 4, float>(la, lc.cl, s);
+    return launch_leaf<4, 8, float>(la, lc.cl, s);
   };
   if ((e = factor_panel(0)) != cudaSuccess) return e;
   for (int P0 = 0; P0 < npad; P0 += PANEL) {
@@ -1191,7 +1195,8 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
     LeafArgs la{w.X, npad, npad, P0, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
     if (lc.w == 32) return launch_leaf<32, 1>(la, lc.cl, s);
     if (lc.w == 16) return launch_leaf<16, 2>(la, lc.cl, s);
-    return launch_leaf<8, 4>(la, lc.cl, s);
+    if (lc.w == 8) return launch_leaf<8, 4>(la, lc.cl, s);
+    return launch_leaf<4, 8>(la, lc.cl, s);
   };
   auto width = [&](int P0) { return (npad - P0) < PANEL ? (npad - P0) : PANEL; };
   if ((e = factor_panel(0, width(0))) != cudaSuccess) return e;
@@ -1299,7 +1304,8 @@ cudaError_t solve_large_f64(int n, int m, const double* A, int64_t lda, const do
     LeafArgs la{w.X, ld, npad, P0, P0, pw, w.pos, w.pivstep, w.rec_p, w.rec_q, w.rec_row, nullptr};
     if (lc.w == 32) return launch_leaf<32, 1>(la, lc.cl, s);
     if (lc.w == 16) return launch_leaf<16, 2>(la, lc.cl, s);
-    return launch_leaf<8, 4>(la, lc.cl, s);
+    if (lc.w == 8) return launch_leaf<8, 4>(la, lc.cl, s);
+    return launch_leaf<4, 8>(la, lc.cl, s);
   };
   auto width = [&](int P0) { return (npad - P0) < PANEL ? (npad - P0) : PANEL; };
   if ((e = factor_panel(0, width(0))) != cudaSuccess) return e;
@@ -1492,7 +1498,8 @@ cudaError_t dist_factor(int n, int P, int rank, int k, double* Xl, int* pos, int
   LeafArgs la{Xl, nl, npad, c0, k * dist::DB, dist::DB, pos, pivstep, rec_p, rec_q, rec_row, W};
   return lc.w == 32 ? launch_leaf<32, 1>(la, lc.cl, s)
          : lc.w == 16 ? launch_leaf<16, 2>(la, lc.cl, s)
-                      : launch_leaf<8, 4>(la, lc.cl, s);
+         : lc.w == 8  ? launch_leaf<8, 4>(la, lc.cl, s)
+                      : launch_leaf<4, 8>(la, lc.cl, s);
 }
 
 // part 0: every local column except this rank's own panel k (gather + GEMM);

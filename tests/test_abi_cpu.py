@@ -95,3 +95,12 @@ def test_solve_workspace_sizes(gj):
     for dt in (0, 1):
         small, big = L.gj_solve_workspace_size(dt, 100, 1), L.gj_solve_workspace_size(dt, 1000, 64)
         assert 0 < small < big
+
+
+def test_large_order_limit(gj):
+    """Above GJ_LARGE_MAX_N (65536) the single-matrix entries answer GJ_ERR_UNSUPPORTED."""
+    L = gj.lib
+    n = 65536 + 128
+    assert L.gj_invert(1, n, 1, n, 1, n, None, None, None, None, -1.0, 1, 1 << 40, None) == 2
+    assert L.gj_det(1, n, 1, 1, None, None, None, None, None, -1.0, 1, 1 << 40, None) == 2
+    assert L.gj_solve(1, n, 1, 1, n, 1, 1, 1, 1, None, None, None, None, -1.0, 1, 1 << 40, None) == 2

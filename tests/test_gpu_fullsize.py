@@ -190,3 +190,22 @@ def test_c2_solve_sampled(gj, torch):
     e = np.abs(X[ok] - ref.X[ok]).max(axis=(1, 2)) / np.abs(ref.X[ok]).max(axis=(1, 2))
     print(f"C2 solve sample: max e/(kappa eps) {np.max(e / (kappa * 2.0 ** -23)):.3e}")
     assert np.all(e <= np.maximum(2e-4, kappa * 2.0 ** -23))
+
+
+def test_order_above_32768_exact(gj, torch):
+    """n = 32896 > 32768 (the W = 4 leaf, 8 rows per thread): blockdiag(P H D, I_128) with
+    the Sylvester-Hadamard block of order 32768 — exact inverse blockdiag(A_H^T / 32768, I)."""
+    m, n = 32768, 32896
+    H = _hadamard_device(torch, m)
+    A = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    A[:m, :m] = H
+    A[m:, m:] = torch.eye(n - m, dtype=torch.float64, device="cuda")
+    del H
+    r = gj.invert(A)
+    torch.cuda.synchronize()
+    assert int(r.info) == 0
+    X = r.inverse
+    assert bool(torch.equal(X[:m, :m], A[:m, :m].T / m))
+    assert bool(torch.equal(X[m:, m:], torch.eye(n - m, dtype=torch.float64, device="cuda")))
+    assert int(torch.count_nonzero(X[:m, m:])) == 0 and int(torch.count_nonzero(X[m:, :m])) == 0
+    assert abs(float(r.logabsdet) - 0.5 * m * math.log(m)) <= 1e-8
