@@ -919,11 +919,12 @@ template <int R, int BS, int NST>
 cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
   const size_t smem = BlkMisc<R, BS>::smem(NST);
   auto kern = gj_blk32_kernel<R, BS, NST>;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured |= dbit;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
@@ -979,11 +980,12 @@ cudaError_t launch_warp(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t 
   using S = Smem<T, NP, TMA>;
   const size_t smem = (size_t)S::per_warp * kWarpsPerBlock + 1024;
   auto kern = gj_batched_warp_kernel<T, NP, TMA>;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured |= dbit;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);

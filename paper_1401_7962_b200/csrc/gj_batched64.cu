@@ -346,11 +346,12 @@ template <typename T, bool TMA>
 cudaError_t launch64(const BatchedArgs& a, const Maps64& maps, cudaStream_t s) {
   const size_t smem = (size_t)L64<T>::TOTAL + 1024;
   auto kern = gj_batched64_kernel<T, TMA>;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured |= dbit;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);

@@ -415,11 +415,12 @@ cudaError_t launch_batched64b(const BatchedArgs& a, cudaStream_t s) {
     maps.x = maps.a;
   }
   const size_t smem = (size_t)SmemB::TOTAL + 1024;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaError_t e = cudaFuncSetAttribute(gj_batched64b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured |= dbit;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_batched64b_kernel, kThreadsB, smem);

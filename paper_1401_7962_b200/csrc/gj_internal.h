@@ -96,6 +96,13 @@ cudaError_t dist_unpermute_unpack(int n, const double* recvbuf, const int* recv_
 
 // Number of SMs of the current device (cached per device).
 int device_sm_count();
+// Bit of the current device: launch-time function attributes (dynamic shared memory,
+// cluster size) are per device context, so "configured once" caches are per device.
+inline unsigned long long device_bit() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return 1ull << (d & 63);
+}
 
 }  // namespace gj
 

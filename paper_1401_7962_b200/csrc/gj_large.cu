@@ -781,11 +781,12 @@ static Workspace carve(void* ws, int npad) {
 template <int W, int RPT, typename T = double>
 static cudaError_t launch_leaf(const LeafArgs& la, int cl, cudaStream_t s) {
   const size_t smem = (size_t)LeafSmem<T, W>::bytes(cl);
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaFuncSetAttribute(leaf_kernel<T, W, RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(leaf_kernel<T, W, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+    configured |= dbit;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cl, 1, 1);
@@ -807,10 +808,15 @@ static cudaError_t launch_leaf(const LeafArgs& la, int cl, cudaStream_t s) {
 static cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s, int grid_sms = 0, bool pdl = false) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaSuccess;
   static int per_sm = 0;
-  if (per_sm == 0) {
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaError_t e = cudaFuncSetAttribute(gemm_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_update_kernel, kGemmThreads, GEMM_SMEM);
+    configured |= dbit;
+  }
+  if (per_sm == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_update_kernel, kGemmThreads, GEMM_SMEM);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }

@@ -302,11 +302,12 @@ template <typename T, int NP, int NR>
 cudaError_t launch_solve_t(const SolveArgs& a, cudaStream_t s) {
   using S = SolveSmem<T, NP, NR>;
   const int smem = kSolveWarps * S::per_warp;
-  static bool configured = false;   // > 48 KB for fp64 with many right-hand sides
-  if (!configured) {
+  static unsigned long long configured = 0;   // > 48 KB for fp64 with many right-hand sides
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaError_t e = cudaFuncSetAttribute(gj_solve_kernel<T, NP, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured |= dbit;
   }
   const int64_t ntasks = (a.batch + S::MPW - 1) / S::MPW;
   const int64_t need = (ntasks + kSolveWarps - 1) / kSolveWarps;

@@ -252,11 +252,12 @@ cudaError_t launch_tc_update(const TcUpdateArgs& g, int grid_sms, bool pdl, cuda
       !make_tma_map_2d(&mp.bh, false, g.Bh, K, (uint64_t)g.Nrows, K * 4, KB, TN, 128) ||
       !make_tma_map_2d(&mp.bl, false, g.Bl, K, (uint64_t)g.Nrows, K * 4, KB, TN, 128))
     return cudaErrorInvalidValue;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
     cudaError_t e = cudaFuncSetAttribute(tc_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured |= dbit;
   }
   const int ntm = (g.M + TM - 1) / TM, ntn = (g.N + TN - 1) / TN;
   const int sms = grid_sms > 0 ? grid_sms : device_sm_count();
