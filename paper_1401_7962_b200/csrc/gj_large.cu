@@ -575,7 +575,13 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 constexpr int BM = 128, BN = 64, BK = 16;   // 2 CTAs per SM: one streams C while the other computes
 constexpr int AST = BK + 4;    // A smem row stride (doubles): conflict-free fragment loads
 constexpr int BST = BN + 4;    // B smem row stride
-constexpr int kGemmThreads = 128;
+#ifndef GJ_GEMM_WARPS
+#define GJ_GEMM_WARPS 4
+#endif
+constexpr int kGemmWarps = GJ_GEMM_WARPS;          // 4: warp tiles 64 x 32; 8: 32 x 32 (build option)
+constexpr int kGemmThreads = 32 * kGemmWarps;
+constexpr int WTM = kGemmWarps == 4 ? 64 : 32;    // warp tile rows
+constexpr int MT = WTM / 16;                      // m16 tiles per warp
 #ifndef GJ_GEMM_NST
 #define GJ_GEMM_NST 2
 #endif
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g
   double* As = gsm;                       // [GEMM_NST][BM][AST]
   double* Bs = gsm + GEMM_NST * BM * AST; // [GEMM_NST][BK][BST]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;       // 2 x 2 warps, warp tile 64 x 32
+  const int wm = warp >> 1, wn = warp & 1;       // (kGemmWarps/2) x 2 warps, warp tile WTM x 32
   const int gq = lane >> 2, tq = lane & 3;
   const int ntn = (g.N + BN - 1) / BN, ntm = (g.M + BM - 1) / BM;
   const int shift = g.skip_hi - g.skip_lo;
@@ -654,12 +660,12 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g
   };
 
   // accumulators initialised from C (0 for the rows the update replaces)
-  double acc[4][4][4];
+  double acc[MT][4][4];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
+  for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = m0 + wm * 64 + mt * 16 + gq + 8 * h;
+      const int r = m0 + wm * WTM + mt * 16 + gq + 8 * h;
       bool keep = r < g.M;
       if (keep) {
         const int ps = g.pivstep[r];
@@ -688,7 +694,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g
     cp_async_wait<GEMM_NST - 1>();
     __syncthreads();
     const int cs = kb % GEMM_NST;
-    const double* as = As + cs * BM * AST + (wm * 64) * AST;
+    const double* as = As + cs * BM * AST + (wm * WTM) * AST;
     const double* bs = Bs + cs * BK * BST + wn * 32;
     // m16n8k16 (8 DMMA.8x8x4 in SASS); measured faster here than k-outer m8n8k4 issue
 #pragma unroll
@@ -699,7 +705,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g
 #pragma unroll
         for (int i = 0; i < 4; ++i) bf[nt][i] = bs[(k16 + tq + 4 * i) * BST + nt * 8 + gq];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
+      for (int mt = 0; mt < MT; ++mt) {
         double af[8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -714,10 +720,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs g
   }
 
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = m0 + wm * 64 + mt * 16 + gq + 8 * h;
+      const int r = m0 + wm * WTM + mt * 16 + gq + 8 * h;
       if (r >= g.M) continue;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
