@@ -938,6 +938,16 @@ cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t
   return cudaGetLastError();
 }
 
+// K1t on/off (GJ_K1_TC=1).
+bool k1_tc() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GJ_K1_TC");
+    v = (e != nullptr && atoi(e) != 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // Variant of the fp32 n = 32 path: 0 = unblocked K1, 4 / 8 = K1b block size.  Fixed at
 // the best measured value; GJ_K1_BLOCK overrides it for A/B measurement only.
 int k1_block_size() {
@@ -1012,6 +1022,11 @@ cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
     const uint64_t rows = (uint64_t)a.batch * NP;
     const int swz = TL::SPAN >= 32 ? TL::SPAN : 0;
     if constexpr (NP == 32 && sizeof(T) == 4) {
+      // K1t (tensor-core blocked update), selected by GJ_K1_TC=1 while it is being measured
+      if (full && k1_tc()) {
+        const cudaError_t e = launch_tc32(a, s);
+        if (e != cudaErrorNotSupported) return e;
+      }
       // K1b (blocked): box of 32 * R rows (R matrices per warp task)
       const int bsz = k1_block_size();
       const int R = k1_rows();

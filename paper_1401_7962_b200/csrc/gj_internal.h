@@ -49,6 +49,9 @@ cudaError_t solve_large_f32(int n, int m, const float* A, int64_t lda, const flo
 cudaError_t solve_large_f64(int n, int m, const double* A, int64_t lda, const double* B, int64_t ldb, double* Xs,
                             int64_t ldx, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
                             void* ws, cudaStream_t s);
+// K1t, fp32 n = 32 with the blocked update on tcgen05 (gj_batched_tc.cu); cudaErrorNotSupported
+// if the buffers do not suit TMA.
+cudaError_t launch_tc32(const BatchedArgs& a, cudaStream_t s);
 // K6, n <= 32 (gj_fullpiv.cu): strategy 2 = full pivoting, 1 = partial, 0 = none; jpiv may be null.
 cudaError_t launch_batched_strategy(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, int strategy, cudaStream_t s);
 

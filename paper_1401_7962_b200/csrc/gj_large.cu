@@ -911,10 +911,13 @@ __global__ void copy_pad_f32(const float* __restrict__ A, int64_t lda, int n, fl
   if ((threadIdx.x & 31) == 0) atomicMax(smax, b);
 }
 
-// x = hi + lo with hi exactly representable in TF32 (low 13 mantissa bits cleared)
+// x = hi + lo, both rounded to TF32 (10 explicit mantissa bits; the tensor core ignores the
+// low 13 bits of an fp32 operand, so rounding them here halves the representation error):
+// |x - hi - lo| <= 2^-22 |x|
+__device__ __forceinline__ float round_tf32(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u); }
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
-  lo = x - hi;
+  hi = round_tf32(x);
+  lo = round_tf32(x - hi);
 }
 
 // Ah/Al (npad x 128) = split X[:, P0 .. P0 + 128)  (X rows of stride ld)

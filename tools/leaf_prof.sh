@@ -3,7 +3,7 @@
 set -e
 mkdir -p /tmp/leafprof
 cd paper_1401_7962_b200/csrc
-for f in gj_api gj_batched gj_batched64 gj_batched64b gj_fullpiv gj_solve gj_large gj_tcgemm gj_tma; do
+for f in $(ls *.cu | sed "s/\.cu$//"); do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -DGJ_LEAF_PROF -I ../../include -c $f.cu -o /tmp/leafprof/$f.o &
 done
 wait
