@@ -41,25 +41,33 @@ namespace {
 using namespace ptx;
 using namespace rowops;
 
-constexpr int TW = 4;                 // warps per CTA = matrices per task
+constexpr int TW = 4;                 // warps per CTA
+#ifndef GJ_TC_MH
+#define GJ_TC_MH 1
+#endif
+constexpr int MH = GJ_TC_MH;          // matrices per warp (lane = one row of each)
+constexpr int MPC = TW * MH;          // matrices per CTA task
 #ifndef GJ_TC_BS
 #define GJ_TC_BS 4
 #endif
-constexpr int TBS = GJ_TC_BS;         // block size (pivot steps per MMA): 4 or 8
-constexpr int TK = TW * TBS;          // K of the block product (16)
-constexpr int STAGE_B = 128 * 128;    // one task: 128 rows x 32 fp32 (TMA box, 128-byte swizzle)
-constexpr int BOP_B = 32 * 128;       // B operand: 32 rows (N) x 128 B (K-major)
-
-// TMEM columns: D (the four matrices) [0, 32); the A operand, hi / lo, [32, 32 + TK), [32 + TK, 32 + 2 TK)
-constexpr int TM_COLS = 32 + 2 * TK <= 64 ? 64 : 128;
+constexpr int TBS = GJ_TC_BS;         // block size (pivot steps per MMA)
+constexpr int TK = MPC * TBS;         // K of the block product (16 or 32)
+static_assert(TK <= 32, "one 128-byte K row");
+constexpr int TN = 32 * MH;           // N of the block product (a warp's matrices side by side)
+constexpr int STAGE_B = MPC * 32 * 128;   // one task: MPC matrices, rows of 128 B (TMA, 128-byte swizzle)
+constexpr int BOP_B = TN * 128;           // B operand: TN rows (N) x 128 B (K-major)
+// TMEM columns: D [0, TN) (matrix (w, h) in lanes 32w.., columns 32h..); A hi [TN, TN + TK),
+// A lo [TN + TK, TN + 2 TK)
+constexpr int TM_NEED = TN + 2 * TK;
+constexpr int TM_COLS = TM_NEED <= 32 ? 32 : TM_NEED <= 64 ? 64 : TM_NEED <= 128 ? 128 : 256;
 struct TcSmem {
-  static constexpr int STAGE = 0;                       // [STAGE_B]
-  static constexpr int BH = STAGE + STAGE_B;            // [BOP_B]
+  static constexpr int STAGE = 0;
+  static constexpr int BH = STAGE + STAGE_B;
   static constexpr int BL = BH + BOP_B;
-  static constexpr int RS = BL + BOP_B;                 // [TW][TBS][32] fp32 pivot rows (transpose staging)
-  static constexpr int REC = RS + TW * TBS * 32 * 4;    // [TW][32] (p, q)
-  static constexpr int PERM = REC + TW * 32 * 8;        // [TW][32] int
-  static constexpr int BAR = PERM + TW * 32 * 4;        // load, mma mbarriers; TMEM base
+  static constexpr int RS = BL + BOP_B;                  // [MPC][TBS][32] fp32 pivot rows (transpose staging)
+  static constexpr int PERM = RS;                        // [MPC][32] int — aliases RS (blocks done)
+  static constexpr int REC = RS + MPC * TBS * 32 * 4;    // [MPC][32] (p, q)
+  static constexpr int BAR = REC + MPC * 32 * 8;         // load, mma mbarriers; TMEM base
   static constexpr int BYTES = BAR + 32;
 };
 
@@ -75,8 +83,6 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-// D f32, A/B tf32, both K-major, N = 32, M = 128
-constexpr uint32_t kIdescT = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 
 // x = hi + lo, both rounded to TF32 (10 explicit mantissa bits; the tensor core ignores the
 // low 13 bits of an fp32 operand, so rounding them ourselves halves the representation
@@ -153,43 +159,56 @@ __device__ __forceinline__ void tm_st32(uint32_t addr, const float (&v)[32]) {
       : "memory");
 }
 
-// One panel step s (static) at global step k on the lane's panel values P (K1b's step with
-// one row per lane and one matrix per warp: full-warp reductions).
+// One panel step S (static) at global step k for each of the lane's MH matrices (full-warp
+// reductions per matrix; the MH chains are independent and interleave).
 template <int S>
-__device__ __forceinline__ void tc_panel_step(const int k, float (&P)[TBS], uint32_t& kmask, int& pos, int& bs,
-                                              unsigned char* rec_w, int lane) {
-  const uint32_t key = __float_as_uint(P[S]) & 0x7fffffffu & kmask;
-  const uint32_t m = __reduce_max_sync(0xffffffffu, key);
-  const uint32_t c = (key == m && kmask != 0u) ? ((uint32_t)pos << 5 | (uint32_t)lane) : 0xffffffffu;
-  const uint32_t win = __reduce_min_sync(0xffffffffu, c);
-  const int q = (int)(win >> 5), src = (int)(win & 31u);
-  const bool pv = lane == src;
-  float z[TBS];
+__device__ __forceinline__ void tc_panel_step(const int k, float (&P)[MH][TBS], uint32_t (&kmask)[MH],
+                                              int (&pos)[MH], int (&bs)[MH], unsigned char* rec, int mm0, int lane) {
+  uint32_t key[MH], m[MH], win[MH];
 #pragma unroll
-  for (int j = 0; j < TBS; ++j) z[j] = __shfl_sync(0xffffffffu, P[j], src);
-  const float p = z[S];
-  // 1/p (0 for a zero pivot: a singular item stays finite, so it cannot poison the
-  // neighbours' products); Eq. (15)'s multiplier with the deferred pivot-row scale
-  const float rp = p != 0.0f ? rcp(p) : 0.0f;
-  const float nf = pv ? 0.0f : -(P[S] * rp);
+  for (int h = 0; h < MH; ++h) {
+    key[h] = __float_as_uint(P[h][S]) & 0x7fffffffu & kmask[h];
+    m[h] = __reduce_max_sync(0xffffffffu, key[h]);
+  }
 #pragma unroll
-  for (int j = 0; j < TBS; ++j)
-    if (j != S) P[j] = fmaf(nf, z[j], P[j]);
-  P[S] = nf;   // compact D entry; 0 on the pivot row (W - S: its 1 is held as 0)
-  kmask = pv ? 0u : kmask;
-  bs = pv ? S : bs;
-  pos = (pos == k) ? q : pos;   // a3: the listing's swap of positions k and q (L156-L162)
-  pos = pv ? k : pos;
-  if (lane == 0) rec_store(rec_w, k, p, q);
-}
-template <int S>
-__device__ __forceinline__ void tc_panel_steps(const int kb, float (&P)[TBS], uint32_t& kmask, int& pos, int& bs,
-                                               unsigned char* rec_w, int lane) {
-  if constexpr (S < TBS) {
-    tc_panel_step<S>(kb + S, P, kmask, pos, bs, rec_w, lane);
-    tc_panel_steps<S + 1>(kb, P, kmask, pos, bs, rec_w, lane);
+  for (int h = 0; h < MH; ++h) {
+    const uint32_t c = (key[h] == m[h] && kmask[h] != 0u) ? ((uint32_t)pos[h] << 5 | (uint32_t)lane) : 0xffffffffu;
+    win[h] = __reduce_min_sync(0xffffffffu, c);
+  }
+#pragma unroll
+  for (int h = 0; h < MH; ++h) {
+    const int q = (int)(win[h] >> 5), src = (int)(win[h] & 31u);
+    const bool pv = lane == src;
+    float z[TBS];
+#pragma unroll
+    for (int j = 0; j < TBS; ++j) z[j] = __shfl_sync(0xffffffffu, P[h][j], src);
+    const float p = z[S];
+    // 1/p (0 for a zero pivot: a singular item stays finite, so it cannot poison the
+    // neighbours' products); Eq. (15)'s multiplier with the deferred pivot-row scale
+    const float rp = p != 0.0f ? rcp(p) : 0.0f;
+    const float nf = pv ? 0.0f : -(P[h][S] * rp);
+#pragma unroll
+    for (int j = 0; j < TBS; ++j)
+      if (j != S) P[h][j] = fmaf(nf, z[j], P[h][j]);
+    P[h][S] = nf;   // compact D entry; 0 on the pivot row (W - S: its 1 is held as 0)
+    kmask[h] = pv ? 0u : kmask[h];
+    bs[h] = pv ? S : bs[h];
+    pos[h] = (pos[h] == k) ? q : pos[h];   // a3: the listing's swap of positions k and q (L156-L162)
+    pos[h] = pv ? k : pos[h];
+    if (lane == 0) rec_store(rec + (mm0 + h) * 32 * 8, k, p, q);
   }
 }
+template <int S>
+__device__ __forceinline__ void tc_panel_steps(const int kb, float (&P)[MH][TBS], uint32_t (&kmask)[MH],
+                                               int (&pos)[MH], int (&bs)[MH], unsigned char* rec, int mm0, int lane) {
+  if constexpr (S < TBS) {
+    tc_panel_step<S>(kb + S, P, kmask, pos, bs, rec, mm0, lane);
+    tc_panel_steps<S + 1>(kb, P, kmask, pos, bs, rec, mm0, lane);
+  }
+}
+
+// D f32, A/B tf32, A from TMEM, B K-major: N = TN, M = 128
+constexpr uint32_t kIdescT = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 
 __global__ void __launch_bounds__(TW * 32) gj_tc32_kernel(BatchedArgs a, const __grid_constant__ CUtensorMap tma_a,
                                                           const __grid_constant__ CUtensorMap tma_x) {
@@ -205,12 +224,8 @@ __global__ void __launch_bounds__(TW * 32) gj_tc32_kernel(BatchedArgs a, const _
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sb + TcSmem::BAR + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int row = warp * 32 + lane;   // TMEM lane / stage row of this thread
-  float* rs_w = rs + warp * TBS * 32;
-  unsigned char* rec_w = rec + warp * 32 * 8;
-  int* perm_w = perm + warp * 32;
+  const int mm0 = warp * MH;   // the warp's first matrix within the task
 
-  // B operand: zero once (K columns beyond TK stay zero)
   for (int e = tid; e < 2 * BOP_B / 16; e += TW * 32) reinterpret_cast<uint4*>(bH)[e] = make_uint4(0u, 0u, 0u, 0u);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(TM_COLS));
@@ -226,93 +241,102 @@ __global__ void __launch_bounds__(TW * 32) gj_tc32_kernel(BatchedArgs a, const _
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   const uint32_t tm_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's lanes, column 0
-  // A operand in TMEM (block-diagonal): zero once; a row's nonzero K columns TBS w .. are
-  // rewritten every block
+  // A operand in TMEM (block-diagonal): zero once; a row's nonzero K columns are rewritten
+  // every block
   {
     float zz[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int c = 0; c < 2 * TK; c += 4) tm_st4(tm_row + 32u + (uint32_t)c, zz);
+    for (int c = 0; c < 2 * TK; c += 4) tm_st4(tm_row + (uint32_t)(TN + c), zz);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
 
-  const int64_t ntasks = (a.batch + TW - 1) / TW;
+  const int64_t ntasks = (a.batch + MPC - 1) / MPC;
   int it = 0, mph = 0;
   if (tid == 0 && (int64_t)blockIdx.x < ntasks) {
     mbar_expect_tx(&bars[0], STAGE_B);
-    tma_load_2d(stage, &tma_a, 0, (int)(blockIdx.x * 128), &bars[0]);
+    tma_load_2d(stage, &tma_a, 0, (int)(blockIdx.x * MPC * 32), &bars[0]);
   }
   for (int64_t task = blockIdx.x; task < ntasks; task += gridDim.x, ++it) {
-    const int64_t item = task * TW + warp;
-    const bool item_ok = item < a.batch;
     const int64_t nxt = task + gridDim.x;
-    if (tid == 0 && nxt < ntasks) bulk_prefetch_l2(static_cast<const float*>(a.A) + nxt * 128 * 32, STAGE_B);
+    if (tid == 0 && nxt < ntasks) bulk_prefetch_l2(static_cast<const float*>(a.A) + nxt * MPC * 32 * 32, STAGE_B);
     while (!mbar_try_wait(&bars[0], it & 1)) {
     }
-    // ---- a1: the lane's row into registers -> TMEM
-    float x[32];
+    // ---- a1: the lane's rows (one per matrix) into TMEM
+    uint32_t kmask[MH];
+    int pos[MH];
+    float tau[MH];
+    bool item_ok[MH];
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) {
-      const float4 v = *reinterpret_cast<const float4*>(stage + swz128(row, j));
-      x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+    for (int h = 0; h < MH; ++h) {
+      const int srow = (mm0 + h) * 32 + lane;
+      item_ok[h] = task * MPC + mm0 + h < a.batch;
+      float x[32];
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(stage + swz128(srow, j));
+        x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+      }
+      if (!item_ok[h]) {   // padding matrices: the identity (finite, harmless in the shared products)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = lane == j ? 1.0f : 0.0f;
+      }
+      float rowmax = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) rowmax = fmaxf(rowmax, fabsf(x[j]));
+      const double smax = (double)__uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(rowmax)));
+      tau[h] = round_down_to(a.tol * smax, 0.0f);
+      tm_st32(tm_row + (uint32_t)(32 * h), x);
+      kmask[h] = 0x7fffffffu;
+      pos[h] = lane;
     }
-    if (!item_ok) {   // padding matrices: the identity (finite, harmless in the shared products)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) x[j] = lane == j ? 1.0f : 0.0f;
-    }
-    float rowmax = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) rowmax = fmaxf(rowmax, fabsf(x[j]));
-    const double smax = (double)__uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(rowmax)));
-    const float tau = round_down_to(a.tol * smax, 0.0f);
-    tm_st32(tm_row, x);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 
-    uint32_t kmask = 0x7fffffffu;
-    int pos = lane;
 #pragma unroll 1
     for (int kb = 0; kb < 32; kb += TBS) {
       // ---- the block's panel columns out of TMEM; BS pivot steps on them
-      float P[TBS];
-      tm_ldp<TBS>(tm_row + (uint32_t)kb, P);
-      int bs = -1;
-      tc_panel_steps<0>(kb, P, kmask, pos, bs, rec_w, lane);
-      // the block's pivot rows as they were at the block's start (their panel columns,
-      // which the product must not touch, zeroed) -> transpose staging
-      {
+      float P[MH][TBS];
+#pragma unroll
+      for (int h = 0; h < MH; ++h) tm_ldp<TBS>(tm_row + (uint32_t)(32 * h + kb), P[h]);
+      int bs[MH];
+#pragma unroll
+      for (int h = 0; h < MH; ++h) bs[h] = -1;
+      tc_panel_steps<0>(kb, P, kmask, pos, bs, rec, mm0, lane);
+      // the block's pivot rows as they were at the block's start -> transpose staging
+#pragma unroll
+      for (int h = 0; h < MH; ++h) {
         float y[32];
-        tm_ld32(tm_row, y);
-        if (bs >= 0) {
-          float* dst = rs_w + bs * 32;
+        tm_ld32(tm_row + (uint32_t)(32 * h), y);
+        if (bs[h] >= 0) {
+          float* dst = rs + ((mm0 + h) * TBS + bs[h]) * 32;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
         }
-      }
-      tm_stp<TBS>(tm_row + (uint32_t)kb, P);   // the panel's compact values (W - S)
-      // A operand (TMEM): row `row`, K columns TBS w .. TBS w + TBS - 1 (hi / lo)
-      {
-        float h[TBS], l[TBS];
+        tm_stp<TBS>(tm_row + (uint32_t)(32 * h + kb), P[h]);   // the panel's compact values (W - S)
+        // A operand (TMEM): row = this lane, K columns TBS (mm0 + h) .. (hi / lo)
+        float hh[TBS], ll[TBS];
 #pragma unroll
-        for (int s = 0; s < TBS; ++s) split_tf32(P[s], h[s], l[s]);
-        tm_stp<TBS>(tm_row + 32u + (uint32_t)(TBS * warp), h);
-        tm_stp<TBS>(tm_row + 32u + (uint32_t)(TK + TBS * warp), l);
+        for (int s2 = 0; s2 < TBS; ++s2) split_tf32(P[h][s2], hh[s2], ll[s2]);
+        tm_stp<TBS>(tm_row + (uint32_t)(TN + TBS * (mm0 + h)), hh);
+        tm_stp<TBS>(tm_row + (uint32_t)(TN + TK + TBS * (mm0 + h)), ll);
       }
       __syncwarp();
-      // B operand (K-major: row j = matrix column j, K column TBS warp + s = step s's pivot
-      // row of this warp's matrix): lane j gathers column j of the four staged rows
-      {
-        float h[TBS], l[TBS];
+      // B operand (K-major): row 32 h + j (N) holds, in K columns TBS (mm0 + h) + s, column j
+      // of step s's pivot row of matrix (warp, h); lane j gathers its column
 #pragma unroll
-        for (int s = 0; s < TBS; ++s) {
-          float v = rs_w[s * 32 + lane];
+      for (int h = 0; h < MH; ++h) {
+        float hh[TBS], ll[TBS];
+#pragma unroll
+        for (int s2 = 0; s2 < TBS; ++s2) {
+          float v = rs[((mm0 + h) * TBS + s2) * 32 + lane];
           // the panel's own columns take no product term; and no Inf / NaN may enter the
-          // shared product (0 * Inf would reach the other three matrices)
+          // shared product (0 * Inf would reach the other matrices)
           v = (lane >= kb && lane < kb + TBS) || !(fabsf(v) <= 3.0e38f) ? 0.0f : v;
-          split_tf32(v, h[s], l[s]);
+          split_tf32(v, hh[s2], ll[s2]);
         }
 #pragma unroll
         for (int c = 0; c < TBS; c += 4) {
-          *reinterpret_cast<float4*>(bH + swz128(lane, TBS * warp + c)) = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
-          *reinterpret_cast<float4*>(bL + swz128(lane, TBS * warp + c)) = make_float4(l[c], l[c + 1], l[c + 2], l[c + 3]);
+          *reinterpret_cast<float4*>(bH + swz128(32 * h + lane, TBS * (mm0 + h) + c)) = make_float4(hh[c], hh[c + 1], hh[c + 2], hh[c + 3]);
+          *reinterpret_cast<float4*>(bL + swz128(32 * h + lane, TBS * (mm0 + h) + c)) = make_float4(ll[c], ll[c + 1], ll[c + 2], ll[c + 3]);
         }
       }
       fence_async_smem();
@@ -323,7 +347,7 @@ __global__ void __launch_bounds__(TW * 32) gj_tc32_kernel(BatchedArgs a, const _
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
         for (int kk = 0; kk < TK / 8; ++kk) {
-          const uint32_t ah = tmem + 32u + (uint32_t)(8 * kk), al = tmem + 32u + (uint32_t)(TK + 8 * kk);
+          const uint32_t ah = tmem + (uint32_t)(TN + 8 * kk), al = tmem + (uint32_t)(TN + TK + 8 * kk);
           const uint64_t bh = desc_sw128(smem_u32(bH) + kk * 32), bl = desc_sw128(smem_u32(bL) + kk * 32);
           asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(tmem), "r"(al), "l"(bh), "r"(kIdescT));
           asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(tmem), "r"(ah), "l"(bl), "r"(kIdescT));
@@ -338,54 +362,60 @@ __global__ void __launch_bounds__(TW * 32) gj_tc32_kernel(BatchedArgs a, const _
       asm volatile("tcgen05.fence::after_thread_sync;");
     }
 
-    // ---- a6: det / ipiv / singular flag from the record (lane = step)
-    float xr[32];
-    tm_ld32(tm_row, xr);
-    float p_own, p_k;
-    int q_own, q_k;
-    rec_load(rec_w, pos, p_own, q_own);
-    rec_load(rec_w, lane, p_k, q_k);
-    (void)q_own;
-    const float myrp = rcp(p_own);
-    const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau);
-    const int info = fb ? __ffs(fb) : 0;
-    const int nswap = __popc(__ballot_sync(0xffffffffu, q_k != lane));
-    const int nneg = __popc(__ballot_sync(0xffffffffu, p_k < 0.0f));
-    double lg = log_abs(p_k);
+    // ---- a6 + a7 + a8 per matrix
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
-    const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
-    if (item_ok) {
-      if (a.ipiv) a.ipiv[item * 32 + lane] = q_k + 1;
-      if (lane == 0) {
-        if (a.info) a.info[item] = info;
-        if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
-        if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
-        if (a.det) static_cast<float*>(a.det)[item] = info ? 0.0f : (float)(sgn * exp(lg));
+    for (int h = 0; h < MH; ++h) {
+      const int mm = mm0 + h;
+      const int64_t item = task * MPC + mm;
+      unsigned char* rec_m = rec + mm * 32 * 8;
+      int* perm_m = perm + mm * 32;
+      float xr[32];
+      tm_ld32(tm_row + (uint32_t)(32 * h), xr);
+      float p_own, p_k;
+      int q_own, q_k;
+      rec_load(rec_m, pos[h], p_own, q_own);
+      rec_load(rec_m, lane, p_k, q_k);
+      (void)q_own;
+      const float myrp = rcp(p_own);
+      const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau[h]);
+      const int info = fb ? __ffs(fb) : 0;
+      const int nswap = __popc(__ballot_sync(0xffffffffu, q_k != lane));
+      const int nneg = __popc(__ballot_sync(0xffffffffu, p_k < 0.0f));
+      double lg = log_abs(p_k);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+      const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
+      if (item_ok[h]) {
+        if (a.ipiv) a.ipiv[item * 32 + lane] = q_k + 1;
+        if (lane == 0) {
+          if (a.info) a.info[item] = info;
+          if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
+          if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
+          if (a.det) static_cast<float*>(a.det)[item] = info ? 0.0f : (float)(sgn * exp(lg));
+        }
+      }
+      // A^-1[k][perm[k']] = X[perm[k]][k'] / p through the stage (un-permutation, L179-L198)
+      if (a.Ainv != nullptr) {
+        perm_m[pos[h]] = lane;   // perm[k] = the row pivoted at step k = output column of compact column k
+        __syncwarp();
+        const int orow = mm * 32 + pos[h];
+#pragma unroll
+        for (int kp = 0; kp < 32; ++kp) *reinterpret_cast<float*>(stage + swz128(orow, perm_m[kp])) = myrp * xr[kp];
+        float* own = reinterpret_cast<float*>(stage + swz128(orow, lane));
+        *own = *own + myrp;   // the row's own compact entry was held as W - 1: add the 1 back
       }
     }
-    // ---- a7 + a8: A^-1[k][perm[k']] = X[perm[k]][k'] / p through the stage, TMA store
-    if (a.Ainv != nullptr) {
-      perm_w[pos] = lane;   // perm[k] = the row pivoted at step k = output column of compact column k
-      __syncwarp();
-      const int orow = warp * 32 + pos;
-#pragma unroll
-      for (int kp = 0; kp < 32; ++kp)
-        *reinterpret_cast<float*>(stage + swz128(orow, perm_w[kp])) = myrp * xr[kp];
-      float* own = reinterpret_cast<float*>(stage + swz128(orow, lane));
-      *own = *own + myrp;   // the row's own compact entry was held as W - 1: add the 1 back
-      fence_async_smem();
-    }
+    if (a.Ainv != nullptr) fence_async_smem();
     __syncthreads();   // every warp's rows are in the stage
     if (tid == 0) {
       if (a.Ainv != nullptr) {
-        tma_store_2d(&tma_x, 0, (int)(task * 128), stage);
+        tma_store_2d(&tma_x, 0, (int)(task * MPC * 32), stage);
         bulk_commit();
         bulk_wait_read0();   // the store has read the stage
       }
       if (nxt < ntasks) {
         mbar_expect_tx(&bars[0], STAGE_B);
-        tma_load_2d(stage, &tma_a, 0, (int)(nxt * 128), &bars[0]);
+        tma_load_2d(stage, &tma_a, 0, (int)(nxt * MPC * 32), &bars[0]);
       }
     }
   }
@@ -404,9 +434,9 @@ cudaError_t launch_tc32(const BatchedArgs& a, cudaStream_t s) {
   if (a.batch * 32 >= (int64_t(1) << 31)) return cudaErrorNotSupported;
   CUtensorMap ta, tx;
   const uint64_t rows = (uint64_t)a.batch * 32;
-  if (!make_tma_map_2d(&ta, false, a.A, 32, rows, 128, 32, 128, 128)) return cudaErrorNotSupported;
+  if (!make_tma_map_2d(&ta, false, a.A, 32, rows, 128, 32, MPC * 32, 128)) return cudaErrorNotSupported;
   if (a.Ainv != nullptr) {
-    if (!make_tma_map_2d(&tx, false, a.Ainv, 32, rows, 128, 32, 128, 128)) return cudaErrorNotSupported;
+    if (!make_tma_map_2d(&tx, false, a.Ainv, 32, rows, 128, 32, MPC * 32, 128)) return cudaErrorNotSupported;
   } else {
     tx = ta;
   }
@@ -432,7 +462,7 @@ cudaError_t launch_tc32(const BatchedArgs& a, cudaStream_t s) {
   if (per_sm > 512 / TM_COLS) per_sm = 512 / TM_COLS;   // tensor-memory columns
   if (per_sm < 1) per_sm = 1;
   if (getenv("GJ_TC_DEBUG")) fprintf(stderr, "tc32: smem %d per_sm %d\n", smem, per_sm);
-  const int64_t ntasks = (a.batch + TW - 1) / TW;
+  const int64_t ntasks = (a.batch + MPC - 1) / MPC;
   const int64_t cap = (int64_t)device_sm_count() * per_sm;
   const int grid = (int)(ntasks < cap ? ntasks : cap);
   gj_tc32_kernel<<<grid, TW * 32, smem, s>>>(a, ta, tx);
