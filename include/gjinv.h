@@ -197,16 +197,20 @@ size_t gj_workspace_size(gj_dtype dt, int n, int64_t batch, int entry);
 
 /*
  * gj_invert_batched_host — gj_invert_batched on HOST buffers (synchronous).  The library
- * allocates device staging buffers for `chunk` items at a time (chunk <= 0: automatic)
- * and pipelines host->device copy, inversion and device->host copy of consecutive
+ * stages `chunk` items at a time (chunk <= 0: automatic, 128 MiB) through four device
+ * buffers and pipelines host->device copy, inversion and device->host copy of consecutive
  * chunks on its own streams.  Pinned (page-locked) host buffers give overlapped copies;
- * pageable buffers work but copy synchronously.  Ainv must not alias A.
- * Returns as gj_invert_batched; all device memory it allocated is freed before return.
+ * pageable buffers work but copy synchronously.  Ainv must not alias A.  The streams and
+ * staging buffers are kept per device between calls (grown when a call needs more) and
+ * freed by gj_host_release(); concurrent calls on one device are serialised.
+ * Returns as gj_invert_batched.
  */
 gj_status gj_invert_batched_host(gj_dtype dt, int n, int64_t batch, const void* A_host,
                                  void* Ainv_host, int32_t* ipiv_host, double* logabsdet_host,
                                  int8_t* sign_host, void* det_host, int32_t* info_host,
                                  double tol, int64_t chunk);
+/* Frees the device staging buffers and streams gj_invert_batched_host keeps (all devices). */
+gj_status gj_host_release(void);
 
 /*
  * ---------------------------------------------------------------------------------------

@@ -56,6 +56,7 @@ def _load():
     L.gj_workspace_size.restype = ctypes.c_size_t
     L.gj_invert_batched_host.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, dbl, i64]
     L.gj_invert_batched_host.restype = i32
+    L.gj_host_release.restype = i32
     L.gj_status_string.argtypes = [i32]
     L.gj_status_string.restype = ctypes.c_char_p
     L.gj_version.restype = ctypes.c_char_p
@@ -306,3 +307,10 @@ def invert_batched_host(A, tol: Optional[float] = None, *, out=None, ipiv=None, 
                                     ptr(info), TOL_DEFAULT if tol is None else float(tol), int(chunk))
     _check(st)
     return out
+
+
+def host_release() -> None:
+    """``gj_host_release``: free the staging buffers and streams kept by
+    :func:`invert_batched_host` (all devices)."""
+    _check(lib.gj_host_release())
+

@@ -2,6 +2,7 @@
 // stream handling and the host-buffer pipeline.  No compute happens here: every step
 // of the method runs in the kernels of gj_batched.cu / gj_large.cu.
 #include <cuda_runtime.h>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -34,6 +35,28 @@ static size_t esize(gj_dtype dt) { return dt == GJ_F32 ? 4 : 8; }
 }  // namespace gj
 
 using namespace gj;
+
+namespace {
+// Per-device state of gj_invert_batched_host (kept between calls; gj_host_release frees it).
+struct HostCtx {
+  static constexpr int NB = 4;
+  struct Buf {
+    void* p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // X, ipiv, lg, sign, det, info
+    size_t cap[6] = {0, 0, 0, 0, 0, 0};
+    cudaEvent_t h = nullptr, k = nullptr, d = nullptr;
+  } b[NB];
+  cudaStream_t sH = nullptr, sK = nullptr, sD = nullptr;
+  bool ready = false;
+  std::mutex mu;
+};
+constexpr int kMaxDev = 64;
+HostCtx g_host[kMaxDev];
+HostCtx& host_ctx() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return g_host[(d >= 0 && d < kMaxDev) ? d : 0];
+}
+}  // namespace
 
 extern "C" {
 
@@ -204,61 +227,91 @@ gj_status gj_invert_batched_host(gj_dtype dt, int n, int64_t batch, const void* 
   if (chunk > batch) chunk = batch;
   // NB device buffers cycling through three streams — host->device copies, kernels,
   // device->host copies — ordered by events, so both copy directions and the kernels run
-  // back to back on their own engines (PCIe is full duplex).
-  constexpr int NB = 4;
-  struct Buf {
-    void* X = nullptr; int32_t* ipiv = nullptr; double* lg = nullptr;
-    int8_t* sg = nullptr; void* det = nullptr; int32_t* info = nullptr;
-    cudaEvent_t h = nullptr, k = nullptr, d = nullptr;
-  } b[NB];
-  cudaStream_t sH = nullptr, sK = nullptr, sD = nullptr;
+  // back to back on their own engines (PCIe is full duplex).  Streams, events and buffers
+  // are kept per device between calls (cudaMalloc / cudaFree per call cost tens of ms and
+  // made the end-to-end time erratic); gj_host_release() frees them.
+  HostCtx& C = host_ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
   gj_status st = GJ_OK;
   auto ck = [&](cudaError_t e) { if (e != cudaSuccess && st == GJ_OK) st = GJ_ERR_CUDA; return e == cudaSuccess; };
-  ck(cudaStreamCreateWithFlags(&sH, cudaStreamNonBlocking));
-  ck(cudaStreamCreateWithFlags(&sK, cudaStreamNonBlocking));
-  ck(cudaStreamCreateWithFlags(&sD, cudaStreamNonBlocking));
-  for (int i = 0; i < NB && st == GJ_OK; ++i) {
-    ck(cudaMalloc(&b[i].X, mat * chunk));
-    if (ipiv_host) ck(cudaMalloc(&b[i].ipiv, sizeof(int32_t) * n * chunk));
-    if (logabsdet_host) ck(cudaMalloc(&b[i].lg, sizeof(double) * chunk));
-    if (sign_host) ck(cudaMalloc(&b[i].sg, chunk));
-    if (det_host) ck(cudaMalloc(&b[i].det, es * chunk));
-    if (info_host) ck(cudaMalloc(&b[i].info, sizeof(int32_t) * chunk));
-    ck(cudaEventCreateWithFlags(&b[i].h, cudaEventDisableTiming));
-    ck(cudaEventCreateWithFlags(&b[i].k, cudaEventDisableTiming));
-    ck(cudaEventCreateWithFlags(&b[i].d, cudaEventDisableTiming));
+  if (!C.ready) {
+    ck(cudaStreamCreateWithFlags(&C.sH, cudaStreamNonBlocking));
+    ck(cudaStreamCreateWithFlags(&C.sK, cudaStreamNonBlocking));
+    ck(cudaStreamCreateWithFlags(&C.sD, cudaStreamNonBlocking));
+    for (int i = 0; i < HostCtx::NB; ++i) {
+      ck(cudaEventCreateWithFlags(&C.b[i].h, cudaEventDisableTiming));
+      ck(cudaEventCreateWithFlags(&C.b[i].k, cudaEventDisableTiming));
+      ck(cudaEventCreateWithFlags(&C.b[i].d, cudaEventDisableTiming));
+    }
+    if (st != GJ_OK) return st;
+    C.ready = true;
   }
+  const size_t need[6] = {mat * chunk, ipiv_host ? sizeof(int32_t) * n * chunk : 0, logabsdet_host ? sizeof(double) * chunk : 0,
+                          sign_host ? (size_t)chunk : 0, det_host ? es * chunk : 0, info_host ? sizeof(int32_t) * chunk : 0};
+  for (int i = 0; i < HostCtx::NB && st == GJ_OK; ++i)
+    for (int f = 0; f < 6; ++f)
+      if (need[f] > C.b[i].cap[f]) {
+        if (C.b[i].p[f]) ck(cudaFree(C.b[i].p[f]));
+        C.b[i].p[f] = nullptr;
+        C.b[i].cap[f] = 0;
+        if (ck(cudaMalloc(&C.b[i].p[f], need[f]))) C.b[i].cap[f] = need[f];
+      }
+  if (st != GJ_OK) return st;
   const char* Ah = static_cast<const char*>(A_host);
   char* Xh = static_cast<char*>(Ainv_host);
   for (int64_t c0 = 0, ci = 0; c0 < batch && st == GJ_OK; c0 += chunk, ++ci) {
-    Buf& B = b[ci % NB];
+    HostCtx::Buf& B = C.b[ci % HostCtx::NB];
+    void* X = B.p[0];
+    int32_t* ipiv = ipiv_host ? static_cast<int32_t*>(B.p[1]) : nullptr;
+    double* lg = logabsdet_host ? static_cast<double*>(B.p[2]) : nullptr;
+    int8_t* sg = sign_host ? static_cast<int8_t*>(B.p[3]) : nullptr;
+    void* det = det_host ? B.p[4] : nullptr;
+    int32_t* info = info_host ? static_cast<int32_t*>(B.p[5]) : nullptr;
     const int64_t m = (batch - c0) < chunk ? (batch - c0) : chunk;
-    if (ci >= NB) ck(cudaStreamWaitEvent(sH, B.d, 0));   // the buffer's previous results are out
-    ck(cudaMemcpyAsync(B.X, Ah + c0 * mat, m * mat, cudaMemcpyHostToDevice, sH));
-    ck(cudaEventRecord(B.h, sH));
-    ck(cudaStreamWaitEvent(sK, B.h, 0));
-    gj_status k = gj_invert_batched(dt, n, m, B.X, Xh ? B.X : nullptr, B.ipiv, B.lg, B.sg, B.det, B.info, tol, sK);
+    if (ci >= HostCtx::NB) ck(cudaStreamWaitEvent(C.sH, B.d, 0));   // the buffer's previous results are out
+    ck(cudaMemcpyAsync(X, Ah + c0 * mat, m * mat, cudaMemcpyHostToDevice, C.sH));
+    ck(cudaEventRecord(B.h, C.sH));
+    ck(cudaStreamWaitEvent(C.sK, B.h, 0));
+    gj_status k = gj_invert_batched(dt, n, m, X, Xh ? X : nullptr, ipiv, lg, sg, det, info, tol, C.sK);
     if (k != GJ_OK && st == GJ_OK) st = k;
-    ck(cudaEventRecord(B.k, sK));
-    ck(cudaStreamWaitEvent(sD, B.k, 0));
-    if (Xh) ck(cudaMemcpyAsync(Xh + c0 * mat, B.X, m * mat, cudaMemcpyDeviceToHost, sD));
-    if (ipiv_host) ck(cudaMemcpyAsync(ipiv_host + c0 * n, B.ipiv, sizeof(int32_t) * n * m, cudaMemcpyDeviceToHost, sD));
-    if (logabsdet_host) ck(cudaMemcpyAsync(logabsdet_host + c0, B.lg, sizeof(double) * m, cudaMemcpyDeviceToHost, sD));
-    if (sign_host) ck(cudaMemcpyAsync(sign_host + c0, B.sg, m, cudaMemcpyDeviceToHost, sD));
-    if (det_host) ck(cudaMemcpyAsync(static_cast<char*>(det_host) + c0 * es, B.det, es * m, cudaMemcpyDeviceToHost, sD));
-    if (info_host) ck(cudaMemcpyAsync(info_host + c0, B.info, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, sD));
-    ck(cudaEventRecord(B.d, sD));
+    ck(cudaEventRecord(B.k, C.sK));
+    ck(cudaStreamWaitEvent(C.sD, B.k, 0));
+    if (Xh) ck(cudaMemcpyAsync(Xh + c0 * mat, X, m * mat, cudaMemcpyDeviceToHost, C.sD));
+    if (ipiv) ck(cudaMemcpyAsync(ipiv_host + c0 * n, ipiv, sizeof(int32_t) * n * m, cudaMemcpyDeviceToHost, C.sD));
+    if (lg) ck(cudaMemcpyAsync(logabsdet_host + c0, lg, sizeof(double) * m, cudaMemcpyDeviceToHost, C.sD));
+    if (sg) ck(cudaMemcpyAsync(sign_host + c0, sg, m, cudaMemcpyDeviceToHost, C.sD));
+    if (det) ck(cudaMemcpyAsync(static_cast<char*>(det_host) + c0 * es, det, es * m, cudaMemcpyDeviceToHost, C.sD));
+    if (info) ck(cudaMemcpyAsync(info_host + c0, info, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, C.sD));
+    ck(cudaEventRecord(B.d, C.sD));
   }
-  for (cudaStream_t x : {sH, sK, sD})
-    if (x) ck(cudaStreamSynchronize(x));
-  for (int i = 0; i < NB; ++i) {
-    cudaFree(b[i].X); cudaFree(b[i].ipiv); cudaFree(b[i].lg); cudaFree(b[i].sg); cudaFree(b[i].det); cudaFree(b[i].info);
-    if (b[i].h) cudaEventDestroy(b[i].h);
-    if (b[i].k) cudaEventDestroy(b[i].k);
-    if (b[i].d) cudaEventDestroy(b[i].d);
+  for (cudaStream_t x : {C.sH, C.sK, C.sD}) ck(cudaStreamSynchronize(x));
+  return st;
+}
+
+gj_status gj_host_release(void) {
+  gj_status st = GJ_OK;
+  for (int d = 0; d < kMaxDev; ++d) {
+    HostCtx& C = g_host[d];
+    std::lock_guard<std::mutex> lock(C.mu);
+    if (!C.ready) continue;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cudaSetDevice(d) != cudaSuccess) { st = GJ_ERR_CUDA; continue; }
+    for (cudaStream_t x : {C.sH, C.sK, C.sD}) cudaStreamSynchronize(x);
+    for (int i = 0; i < HostCtx::NB; ++i) {
+      for (int f = 0; f < 6; ++f) {
+        if (C.b[i].p[f]) cudaFree(C.b[i].p[f]);
+        C.b[i].p[f] = nullptr;
+        C.b[i].cap[f] = 0;
+      }
+      cudaEventDestroy(C.b[i].h);
+      cudaEventDestroy(C.b[i].k);
+      cudaEventDestroy(C.b[i].d);
+    }
+    for (cudaStream_t x : {C.sH, C.sK, C.sD}) cudaStreamDestroy(x);
+    C.ready = false;
+    cudaSetDevice(cur);
   }
-  for (cudaStream_t x : {sH, sK, sD})
-    if (x) cudaStreamDestroy(x);
   return st;
 }
 
