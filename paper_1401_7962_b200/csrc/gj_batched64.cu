@@ -380,12 +380,16 @@ cudaError_t dispatch64(const BatchedArgs& a, cudaStream_t s) {
   return launch64<T, false>(a, maps, s);
 }
 
-// fp64 n = 64: 1 = column-split blocked K2b (default), 0 = K2 (GJ_K2_VARIANT, A/B only)
+// fp64 n = 64: 2 = K2d (DMMA blocked update; default, C3 18.7 ms), 1 = column-split
+// blocked K2b (20.7 ms), 0 = K2 (GJ_K2_VARIANT overrides for A/B measurement)
 int k2_variant() {
   static int v = -1;
   if (v < 0) {
-    v = 1;
-    if (const char* e = getenv("GJ_K2_VARIANT")) v = atoi(e) == 0 ? 0 : 1;
+    v = 2;
+    if (const char* e = getenv("GJ_K2_VARIANT")) {
+      v = atoi(e);
+      if (v < 0 || v > 2) v = 1;
+    }
   }
   return v;
 }
@@ -394,7 +398,11 @@ int k2_variant() {
 
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s) {
   if (a.batch == 0) return cudaSuccess;
-  if (dt == GJ_F64 && a.n == 64 && k2_variant() == 1) {
+  if (dt == GJ_F64 && a.n == 64 && k2_variant() == 2) {
+    const cudaError_t e = launch_batched64d(a, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  if (dt == GJ_F64 && a.n == 64 && k2_variant() >= 1) {
     const cudaError_t e = launch_batched64b(a, s);
     if (e != cudaErrorNotSupported) return e;
   }
