@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, GJ_K2D_MINB) gj_batched64d_kerne
       if (lane == 0) red[warp] = ((unsigned long long)mh << 32) | ml;
     }
     // warp 0's pivot state: rows lane and lane + 32
-    uint32_t kmask[2] = {0x7fffffffu, 0x7fffffffu};
+    uint32_t kmask[2] = {0xffffffffu, 0xffffffffu};   // all ones: eligible (the low key word keeps bit 31)
     int pos[2] = {lane, lane + 32};
     __syncthreads();
     double tau;
