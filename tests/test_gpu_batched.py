@@ -234,3 +234,21 @@ def test_single_strided(gj, torch):
     e = np.abs(r.inverse.cpu().numpy() - ref.inverse[0]).max() / np.abs(ref.inverse[0]).max()
     assert e <= TOL_INV[np.float64]
     assert np.array_equal(r.ipiv.cpu().numpy(), ref.ipiv[0])
+
+
+@pytest.mark.parametrize("n", [8, 32, 48, 64])
+@pytest.mark.parametrize("dtype,eps_bit", [(np.float32, 2.0 ** -20), (np.float64, 2.0 ** -21), (np.float64, 2.0 ** -44)])
+def test_near_tie_exact_max(gj, torch, n, dtype, eps_bit):
+    """Obs. 3 asks for THE maximum |a_ik|: candidates that differ only in the last mantissa
+    bits (below the R3 1e-6 tie band, so the general rule would excuse a wrong pick) must
+    still be ordered exactly — the key comparison may not drop any bit of the value."""
+    # fp64: 2^-21 is bit 31 of the low 32-bit key word, 2^-44 bit 8
+    rng = np.random.default_rng(n)
+    A = rng.uniform(-0.5, 0.5, (n, n))
+    A[:, 0] = 0.25
+    A[0, 0] = 1.0
+    A[n - 1, 0] = -(1.0 + eps_bit)          # the true maximum, at the last position
+    A = A.astype(dtype)[None]
+    g = run_gpu(gj, torch, A)
+    ref = oracle.invert_batched(A)
+    assert ref.ipiv[0, 0] == n and g["ipiv"][0, 0] == n

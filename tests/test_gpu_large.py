@@ -128,3 +128,19 @@ def test_c4_full_vs_stored_oracle(gj, torch, fname):
     assert abs(g["logabsdet"] - float(ref["logabsdet"])) <= max(1e-10, kappa * 2.0 ** -52)
     res = oracle.residual(A, g["inverse"], rows=ref["rows"])
     assert res <= TOL_RES[np.float64]
+
+
+@pytest.mark.parametrize("dtype,eps_bit", [(np.float64, 2.0 ** -21), (np.float64, 2.0 ** -44), (np.float32, 2.0 ** -20)])
+def test_near_tie_exact_max_large(gj, torch, dtype, eps_bit):
+    """The cluster argmax of the panel kernel orders candidates by every bit (see the batched
+    test of the same name): the true maximum sits at the last row."""
+    n = 300
+    rng = np.random.default_rng(3)
+    A = rng.uniform(-0.5, 0.5, (n, n))
+    A[:, 0] = 0.25
+    A[0, 0] = 1.0
+    A[n - 1, 0] = -(1.0 + eps_bit)
+    A = A.astype(dtype)
+    r = gj.invert(torch.from_numpy(A).cuda())
+    torch.cuda.synchronize()
+    assert int(r.ipiv[0]) == n
