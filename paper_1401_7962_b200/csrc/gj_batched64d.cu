@@ -69,10 +69,30 @@ __device__ __forceinline__ double rcp64d(double p) {
   return fma(r, e, r);
 }
 
+#ifdef GJ_K2D_PROF
+// diagnostic build only (tools/k2d_prof.py): per-phase cycle sums of warp 0's pivot step
+// (CTA 0, lane 0)
+__device__ unsigned long long g_k2d_prof[8];
+#define K2D_T(i)                                                                          \
+  do {                                                                                    \
+    if (lane == 0 && blockIdx.x == 0) {                                                   \
+      const long long t_ = clock64();                                                     \
+      if ((i) > 0) atomicAdd(&g_k2d_prof[(i)], (unsigned long long)(t_ - t_prev));       \
+      t_prev = t_;                                                                        \
+    }                                                                                     \
+  } while (0)
+#else
+#define K2D_T(i) do { } while (0)
+#endif
+
 // Warp 0's pivot step S (static) at global step k on the panel rows lane and lane + 32.
 template <int S>
 __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
                                              int (&bs)[2], unsigned char* rec, int* rowk, int lane) {
+#ifdef GJ_K2D_PROF
+  long long t_prev = 0;
+#endif
+  K2D_T(0);
   uint32_t hi[2], lo[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -94,11 +114,14 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
   const int q = (int)(win >> 6);
   const int src = (int)((win >> 1) & 31u);
   const int slot = (int)(win & 1u);
+  K2D_T(1);
   double z[BSD];
 #pragma unroll
   for (int j = 0; j < BSD; ++j) z[j] = shfl_dd(slot ? x[1][j] : x[0][j], src);
   const double p = z[S];
+  K2D_T(2);
   const double rp = rcp64d(p);
+  K2D_T(3);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const bool pv = pos[r] == q && kmask[r] != 0u;
@@ -112,10 +135,12 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
     pos[r] = (pos[r] == k) ? q : pos[r];   // a3: the listing's swap of positions k and q (L156-L162)
     pos[r] = pv ? k : pos[r];
   }
+  K2D_T(4);
   if (lane == 0) {
     rec_store(rec, k, p, q);
     rowk[k] = src + 32 * slot;
   }
+  K2D_T(5);
 }
 template <int S>
 __device__ __forceinline__ void d_panel_steps(const int kb, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
@@ -329,3 +354,15 @@ cudaError_t launch_batched64d(const BatchedArgs& a, cudaStream_t s) {
 }
 
 }  // namespace gj
+
+#ifdef GJ_K2D_PROF
+extern "C" int gj_debug_k2d_prof(unsigned long long* out8, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out8, gj::g_k2d_prof, 8 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(gj::g_k2d_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
