@@ -12,7 +12,10 @@ __global__ void k(float* out) {
   if (PAT == 0) off = 0;                       // all 32 lanes one address
   else if (PAT == 1) off = (lane >> 4) * 112;  // two half-warps, two addresses (distinct banks)
   else if (PAT == 2) off = (lane >> 3) * 112;  // four quarter-warps
-  else off = lane * 4;                         // all distinct (512 B)
+  else if (PAT == 3) off = lane * 4;           // all distinct (512 B)
+  else if (PAT == 4) off = (lane >> 4) * 4;    // two half-warps, adjacent 16-byte chunks
+  else if (PAT == 5) off = (lane >> 4) * 8;    // two half-warps, 32 bytes apart
+  else off = (lane >> 4) * 16;                 // two half-warps, 64 bytes apart (same 128-B line)
   float a = 0;
   for (int i = 0; i < 1024; ++i) {
     float4 v; asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"((unsigned)__cvta_generic_to_shared(s + ((off + (i & 7) * 32) & 4095))));
@@ -22,6 +25,6 @@ __global__ void k(float* out) {
 }
 int main() {
   float* o; cudaMalloc(&o, 4096);
-  k<0><<<1, 32>>>(o); k<1><<<1, 32>>>(o); k<2><<<1, 32>>>(o); k<3><<<1, 32>>>(o);
+  k<0><<<1, 32>>>(o); k<1><<<1, 32>>>(o); k<2><<<1, 32>>>(o); k<3><<<1, 32>>>(o); k<4><<<1, 32>>>(o); k<5><<<1, 32>>>(o); k<6><<<1, 32>>>(o);
   cudaDeviceSynchronize(); printf("ok\n"); return 0;
 }
