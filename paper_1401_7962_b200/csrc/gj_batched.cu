@@ -938,6 +938,332 @@ cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ K1s: blocked solve / det, fp32 n = 32
+// [A | B] -> [diag(p) | P B] by K1b's blocked elimination (R = 2 rows per lane, two
+// matrices per warp, BS = 4, the same panel step, tie-break, record and look-ahead), but
+// nothing left of the current panel is kept: the compact D columns are dropped (the
+// "skip the D half" of SURVEY.md §8f f4 — the det-only and solve variants never need
+// A^-1), so block KB's trailing update covers only the columns right of the next panel plus
+// the NR right-hand-side columns.  The eight blocks are unrolled (static column ranges, no
+// register rotation).  At the end the row pivoted at step k holds p_k x_k (Eq. (12) with B
+// in place of I): X[k][:] = b_row / p_k, a row gather.  NR = 0 is the determinant-only run.
+struct BlkSolveArgs {
+  int64_t batch;
+  int m;                // right-hand sides actually present (<= NR)
+  const float* B;       // [batch][32][m]
+  float* X;             // [batch][32][m], may alias B
+  int32_t* ipiv;
+  double* logabsdet;
+  int8_t* sign;
+  float* det;
+  int32_t* info;
+  double tol;
+};
+
+template <int NR>
+struct SolveBlk {
+  static constexpr int R = 2, BS = 4, NST = 2;
+  static constexpr int NRP = NR == 0 ? 0 : (NR + 3) / 4 * 4;
+  static constexpr int RS = 32 + NRP;                                // pivot-row record: absolute column, then B
+  static constexpr int RBUF = BlkGeo<R>::M * BS * RS * 4;
+  static constexpr int REC = BlkGeo<R>::M * 32 * 8;
+  static constexpr int BYTES = RBUF + REC + 16;
+  static constexpr int smem() { return kWarpsPerBlock * (NST * BlkGeo<R>::STAGE + BYTES) + 1024; }
+};
+
+// the pivot rows of block KB publish their columns [(KB + 1) BS, 32) and their B part
+template <int NR, int KB>
+__device__ __forceinline__ void slv_publish(const float (&x)[2][32], const float (&b)[2][NR > 0 ? NR : 1],
+                                            const int (&bs)[2], float* rb) {
+  using S = SolveBlk<NR>;
+  constexpr int C0 = (KB + 1) * S::BS;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const bool on = bs[r] >= 0;
+    const uint32_t dst = smem_u32(rb) + (uint32_t)(on ? bs[r] : 0) * (S::RS * 4);
+#pragma unroll
+    for (int j = C0; j < 32; j += 4) st_shared_v4_if(on, dst + 4u * j, x[r][j], x[r][j + 1], x[r][j + 2], x[r][j + 3]);
+    if constexpr (NR % 4 == 0 && NR > 0) {
+#pragma unroll
+      for (int j = 0; j < NR; j += 4) st_shared_v4_if(on, dst + 4u * (32 + j), b[r][j], b[r][j + 1], b[r][j + 2], b[r][j + 3]);
+    } else if constexpr (NR > 0) {
+      if (on) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) rb[bs[r] * S::RS + 32 + j] = b[r][j];
+      }
+    }
+  }
+}
+
+// rank-1 term s of block KB's update on the A columns [J0, 32) and the B columns
+template <int NR, int J0>
+__device__ __forceinline__ void slv_trail(float (&x)[2][32], float (&b)[2][NR > 0 ? NR : 1], const float (&P)[2][4], int s,
+                                          const float* rb) {
+  using S = SolveBlk<NR>;
+  if constexpr (J0 < 32) {
+    float Rs[32 - J0];
+    ld_row<float, 32 - J0>(Rs, rb + s * S::RS + J0);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < 32 - J0; j += 2) ffma2(x[r][J0 + j], x[r][J0 + j + 1], P[r][s], Rs[j], Rs[j + 1]);
+  }
+  if constexpr (NR > 0) {
+    float Rb[NR];
+    ld_row<float, NR>(Rb, rb + s * S::RS + 32);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if constexpr (NR % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < NR; j += 2) ffma2(b[r][j], b[r][j + 1], P[r][s], Rb[j], Rb[j + 1]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) b[r][j] = fmaf(P[r][s], Rb[j], b[r][j]);
+      }
+    }
+  }
+}
+
+// block KB has been factored (panel values P = W - S); apply its update, factoring block
+// KB + 1 under it (look-ahead), then recurse
+template <int NR, int KB>
+__device__ __forceinline__ void slv_blocks(float (&x)[2][32], float (&b)[2][NR > 0 ? NR : 1], float (&P)[2][4],
+                                           uint32_t (&kmask)[2], int (&pos)[2], int (&bs)[2], float* rb,
+                                           unsigned char* rec_g, int li, int g, int lane) {
+  constexpr int BS = 4;
+  slv_publish<NR, KB>(x, b, bs, rb);
+  __syncwarp();
+  if constexpr (KB + 1 < 32 / BS) {
+    constexpr int C1 = (KB + 1) * BS;   // the next panel
+    float NP[2][4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < BS; ++j) NP[r][j] = x[r][C1 + j];
+#pragma unroll
+    for (int s = 0; s < BS; ++s) {
+      float Rs[4];
+      ld_row<float, 4>(Rs, rb + s * SolveBlk<NR>::RS + C1);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        ffma2(NP[r][0], NP[r][1], P[r][s], Rs[0], Rs[1]);
+        ffma2(NP[r][2], NP[r][3], P[r][s], Rs[2], Rs[3]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) bs[r] = -1;
+#pragma unroll
+    for (int s = 0; s < BS; ++s) {
+      blk_panel_step<2, BS>(s, C1 + s, NP, kmask, pos, bs, rec_g, li, g, lane);
+      slv_trail<NR, C1 + BS>(x, b, P, s, rb);
+    }
+    __syncwarp();   // every lane has read rb before the next publish
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < BS; ++j) P[r][j] = NP[r][j];
+    slv_blocks<NR, KB + 1>(x, b, P, kmask, pos, bs, rb, rec_g, li, g, lane);
+  } else {
+#pragma unroll
+    for (int s = 0; s < BS; ++s) slv_trail<NR, 32>(x, b, P, s, rb);
+  }
+}
+
+template <int NR>
+// 3 CTAs per SM (168 registers) up to four right-hand sides; with eight the B registers
+// spill there, and 2 CTAs (255 registers, no spill) measure faster (tools/ab_solve.py)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, NR >= 8 ? 2 : 3)
+gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
+  using S = SolveBlk<NR>;
+  using Geo = BlkGeo<2>;
+  constexpr int R = 2, BS = 4, L = Geo::L, MT = Geo::M, NB = NR > 0 ? NR : 1;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  unsigned char* sbase = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stage0 = sbase + warp * S::NST * Geo::STAGE;
+  unsigned char* misc = sbase + kWarpsPerBlock * S::NST * Geo::STAGE + warp * S::BYTES;
+  float* rbuf = reinterpret_cast<float*>(misc);
+  unsigned char* rec = misc + S::RBUF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(misc + S::RBUF + S::REC);
+
+  const int g = lane / L;
+  const int li = lane % L;
+  const unsigned gmask = ((1u << L) - 1u) << (L * g);
+  float* rb = rbuf + g * BS * S::RS;
+  unsigned char* rec_g = rec + g * 32 * 8;
+
+  const int64_t ntasks = (a.batch + MT - 1) / MT;
+  const int64_t wstride = (int64_t)gridDim.x * kWarpsPerBlock;
+  const int64_t task0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+  const int m = a.m;
+
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0 && task0 < ntasks) {
+    mbar_expect_tx(&bars[0], Geo::STAGE);
+    tma_load_2d(stage0, &tm.a, 0, (int)(task0 * Geo::ROWS), &bars[0]);
+  }
+
+  int it = 0;
+  for (int64_t task = task0; task < ntasks; task += wstride, ++it) {
+    const int64_t item0 = task * MT;
+    const bool item_ok = item0 + g < a.batch;
+    unsigned char* stage = stage0 + (it & 1) * Geo::STAGE;
+    const int64_t nxt = task + wstride;
+    if (lane == 0 && nxt < ntasks) {
+      mbar_expect_tx(&bars[(it + 1) & 1], Geo::STAGE);
+      tma_load_2d(stage0 + ((it + 1) & 1) * Geo::STAGE, &tm.a, 0, (int)(nxt * Geo::ROWS), &bars[(it + 1) & 1]);
+      if constexpr (NR > 0) {
+        const int64_t i0 = nxt * MT, i1 = i0 + MT < a.batch ? i0 + MT : a.batch;
+        const uintptr_t lo = ((uintptr_t)(a.B + i0 * 32 * m) + 15) & ~(uintptr_t)15;
+        const uintptr_t hi = (uintptr_t)(a.B + i1 * 32 * m) & ~(uintptr_t)15;
+        if (hi > lo) bulk_prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
+      }
+    }
+    // the right-hand sides of this lane's rows (before the wait: the loads overlap it)
+    float b[R][NB];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = li + L * r;
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        b[r][j] = (NR > 0 && item_ok && j < m) ? __ldcs(a.B + ((item0 + g) * 32 + row) * m + j) : 0.0f;
+    }
+    mbar_wait_warp(&bars[it & 1], (it >> 1) & 1);
+    float x[R][32];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = li + L * r;
+      stage_ld_row<float, 32, true>(x[r], stage, g * 32 + row);
+      if (!item_ok) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[r][j] = (row == j) ? 1.0f : 0.0f;
+      }
+    }
+    __syncwarp();
+    float rowmax = 0.0f;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) rowmax = fmaxf(rowmax, fabsf(x[r][j]));
+    const double smax = (double)__uint_as_float(blk_gmax<R>(__float_as_uint(rowmax), g));
+    const float tau = round_down_to(a.tol * smax, 0.0f);
+
+    uint32_t kmask[R];
+    int pos[R], bs[R];
+    float P[R][BS];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      kmask[r] = 0x7fffffffu;
+      pos[r] = li + L * r;
+      bs[r] = -1;
+#pragma unroll
+      for (int j = 0; j < BS; ++j) P[r][j] = x[r][j];
+    }
+#pragma unroll
+    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS>(s, s, P, kmask, pos, bs, rec_g, li, g, lane);
+    slv_blocks<NR, 0>(x, b, P, kmask, pos, bs, rb, rec_g, li, g, lane);
+    __syncwarp();
+
+    // ---- a6: det / ipiv / singular flag from the per-step record (K1b's epilogue)
+    float myrp[R];
+    unsigned failb = 0;
+    int nswap = 0, nneg = 0;
+    double lgl = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = li + L * r;
+      float p_own, p_k;
+      int q_own, q_k;
+      rec_load(rec_g, pos[r], p_own, q_own);
+      rec_load(rec_g, row, p_k, q_k);
+      (void)q_own;
+      myrp[r] = rcp(p_own);
+      const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau) & gmask;
+      if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * L + r * L);
+      nswap += __popc(__ballot_sync(0xffffffffu, q_k != row) & gmask);
+      nneg += __popc(__ballot_sync(0xffffffffu, p_k < 0.0f) & gmask);
+      lgl += log_abs(p_k);
+      if (a.ipiv && item_ok) a.ipiv[(item0 + g) * 32 + row] = q_k + 1;
+    }
+    const int info = (int)failb;
+    const double lg = group_sum<L>(lgl);
+    const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
+    if (item_ok && li == 0) {
+      const int64_t item = item0 + g;
+      if (a.info) a.info[item] = info;
+      if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
+      if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
+      if (a.det) a.det[item] = info ? 0.0f : (float)(sgn * exp(lg));
+    }
+    // ---- a7 + a8: X[k][:] = (row pivoted at step k)[B part] / p_k
+    if constexpr (NR > 0) {
+      if (item_ok) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            if (j < m) __stcs(a.X + ((item0 + g) * 32 + pos[r]) * m + j, b[r][j] * myrp[r]);
+      }
+    }
+    __syncwarp();   // rec and rb are reused by the next task
+  }
+}
+
+template <int NR>
+cudaError_t launch_blk32s(const BlkSolveArgs& a, const TmaMaps& maps, cudaStream_t s) {
+  const size_t smem = SolveBlk<NR>::smem();
+  auto kern = gj_blk32s_kernel<NR>;
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured |= dbit;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntasks = (a.batch + 1) / 2;
+  const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int64_t cap = (int64_t)device_sm_count() * per_sm;
+  const int grid = (int)(need < cap ? need : cap);
+  kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(a, maps);
+  return cudaGetLastError();
+}
+
+// K1s applicability: fp32, n = 32, m <= 8, 16-byte aligned A, rows indexable by the TMA map
+bool blk32s_map(const void* A, int64_t batch, TmaMaps& maps) {
+  if (reinterpret_cast<uintptr_t>(A) % 16 != 0 || batch * 32 >= (int64_t(1) << 31)) return false;
+  if (!make_tma_map_2d(&maps.a, false, A, 32, (uint64_t)batch * 32, 128, 32, 64, 128)) return false;
+  maps.x = maps.a;
+  return true;
+}
+
+cudaError_t launch_blk32s_nr(const BlkSolveArgs& a, const TmaMaps& maps, cudaStream_t s) {
+  if (a.B == nullptr) return launch_blk32s<0>(a, maps, s);
+  if (a.m <= 1) return launch_blk32s<1>(a, maps, s);
+  if (a.m <= 2) return launch_blk32s<2>(a, maps, s);
+  if (a.m <= 4) return launch_blk32s<4>(a, maps, s);
+  return launch_blk32s<8>(a, maps, s);
+}
+
+// K7 instead of K1s for n = 32 fp32 solves (GJ_SOLVE_K7=1, A/B measurement and tests)
+bool solve_force_k7() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GJ_SOLVE_K7");
+    v = (e != nullptr && atoi(e) != 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // K1t on/off (GJ_K1_TC=1).
 bool k1_tc() {
   static int v = -1;
@@ -1027,6 +1353,15 @@ cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
         const cudaError_t e = launch_tc32(a, s);
         if (e != cudaErrorNotSupported) return e;
       }
+      // determinant-only run: K1s without right-hand sides (no D half)
+      if (full && a.Ainv == nullptr && k1_block_size() != 0) {
+        TmaMaps sm;
+        if (blk32s_map(a.A, a.batch, sm)) {
+          const BlkSolveArgs sa{a.batch, 0, nullptr, nullptr, a.ipiv, a.logabsdet, a.sign,
+                                static_cast<float*>(a.det), a.info, a.tol};
+          return launch_blk32s_nr(sa, sm, s);
+        }
+      }
       // K1b (blocked): box of 32 * R rows (R matrices per warp task)
       const int bsz = k1_block_size();
       const int R = k1_rows();
@@ -1064,6 +1399,15 @@ cudaError_t dispatch_np(const BatchedArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+cudaError_t launch_blk32_solve(const SolveArgs& a, cudaStream_t s) {
+  if (a.n != 32 || a.m < 1 || a.m > 8 || solve_force_k7()) return cudaErrorNotSupported;
+  TmaMaps maps;
+  if (!blk32s_map(a.A, a.batch, maps)) return cudaErrorNotSupported;
+  const BlkSolveArgs sa{a.batch, a.m, static_cast<const float*>(a.B), static_cast<float*>(a.X), a.ipiv,
+                        a.logabsdet, a.sign, nullptr, a.info, a.tol};
+  return launch_blk32s_nr(sa, maps, s);
+}
 
 cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s) {
   if (a.batch == 0) return cudaSuccess;

@@ -42,6 +42,9 @@ struct SolveArgs {
   double tol;
 };
 cudaError_t launch_solve_batched(gj_dtype dt, const SolveArgs& a, cudaStream_t s);
+// K1s (gj_batched.cu): fp32 n = 32, 1 <= m <= 8 on the blocked K1b elimination without the
+// D half; cudaErrorNotSupported when it does not apply (then K7 runs)
+cudaError_t launch_blk32_solve(const SolveArgs& a, cudaStream_t s);
 // Large-n solve, fp64, one matrix (gj_large.cu): [A | B] with the det-only trailing update.
 size_t large_solve_workspace_size(int n, int m);
 size_t large_solve_workspace_size_f32(int n, int m);

@@ -341,6 +341,10 @@ cudaError_t launch_solve_dt(const SolveArgs& a, cudaStream_t s) {
 
 cudaError_t launch_solve_batched(gj_dtype dt, const SolveArgs& a, cudaStream_t s) {
   if (a.n < 1 || a.n > 32 || a.m < 1 || a.m > 32) return cudaErrorInvalidValue;
+  if (dt == GJ_F32) {
+    const cudaError_t e = launch_blk32_solve(a, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   return dt == GJ_F32 ? launch_solve_dt<float>(a, s) : launch_solve_dt<double>(a, s);
 }
 

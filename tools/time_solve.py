@@ -31,3 +31,10 @@ for dt, n, m, B in ((torch.float32, 32, 1, 1 << 20), (torch.float32, 32, 8, 1 <<
     es = A.element_size()
     gbs = B * (n * n + 2 * n * m) * es / (ms / 1e3) / 1e9
     print(f"{dt} n={n} nrhs={m} B={B}: {ms:.3f} ms  {B / ms * 1e3:.3e} systems/s  {gbs:.0f} GB/s")
+
+# determinant-only run (gj_det on the batched path: K1s without right-hand sides for fp32 n = 32)
+for dt, n, B in ((torch.float32, 32, 1 << 20), (torch.float64, 32, 1 << 18)):
+    A = torch.randn(B, n, n, dtype=dt, device="cuda")
+    ms_det = t(lambda: gj.det(A))
+    ms_inv = t(lambda: gj.invert_batched(A))
+    print(f"{dt} n={n} B={B}: det-only {ms_det:.3f} ms ({B / ms_det * 1e3:.3e} matrices/s), inverse {ms_inv:.3f} ms")
