@@ -287,13 +287,37 @@ def f4_measure(A, stream, nrhs: int = 1, reps: int = 3):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     ms = float(np.median(ts))
+    # the determinant-only run on the same batch (gj_det: K1s without right-hand sides)
+    lg = torch.empty(Bn, dtype=torch.float64, device=A.device)
+    sg = torch.empty(Bn, dtype=torch.int8, device=A.device)
+
+    def run_det():
+        st = gj.lib.gj_det(0, N, Bn, A.data_ptr(), lg.data_ptr(), sg.data_ptr(), None, None, None,
+                           N * 2.0 ** -23, None, 0, stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    run_det()
+    torch.cuda.synchronize()
+    td = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run_det()
+        b.record(stream)
+        torch.cuda.synchronize()
+        td.append(a.elapsed_time(b))
+    ms_det = float(np.median(td))
     peak, src = measured_peaks()
     gbs = Bn * (N * N + 2 * N * nrhs + N) * 4 / (ms / 1e3) / 1e9
     return {"workload": f"f4: C2 batch (1,048,576 x 32 x 32 fp32) solved for {nrhs} right-hand side(s) (SURVEY §8f f4)",
             "metric": "systems/s", "value": Bn / (ms / 1e3), "unit": "systems/s", "ms": ms, "reps": reps,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                         "peak_source": src, "kernel": f"gj_solve_kernel<float,32,{1 if nrhs == 1 else nrhs}> (K7)",
-                         "note": "unblocked (one row per lane, pivot row through shared memory every step)"}}
+                         "peak_source": src, "kernel": f"gj_blk32s_kernel<{nrhs}> (K1s)",
+                         "note": "K1b's blocked elimination without the D half; pivot-chain bound like K1b"},
+            "det_only": {"api": "gj_det (K1s without right-hand sides)", "ms": ms_det,
+                         "value": Bn / (ms_det / 1e3), "unit": "matrices/s",
+                         "hbm_frac": Bn * (N * N * 4 + 9) / (ms_det / 1e3) / 1e9 / peak}}
 
 
 def cpu_baseline(sample: int, A_host=None):
