@@ -4,7 +4,9 @@ size (exact pins, library cross-checks of det / pivots, residual rows).
 
 * C2 (configs[1]): the whole 1,048,576-item fp32 batch in one gj_invert_batched call
   (the bench's K1b kernel), oracle on a sample spread over the batch incl. its ragged end.
-* C3 (configs[2]): the whole 262,144-item fp64 batch (K2b), every singular flag against the
+* C2 and C3 also EVERY item against the oracle (chunked; SURVEY §8d's oracle plan: "every
+  report run, all items").
+* C3 (configs[2]): the whole 262,144-item fp64 batch (K2d), every singular flag against the
   generator's list (R7), oracle on a sample incl. singular items.
 * C5 (configs[4]) at 32768: the P6 Sylvester–Hadamard pin (exact inverse A^T / n, every
   pivot step an exact tie) through the single-GPU path and through the distributed driver
@@ -59,6 +61,27 @@ def test_c2_full_sampled(gj, torch):
     assert_report(rep)
 
 
+def test_c2_every_item(gj, torch):
+    """The whole C2 batch in the bench's launch configuration (one gj_invert_batched call
+    over 1,048,576 items, K1b), and EVERY item compared with the oracle (chunks of 65,536
+    items; the oracle runs ~6.6e4 items/s on the host cores): R1 inverse (kappa rule), R3
+    ipiv (near-tie rule), R4 sign, R5 log|det|, R7 singular flag."""
+    A = synth.gen_c2()
+    tol = 32 * 2.0 ** -23
+    r = gj.invert_batched(torch.from_numpy(A).cuda(), tol=tol)
+    torch.cuda.synchronize()
+    gall = {k: v.cpu().numpy() for k, v in r._asdict().items() if v is not None}
+    worst = 0.0
+    ch = 65536
+    for c0 in range(0, A.shape[0], ch):
+        sl = slice(c0, c0 + ch)
+        ref = oracle.invert_batched(A[sl], tol=tol)
+        rep = compare(A[sl], {k: v[sl] for k, v in gall.items()}, ref, np.float32, tol)
+        assert_report(rep)
+        worst = max(worst, rep.max_inv_err_over_keps)
+    print(f"C2 every item: max e/(kappa eps) = {worst:.4f}")
+
+
 def test_c3_full_sampled(gj, torch):
     A, S = synth.gen_c3(return_singular=True)            # 262,144 x 64 x 64 fp64, seed 2
     At = torch.from_numpy(A).cuda()
@@ -73,6 +96,26 @@ def test_c3_full_sampled(gj, torch):
     rep = compare(As, g, ref, np.float64, synth.C3_TOL, flat_only=True)
     print(rep.summary())
     assert_report(rep, flat_only=True)
+
+
+def test_c3_every_item(gj, torch):
+    """The whole C3 batch (262,144 fp64 64 x 64, 1% singular) in one call (K2d), EVERY item
+    against the oracle with the flat fp64 bounds (C3 is well-conditioned under
+    reading G15) and every singular flag exact."""
+    A, S = synth.gen_c3(return_singular=True)
+    r = gj.invert_batched(torch.from_numpy(A).cuda(), tol=synth.C3_TOL)
+    torch.cuda.synchronize()
+    gall = {k: v.cpu().numpy() for k, v in r._asdict().items() if v is not None}
+    assert np.array_equal(np.nonzero(gall["info"])[0], S)
+    worst = 0.0
+    ch = 16384
+    for c0 in range(0, A.shape[0], ch):
+        sl = slice(c0, c0 + ch)
+        ref = oracle.invert_batched(A[sl], tol=synth.C3_TOL)
+        rep = compare(A[sl], {k: v[sl] for k, v in gall.items()}, ref, np.float64, synth.C3_TOL, flat_only=True)
+        assert_report(rep, flat_only=True)
+        worst = max(worst, rep.max_inv_err)
+    print(f"C3 every item: max relative inverse error {worst:.3e}")
 
 
 def _hadamard_device(torch, n, seed=5):
