@@ -329,6 +329,163 @@ __global__ void __launch_bounds__(kWarpsD * 32, GJ_K2D_MINB) gj_batched64d_kerne
   }
 }
 
+
+// ------------------------------------------------------------------ K2e: one warp per matrix
+// The same blocked elimination with the matrix resident in SHARED MEMORY (row stride 66
+// doubles: a DMMA accumulator-fragment access of 8 rows x 4 lanes then spreads over all
+// banks, 4 wavefronts per 512 B) and one warp doing everything for its matrix: the 8-step
+// panel (d_panel_steps, K2d's chain), then per 8-column tile the block's B fragments (the
+// pivot rows, read before the tile is written, so no copy of R is needed) and the 8 m-tiles'
+// C fragments through DMMA.  Why: K2d's single panel warp per CTA holds the whole CTA at the
+// per-step chain while the matrix occupies 4 warps' registers (4 CTAs per SM); here a
+// matrix costs 35 KB of shared memory and 32 threads, so six panels run per SM.
+constexpr int MS = N64 + 2;   // shared row stride (doubles)
+struct SmemE {
+  static constexpr int M = 0;                              // [64][MS] the working array
+  static constexpr int REC = M + N64 * MS * 8;             // [64] (p, q)
+  static constexpr int ROW = REC + N64 * 16;               // [64] row pivoted at step k
+  static constexpr int POS = ROW + N64 * 4;                // [64] final position of row i
+  static constexpr int BYTES = POS + N64 * 4;
+};
+
+__global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_e[];
+  double* M = reinterpret_cast<double*>(smem_e + SmemE::M);
+  unsigned char* rec = smem_e + SmemE::REC;
+  int* rowk = reinterpret_cast<int*>(smem_e + SmemE::ROW);
+  int* posm = reinterpret_cast<int*>(smem_e + SmemE::POS);
+  const int lane = threadIdx.x;
+  const int g = lane >> 2, t = lane & 3;
+  const double* __restrict__ Ag = static_cast<const double*>(a.A);
+  double* __restrict__ Xg = static_cast<double*>(a.Ainv);
+
+  for (int64_t item = blockIdx.x; item < a.batch; item += gridDim.x) {
+    const double* Ai = Ag + item * (N64 * N64);
+    if (item + gridDim.x < a.batch) {
+      if (lane == 0) bulk_prefetch_l2(Ag + (item + gridDim.x) * (N64 * N64), N64 * N64 * 8);
+    }
+    // ---- a1: rows -> shared memory (one 512-byte row per instruction), max |a_ij|
+    double rm = 0.0;
+#pragma unroll 4
+    for (int i0 = 0; i0 < N64; i0 += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Ai + (i0 + u) * N64) + lane);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        *reinterpret_cast<double2*>(M + (i0 + u) * MS + 2 * lane) = v[u];
+        rm = fmax(rm, fmax(fabs(v[u].x), fabs(v[u].y)));
+      }
+    }
+    double tau;
+    {
+      const unsigned long long rb = (unsigned long long)__double_as_longlong(rm);
+      const uint32_t mh = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32));
+      const uint32_t ml = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32) == mh ? (uint32_t)rb : 0u);
+      tau = a.tol * __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+    }
+    __syncwarp();
+    uint32_t kmask[2] = {0xffffffffu, 0xffffffffu};
+    int pos[2] = {lane, lane + 32};
+
+#pragma unroll 1
+    for (int kb = 0; kb < N64 / BSD; ++kb) {
+      // ---- the panel: rows lane, lane + 32 of column tile kb
+      double x[2][BSD];
+      int bs[2] = {-1, -1};
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < BSD; j += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(M + (lane + 32 * r) * MS + 8 * kb + j);
+          x[r][j] = v.x;
+          x[r][j + 1] = v.y;
+        }
+      d_panel_steps<0>(kb * BSD, x, kmask, pos, bs, rec, rowk, lane);
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < BSD; j += 2)
+          *reinterpret_cast<double2*>(M + (lane + 32 * r) * MS + 8 * kb + j) = make_double2(x[r][j], x[r][j + 1]);
+      __syncwarp();
+      // ---- X[:, ~panel] += (W - S) R, tile by tile on the FP64 tensor pipe
+      double af[8][2];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        af[mt][0] = M[(8 * mt + g) * MS + 8 * kb + t];       // A[g][t]
+        af[mt][1] = M[(8 * mt + g) * MS + 8 * kb + 4 + t];   // A[g][4 + t]
+      }
+      const int rk0 = rowk[kb * BSD + t], rk1 = rowk[kb * BSD + 4 + t];
+#pragma unroll 1
+      for (int nt = 0; nt < 8; ++nt) {
+        if (nt == kb) continue;
+        const double b0 = M[rk0 * MS + 8 * nt + g];   // B[t][g]: pivot row of step t, block start
+        const double b1 = M[rk1 * MS + 8 * nt + g];
+        __syncwarp();                                  // every lane has its B before the tile is written
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          double2* cp = reinterpret_cast<double2*>(M + (8 * mt + g) * MS + 8 * nt + 2 * t);
+          double2 c = *cp;
+          dmma884(c.x, c.y, af[mt][0], b0);
+          dmma884(c.x, c.y, af[mt][1], b1);
+          *cp = c;
+        }
+      }
+      __syncwarp();
+    }
+
+    // ---- a6: det / ipiv / singular flag from the record (steps lane, lane + 32)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) posm[lane + 32 * r] = pos[r];
+    {
+      unsigned fb0 = 0, fb1 = 0;
+      int nswap = 0, nneg = 0;
+      double lg = 0.0;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int k = lane + 32 * r;
+        double pk;
+        int qk;
+        rec_load(rec, k, pk, qk);
+        const unsigned fb = __ballot_sync(0xffffffffu, fabs(pk) <= tau);
+        if (r == 0) fb0 = fb; else fb1 = fb;
+        nswap += __popc(__ballot_sync(0xffffffffu, qk != k));
+        nneg += __popc(__ballot_sync(0xffffffffu, pk < 0.0));
+        lg += log(fabs(pk));
+        if (a.ipiv) a.ipiv[item * N64 + k] = qk + 1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+      const int info = fb0 ? __ffs(fb0) : (fb1 ? 32 + __ffs(fb1) : 0);
+      const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
+      if (lane == 0) {
+        if (a.info) a.info[item] = info;
+        if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
+        if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
+        if (a.det) static_cast<double*>(a.det)[item] = info ? 0.0 : (double)(sgn * exp(lg));
+      }
+    }
+    __syncwarp();
+    // ---- a7 + a8: Ainv[pos(i)][row(k)] = X[i][k] / p_pos(i) (+ 1 / p on the own entry)
+    if (Xg != nullptr) {
+      double* Xi = Xg + item * (N64 * N64);
+      const int oc0 = rowk[lane], oc1 = rowk[lane + 32];
+#pragma unroll 4
+      for (int i = 0; i < N64; ++i) {
+        const int ps = posm[i];
+        double pown;
+        int qd;
+        rec_load(rec, ps, pown, qd);
+        const double rp = 1.0 / pown;
+        double* orow = Xi + (int64_t)ps * N64;
+        __stcs(orow + oc0, M[i * MS + lane] * rp + (lane == ps ? rp : 0.0));
+        __stcs(orow + oc1, M[i * MS + lane + 32] * rp + (lane + 32 == ps ? rp : 0.0));
+      }
+    }
+    __syncwarp();   // shared state is rewritten by the next matrix
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_batched64d(const BatchedArgs& a, cudaStream_t s) {
@@ -350,6 +507,26 @@ cudaError_t launch_batched64d(const BatchedArgs& a, cudaStream_t s) {
   const int64_t cap = (int64_t)device_sm_count() * per_sm;
   const int grid = (int)(a.batch < cap ? a.batch : cap);
   gj_batched64d_kernel<<<grid, kWarpsD * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
+  if (a.n != N64 || a.batch <= 0) return cudaErrorInvalidValue;
+  const int smem = SmemE::BYTES;
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
+    cudaError_t e = cudaFuncSetAttribute(gj_batched64e_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured |= dbit;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_batched64e_kernel, 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = (int64_t)device_sm_count() * per_sm;
+  const int grid = (int)(a.batch < cap ? a.batch : cap);
+  gj_batched64e_kernel<<<grid, 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 

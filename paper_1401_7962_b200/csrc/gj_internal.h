@@ -28,6 +28,7 @@ cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 cudaError_t launch_batched64b(const BatchedArgs& a, cudaStream_t s);
 // K2d, fp64 n = 64 with the DMMA blocked update (gj_batched64d.cu).
 cudaError_t launch_batched64d(const BatchedArgs& a, cudaStream_t s);
+cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s);   // K2e (one warp per matrix, shared-memory resident)
 // K7, multi-RHS solve X = A^-1 B, n <= 32, m <= 32 (gj_solve.cu).
 struct SolveArgs {
   int n, m;             // order, right-hand sides
