@@ -86,9 +86,13 @@ __device__ unsigned long long g_k2d_prof[8];
 #endif
 
 // Warp 0's pivot step S (static) at global step k on the panel rows lane and lane + 32.
-template <int S>
+// SROW (K2e): |p| is the winning key itself, so 1/|p| starts before the winner is known,
+// and the pivot row travels through shared memory (one writer, broadcast reads, buffered by
+// step parity) instead of sixteen shuffles.
+template <int S, bool SROW = false>
 __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
-                                             int (&bs)[2], unsigned char* rec, int* rowk, int lane) {
+                                             int (&bs)[2], unsigned char* rec, int* rowk, int lane,
+                                             double* prow = nullptr) {
 #ifdef GJ_K2D_PROF
   long long t_prev = 0;
 #endif
@@ -106,6 +110,8 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
   for (int r = 0; r < 2; ++r)
     if (hi[r] == mh) lm = max(lm, lo[r]);
   const uint32_t ml = __reduce_max_sync(0xffffffffu, lm);
+  double rap = 0.0;
+  if constexpr (SROW) rap = rcp64d(__longlong_as_double((long long)(((unsigned long long)mh << 32) | ml)));
   uint32_t c = 0xffffffu;
 #pragma unroll
   for (int r = 0; r < 2; ++r)
@@ -116,11 +122,32 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
   const int slot = (int)(win & 1u);
   K2D_T(1);
   double z[BSD];
+  if constexpr (SROW) {
+    double* pr = prow + (S & 1) * BSD;
+    if (lane == src) {
 #pragma unroll
-  for (int j = 0; j < BSD; ++j) z[j] = shfl_dd(slot ? x[1][j] : x[0][j], src);
+      for (int j = 0; j < BSD; j += 2)
+        *reinterpret_cast<double2*>(pr + j) = slot ? make_double2(x[1][j], x[1][j + 1]) : make_double2(x[0][j], x[0][j + 1]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < BSD; j += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(pr + j);
+      z[j] = v.x;
+      z[j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < BSD; ++j) z[j] = shfl_dd(slot ? x[1][j] : x[0][j], src);
+  }
   const double p = z[S];
   K2D_T(2);
-  const double rp = rcp64d(p);
+  double rp;
+  if constexpr (SROW) {
+    rp = p < 0.0 ? -rap : rap;   // rcp64d is odd: bit-identical to rcp64d(p)
+  } else {
+    rp = rcp64d(p);
+  }
   K2D_T(3);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -142,12 +169,13 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
   }
   K2D_T(5);
 }
-template <int S>
+template <int S, bool SROW = false>
 __device__ __forceinline__ void d_panel_steps(const int kb, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
-                                              int (&bs)[2], unsigned char* rec, int* rowk, int lane) {
+                                              int (&bs)[2], unsigned char* rec, int* rowk, int lane,
+                                              double* prow = nullptr) {
   if constexpr (S < BSD) {
-    d_panel_step<S>(kb + S, x, kmask, pos, bs, rec, rowk, lane);
-    d_panel_steps<S + 1>(kb, x, kmask, pos, bs, rec, rowk, lane);
+    d_panel_step<S, SROW>(kb + S, x, kmask, pos, bs, rec, rowk, lane, prow);
+    d_panel_steps<S + 1, SROW>(kb, x, kmask, pos, bs, rec, rowk, lane, prow);
   }
 }
 
@@ -345,8 +373,17 @@ struct SmemE {
   static constexpr int REC = M + N64 * MS * 8;             // [64] (p, q)
   static constexpr int ROW = REC + N64 * 16;               // [64] row pivoted at step k
   static constexpr int POS = ROW + N64 * 4;                // [64] final position of row i
-  static constexpr int BYTES = POS + N64 * 4;
+  static constexpr int RP = POS + N64 * 4;                 // [64] 1 / p of step k
+  static constexpr int PROW = RP + N64 * 8;                // [2][8] pivot-row broadcast
+  static constexpr int BYTES = PROW + 2 * BSD * 8;
 };
+#ifndef GJ_K2E_SROW
+#define GJ_K2E_SROW 1              // pivot row through shared memory + early 1/|p| (A/B option)
+#endif
+#ifndef GJ_K2E_NTU
+#define GJ_K2E_NTU 2               // tile-loop unroll (measured: 1 13.5, 2 13.1, 4 13.2, 8 13.6 ms)
+#endif
+constexpr int kK2eNtu = GJ_K2E_NTU;
 
 __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_e[];
@@ -354,6 +391,8 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
   unsigned char* rec = smem_e + SmemE::REC;
   int* rowk = reinterpret_cast<int*>(smem_e + SmemE::ROW);
   int* posm = reinterpret_cast<int*>(smem_e + SmemE::POS);
+  double* rpm = reinterpret_cast<double*>(smem_e + SmemE::RP);
+  double* prow = reinterpret_cast<double*>(smem_e + SmemE::PROW);
   const int lane = threadIdx.x;
   const int g = lane >> 2, t = lane & 3;
   const double* __restrict__ Ag = static_cast<const double*>(a.A);
@@ -401,7 +440,7 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
           x[r][j] = v.x;
           x[r][j + 1] = v.y;
         }
-      d_panel_steps<0>(kb * BSD, x, kmask, pos, bs, rec, rowk, lane);
+      d_panel_steps<0, GJ_K2E_SROW != 0>(kb * BSD, x, kmask, pos, bs, rec, rowk, lane, prow);
 #pragma unroll
       for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -416,7 +455,7 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
         af[mt][1] = M[(8 * mt + g) * MS + 8 * kb + 4 + t];   // A[g][4 + t]
       }
       const int rk0 = rowk[kb * BSD + t], rk1 = rowk[kb * BSD + 4 + t];
-#pragma unroll 1
+#pragma unroll kK2eNtu
       for (int nt = 0; nt < 8; ++nt) {
         if (nt == kb) continue;
         const double b0 = M[rk0 * MS + 8 * nt + g];   // B[t][g]: pivot row of step t, block start
@@ -436,7 +475,13 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
 
     // ---- a6: det / ipiv / singular flag from the record (steps lane, lane + 32)
 #pragma unroll
-    for (int r = 0; r < 2; ++r) posm[lane + 32 * r] = pos[r];
+    for (int r = 0; r < 2; ++r) {
+      posm[lane + 32 * r] = pos[r];
+      double pk;
+      int qk;
+      rec_load(rec, lane + 32 * r, pk, qk);
+      rpm[lane + 32 * r] = 1.0 / pk;
+    }
     {
       unsigned fb0 = 0, fb1 = 0;
       int nswap = 0, nneg = 0;
@@ -473,10 +518,7 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
 #pragma unroll 4
       for (int i = 0; i < N64; ++i) {
         const int ps = posm[i];
-        double pown;
-        int qd;
-        rec_load(rec, ps, pown, qd);
-        const double rp = 1.0 / pown;
+        const double rp = rpm[ps];
         double* orow = Xi + (int64_t)ps * N64;
         __stcs(orow + oc0, M[i * MS + lane] * rp + (lane == ps ? rp : 0.0));
         __stcs(orow + oc1, M[i * MS + lane + 32] * rp + (lane + 32 == ps ? rp : 0.0));

@@ -8,4 +8,5 @@ for f in $(ls *.cu | sed "s/\.cu$//"); do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -I ../../include -c $f.cu -o $out/$f.o &
 done
 wait
+for f in $(ls *.cu | sed "s/\.cu$//"); do test -f $out/$f.o || { echo "ab_build: $f.cu failed to compile" >&2; exit 1; }; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $out/libgjinv.so $out/*.o -lcuda
