@@ -367,7 +367,24 @@ __global__ void __launch_bounds__(kWarpsD * 32, GJ_K2D_MINB) gj_batched64d_kerne
 // C fragments through DMMA.  Why: K2d's single panel warp per CTA holds the whole CTA at the
 // per-step chain while the matrix occupies 4 warps' registers (4 CTAs per SM); here a
 // matrix costs 35 KB of shared memory and 32 threads, so six panels run per SM.
-constexpr int MS = N64 + 2;   // shared row stride (doubles)
+#ifndef GJ_K2E_SWZ
+#define GJ_K2E_SWZ 1
+#endif
+// Element (row, col) of the shared working array.  SWZ (default): row stride 64 doubles and
+// the 16-byte chunk index XOR f(row), f = ((row & 1) << 2) | ((row >> 1) & 3): a bijection
+// on 8 consecutive rows (a column access of 8 rows per LDS.128 phase hits 8 distinct
+// chunks) with f(2p) ^ f(2p + 1) = 4 (the two rows of an accumulator-fragment phase use the
+// two halves of the 128-byte line), so both access patterns run at 4 wavefronts per 512 B.
+// Otherwise: padded stride 66 (8 wavefronts for the fragment pattern).
+constexpr int MS = GJ_K2E_SWZ ? N64 : N64 + 2;
+__device__ __forceinline__ int mix(int row, int col) {
+  if constexpr (GJ_K2E_SWZ) {
+    const int f = ((row & 1) << 2) | ((row >> 1) & 3);
+    return row * N64 + ((((col >> 1) ^ f)) << 1) + (col & 1);
+  } else {
+    return row * MS + col;
+  }
+}
 struct SmemE {
   static constexpr int M = 0;                              // [64][MS] the working array
   static constexpr int REC = M + N64 * MS * 8;             // [64] (p, q)
@@ -412,7 +429,7 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
       for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Ai + (i0 + u) * N64) + lane);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        *reinterpret_cast<double2*>(M + (i0 + u) * MS + 2 * lane) = v[u];
+        *reinterpret_cast<double2*>(M + mix(i0 + u, 2 * lane)) = v[u];
         rm = fmax(rm, fmax(fabs(v[u].x), fabs(v[u].y)));
       }
     }
@@ -436,7 +453,7 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
       for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int j = 0; j < BSD; j += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(M + (lane + 32 * r) * MS + 8 * kb + j);
+          const double2 v = *reinterpret_cast<const double2*>(M + mix(lane + 32 * r, 8 * kb + j));
           x[r][j] = v.x;
           x[r][j + 1] = v.y;
         }
@@ -445,25 +462,25 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
       for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int j = 0; j < BSD; j += 2)
-          *reinterpret_cast<double2*>(M + (lane + 32 * r) * MS + 8 * kb + j) = make_double2(x[r][j], x[r][j + 1]);
+          *reinterpret_cast<double2*>(M + mix(lane + 32 * r, 8 * kb + j)) = make_double2(x[r][j], x[r][j + 1]);
       __syncwarp();
       // ---- X[:, ~panel] += (W - S) R, tile by tile on the FP64 tensor pipe
       double af[8][2];
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
-        af[mt][0] = M[(8 * mt + g) * MS + 8 * kb + t];       // A[g][t]
-        af[mt][1] = M[(8 * mt + g) * MS + 8 * kb + 4 + t];   // A[g][4 + t]
+        af[mt][0] = M[mix(8 * mt + g, 8 * kb + t)];       // A[g][t]
+        af[mt][1] = M[mix(8 * mt + g, 8 * kb + 4 + t)];   // A[g][4 + t]
       }
       const int rk0 = rowk[kb * BSD + t], rk1 = rowk[kb * BSD + 4 + t];
 #pragma unroll kK2eNtu
       for (int nt = 0; nt < 8; ++nt) {
         if (nt == kb) continue;
-        const double b0 = M[rk0 * MS + 8 * nt + g];   // B[t][g]: pivot row of step t, block start
-        const double b1 = M[rk1 * MS + 8 * nt + g];
+        const double b0 = M[mix(rk0, 8 * nt + g)];   // B[t][g]: pivot row of step t, block start
+        const double b1 = M[mix(rk1, 8 * nt + g)];
         __syncwarp();                                  // every lane has its B before the tile is written
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
-          double2* cp = reinterpret_cast<double2*>(M + (8 * mt + g) * MS + 8 * nt + 2 * t);
+          double2* cp = reinterpret_cast<double2*>(M + mix(8 * mt + g, 8 * nt + 2 * t));
           double2 c = *cp;
           dmma884(c.x, c.y, af[mt][0], b0);
           dmma884(c.x, c.y, af[mt][1], b1);
@@ -520,8 +537,8 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
         const int ps = posm[i];
         const double rp = rpm[ps];
         double* orow = Xi + (int64_t)ps * N64;
-        __stcs(orow + oc0, M[i * MS + lane] * rp + (lane == ps ? rp : 0.0));
-        __stcs(orow + oc1, M[i * MS + lane + 32] * rp + (lane + 32 == ps ? rp : 0.0));
+        __stcs(orow + oc0, M[mix(i, lane)] * rp + (lane == ps ? rp : 0.0));
+        __stcs(orow + oc1, M[mix(i, lane + 32)] * rp + (lane + 32 == ps ? rp : 0.0));
       }
     }
     __syncwarp();   // shared state is rewritten by the next matrix
