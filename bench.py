@@ -494,7 +494,7 @@ def run_c3(args, rank, world, local):
                        "n": n, "parallelism": f"dp{world} (independent shards, no collective)",
                        "l2": "inputs (8 GiB/GPU) larger than L2 (126 MB); no flush needed"},
             "roofline": {"bound": "fp64", "achieved": tf, "peak": dfma_peak, "unit": "TFLOP/s",
-                         "frac": tf / dfma_peak, "traffic": None, "kernel": "gj_batched64d_kernel (K2d: DMMA blocked update)",
+                         "frac": tf / dfma_peak, "traffic": None, "kernel": "gj_batched64e_kernel (K2e: one warp per matrix, shared-memory resident, DMMA blocked update)",
                          "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md unit counts)",
                          "hbm_achieved_gbs": byts / (ms / 1e3) / 1e9, "hbm_peak_gbs": hbm},
             "singular_items": int((info != 0).sum().item()), "gpu_launches": args.steps, "clocks": clk.summary()}),
