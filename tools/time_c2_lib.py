@@ -33,3 +33,8 @@ for path in sys.argv[1:]:
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     print(f"{path}: median {np.median(ts):.3f} ms  min {min(ts):.3f} ms", flush=True)
+    if path == sys.argv[1]:
+        ref = (X.clone(), lg.clone(), sg.clone())
+    else:
+        same = torch.equal(ref[0].view(torch.int32), X.view(torch.int32)) and torch.equal(ref[1], lg) and torch.equal(ref[2], sg)
+        print(f"  bitwise equal to {sys.argv[1]}: {same}", flush=True)
