@@ -418,6 +418,9 @@ struct SmemE {
 #define GJ_K2E_NTU 2               // tile-loop unroll (measured: 1 13.5, 2 13.1, 4 13.2, 8 13.6 ms)
 #endif
 constexpr int kK2eNtu = GJ_K2E_NTU;
+#ifndef GJ_K2E_OVERLAP
+#define GJ_K2E_OVERLAP 1           // load the next matrix under this one's store
+#endif
 
 __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_e[];
@@ -432,15 +435,17 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
   const double* __restrict__ Ag = static_cast<const double*>(a.A);
   double* __restrict__ Xg = static_cast<double*>(a.Ainv);
 
+  bool loaded = false;   // this item's rows already in shared memory (loaded under the previous store)
+  double rm_next = 0.0;
   for (int64_t item = blockIdx.x; item < a.batch; item += gridDim.x) {
     const double* Ai = Ag + item * (N64 * N64);
     if (item + gridDim.x < a.batch) {
       if (lane == 0) bulk_prefetch_l2(Ag + (item + gridDim.x) * (N64 * N64), N64 * N64 * 8);
     }
     // ---- a1: rows -> shared memory (one 512-byte row per instruction), max |a_ij|
-    double rm = 0.0;
+    double rm = rm_next;
 #pragma unroll 4
-    for (int i0 = 0; i0 < N64; i0 += 8) {
+    for (int i0 = 0; i0 < (loaded ? 0 : N64); i0 += 8) {
       double2 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Ai + (i0 + u) * N64) + lane);
@@ -560,9 +565,44 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
     }
     __syncwarp();
     // ---- a7 + a8: Ainv[pos(i)][row(k)] = X[i][k] / p_pos(i) (+ 1 / p on the own entry)
+    loaded = false;
+    rm_next = 0.0;
     if (Xg != nullptr) {
       double* Xi = Xg + item * (N64 * N64);
       const int oc0 = rowk[lane], oc1 = rowk[lane + 32];
+#if GJ_K2E_OVERLAP
+      // the next matrix's rows stream in under this one's store: rows i0..i0+7 are loaded
+      // while they are read out, and written once every lane has read them
+      const int64_t nitem = item + gridDim.x;
+      const bool pre = nitem < a.batch;
+      const double* An = Ag + nitem * (N64 * N64);
+#pragma unroll 1
+      for (int i0 = 0; i0 < N64; i0 += 8) {
+        double2 v[8];
+        if (pre) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(An + (i0 + u) * N64) + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u;
+          const int ps = posm[i];
+          const double rp = rpm[ps];
+          double* orow = Xi + (int64_t)ps * N64;
+          __stcs(orow + oc0, M[mix(i, lane)] * rp + (lane == ps ? rp : 0.0));
+          __stcs(orow + oc1, M[mix(i, lane + 32)] * rp + (lane + 32 == ps ? rp : 0.0));
+        }
+        __syncwarp();
+        if (pre) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            *reinterpret_cast<double2*>(M + mix(i0 + u, 2 * lane)) = v[u];
+            rm_next = fmax(rm_next, fmax(fabs(v[u].x), fabs(v[u].y)));
+          }
+        }
+      }
+      loaded = pre;
+#else
 #pragma unroll 4
       for (int i = 0; i < N64; ++i) {
         const int ps = posm[i];
@@ -571,6 +611,7 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
         __stcs(orow + oc0, M[mix(i, lane)] * rp + (lane == ps ? rp : 0.0));
         __stcs(orow + oc1, M[mix(i, lane + 32)] * rp + (lane + 32 == ps ? rp : 0.0));
       }
+#endif
     }
     __syncwarp();   // shared state is rewritten by the next matrix
   }
