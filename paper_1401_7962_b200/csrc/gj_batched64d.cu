@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
       const int rk0 = rowk[kb * BSD + t], rk1 = rowk[kb * BSD + 4 + t];
 #pragma unroll kK2eNtu
       for (int nt = 0; nt < 8; ++nt) {
-        if (nt == kb) continue;
+        // determinant-only run: the compact D columns left of the panel are never read again
+        if (nt == kb || (Xg == nullptr && nt < kb)) continue;
         const double b0 = M[mix(rk0, 8 * nt + g)];   // B[t][g]: pivot row of step t, block start
         const double b1 = M[mix(rk1, 8 * nt + g)];
         __syncwarp();                                  // every lane has its B before the tile is written

@@ -200,8 +200,12 @@ def test_zero_pivot_not_singular(gj, torch):
 
 
 # ------------------------------------------------------------------ other entry points
-def test_det_entry_matches_invert(gj, torch):
-    A = synth.gen_normal_batch(700, 20, seed=9, dtype=np.float64)
+@pytest.mark.parametrize("n,dtype", [(20, np.float64), (64, np.float64), (32, np.float32), (48, np.float32)])
+def test_det_entry_matches_invert(gj, torch, n, dtype):
+    """gj_det (Ainv = NULL) — the det-only kernels (K1s for fp32 n = 32, K2e skipping the
+    compact D columns for fp64 n = 64) give bitwise the inverting path's pivots and dets."""
+    A = synth.gen_normal_batch(700, n, seed=9, dtype=dtype)
+    A[5, 3] = A[5, 1]   # a singular item
     At = torch.from_numpy(A).cuda()
     r1 = gj.invert_batched(At)
     r2 = gj.det(At)
