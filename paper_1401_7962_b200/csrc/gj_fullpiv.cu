@@ -108,6 +108,13 @@ __device__ __forceinline__ void ld_masks(uint32_t (&m)[NP], const uint32_t* src)
   }
 }
 
+// the key every NaN maps to (one above +inf's)
+template <typename K>
+__device__ __forceinline__ K knan() {
+  if constexpr (sizeof(K) == 4) return 0x7f800001u;
+  else return 0x7ff0000000000001ull;
+}
+
 // |x| key with a per-column mask m (all ones: column un-pivoted; 0: pivoted or padding)
 __device__ __forceinline__ uint32_t mkey(float v, uint32_t m) { return __float_as_uint(v) & m & 0x7fffffffu; }
 __device__ __forceinline__ unsigned long long mkey(double v, uint32_t m) {
@@ -238,6 +245,10 @@ __global__ void __launch_bounds__(kFullWarps * 32, full_min_blocks<T, NP>()) gj_
           const K kj = mkey(x[j], cm[j]);
           km = kj > km ? kj : km;
         }
+        // a singular item turns its rows into NaN after a zero pivot (1/0 * 0); all NaN keys
+        // are mapped to one value just above +inf, so the candidate searches below always
+        // find a row and a column (the item is flagged; its inverse is unspecified)
+        km = km > knan<K>() ? knan<K>() : km;
         const K m = gmax_key<L>(rdone ? K(0) : km);
         // smallest physical row position among the rows attaining m
         const uint32_t rc = (!rdone && km == m) ? ((uint32_t)pos << 8 | (uint32_t)li) : 0xffffffu;
@@ -249,7 +260,9 @@ __global__ void __launch_bounds__(kFullWarps * 32, full_min_blocks<T, NP>()) gj_
         __syncwarp();
         // smallest physical column position among the pivot row's columns attaining m
         const T yl = prow_g[li];
-        const uint32_t cc = (!cdone_l && akey(yl) == m) ? ((uint32_t)cpos << 8 | (uint32_t)li) : 0xffffffu;
+        K ky = akey(yl);
+        ky = ky > knan<K>() ? knan<K>() : ky;
+        const uint32_t cc = (!cdone_l && ky == m) ? ((uint32_t)cpos << 8 | (uint32_t)li) : 0xffffffu;
         const uint32_t cw = gmin_u32<L>(cc);
         qc = (int)(cw >> 8);
         c = (int)(cw & 0xffu);
@@ -258,7 +271,8 @@ __global__ void __launch_bounds__(kFullWarps * 32, full_min_blocks<T, NP>()) gj_
         // ties -> smallest physical row position (G3); columns never move
         c = k;
         qc = k;
-        const K key = akey(sel_col<T, NP>(x, k));
+        K key = akey(sel_col<T, NP>(x, k));
+        key = key > knan<K>() ? knan<K>() : key;
         const K m = gmax_key<L>(rdone ? K(0) : key);
         const uint32_t rc = (!rdone && key == m) ? ((uint32_t)pos << 8 | (uint32_t)li) : 0xffffffu;
         const uint32_t rw = gmin_u32<L>(rc);

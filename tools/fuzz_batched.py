@@ -1,0 +1,116 @@
+"""Randomised parity sweep of the batched entry points against the oracle (evidence run,
+not a test: `python tools/fuzz_batched.py [trials] [seed]`).  Per trial: a dtype, an order
+n in 1..64, a batch size (ragged against every kernel's task size) and an input family —
+Gaussian, graded rows (1e-6..1e6), small integers (exact ties), near-singular (a row
+duplicated and perturbed by 1e-9), exactly singular items mixed in, diagonally dominant,
+scaled signed permutations, all-zero items — through gj_invert_batched (K1/K1b/K2/K2e),
+gj_det, gj_solve_batched (K1s/K7, n <= 32) and full pivoting (K6, n <= 32), compared with
+the oracle under the rules of tests/parity.py.  Prints one line per failing trial and a
+summary."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import oracle  # noqa: E402
+import paper_1401_7962_b200 as gj  # noqa: E402
+from tests.parity import compare, ipiv_match, tie_gap  # noqa: E402
+
+VERBOSE = False
+EPS = {np.float32: 2.0 ** -23, np.float64: 2.0 ** -52}
+
+
+def family(rng, kind, B, n, dtype):
+    A = rng.standard_normal((B, n, n))
+    if kind == "graded":
+        A *= 10.0 ** rng.uniform(-6, 6, (B, n, 1))
+    elif kind == "int":
+        A = rng.integers(-3, 4, (B, n, n)).astype(np.float64)
+    elif kind == "nearsing" and n > 1:
+        i, j = rng.choice(n, 2, replace=False)
+        A[:, j] = A[:, i] + 1e-9 * rng.standard_normal((B, n))
+    elif kind == "singular" and n > 1:
+        S = rng.choice(B, max(1, B // 10), replace=False)
+        A[S, 0] = A[S, n - 1]
+        A[S[0]] = 0.0
+    elif kind == "diagdom":
+        A += 2 * n * np.eye(n)
+    elif kind == "perm":
+        A = np.zeros((B, n, n))
+        for b in range(B):
+            A[b, np.arange(n), rng.permutation(n)] = rng.choice([-4.0, -0.5, 0.25, 2.0], n)
+    return A.astype(dtype)
+
+
+def main(trials=120, seed=0):
+    rng = np.random.default_rng(seed)
+    kinds = ["gauss", "graded", "int", "nearsing", "singular", "diagdom", "perm"]
+    fails = 0
+    for tr in range(trials):
+        dtype = [np.float32, np.float64][rng.integers(2)]
+        n = int(rng.choice([1, 2, 3, 5, 8, 13, 16, 17, 24, 31, 32, 33, 40, 47, 63, 64]))
+        B = int(rng.integers(1, 1500))
+        kind = kinds[rng.integers(len(kinds))]
+        tol = float(n * EPS[dtype]) if rng.integers(2) else float(10.0 ** rng.uniform(-12, -4))
+        A = family(rng, kind, B, n, dtype)
+        At = torch.from_numpy(A).cuda()
+        tag = f"trial {tr}: {dtype.__name__} n={n} B={B} {kind} tol={tol:.1e}"
+        if VERBOSE:
+            print("start", tag, flush=True)
+        msgs = []
+        # inverse
+        r = gj.invert_batched(At, tol=tol)
+        d = gj.det(At, tol=tol)
+        torch.cuda.synchronize()
+        g = {k: (None if v is None else v.cpu().numpy()) for k, v in r._asdict().items()}
+        ref = oracle.invert_batched(A, tol=tol)
+        rep = compare(A, g, ref, dtype, tol)
+        if rep.info_fail or rep.ipiv_fail or rep.sign_fail or rep.logdet_fail or rep.inv_kappa_fail:
+            msgs.append("invert: " + rep.summary())
+        for k in ("logabsdet", "sign", "ipiv", "info"):
+            if not torch.equal(getattr(r, k), getattr(d, k)):
+                msgs.append(f"det-only {k} differs from the inverting path")
+        if n <= 32:
+            m = int(rng.integers(1, 33)) if rng.integers(2) else int(rng.integers(1, 9))
+            Bm = rng.standard_normal((B, n, m)).astype(dtype)
+            s = gj.solve_batched(At, torch.from_numpy(Bm).cuda(), tol=tol)
+            f = gj.invert_batched_full(At, tol=tol)
+            torch.cuda.synchronize()
+            rs = oracle.solve_batched(A, Bm, tol=tol)
+            ok = (rs.info == 0) & (s.info.cpu().numpy() == 0)
+            if not np.array_equal(s.info.cpu().numpy() != 0, rs.info != 0):
+                cmin = np.nanmin(np.where(np.isnan(ref.cmax_rel), np.inf, ref.cmax_rel), axis=1)
+                band = (cmin >= tol / 10) & (cmin <= tol * 10)
+                if np.any((s.info.cpu().numpy() != 0) != (rs.info != 0) & ~band):
+                    msgs.append("solve: singular flags differ")
+            if ok.any():
+                Ai = ref.inverse[ok]
+                kap = np.abs(A[ok].astype(np.float64)).sum(2).max(1) * np.abs(Ai).sum(2).max(1)
+                X = s.X.cpu().numpy()[ok].astype(np.float64)
+                e = np.abs(X - rs.X[ok]).max(axis=(1, 2)) / np.maximum(np.abs(rs.X[ok]).max(axis=(1, 2)), 1e-300)
+                lim = np.maximum(2e-4 if dtype == np.float32 else 1e-10, kap * EPS[dtype])
+                if np.any(e > lim):
+                    msgs.append(f"solve m={m}: max e/lim {np.max(e / lim):.2f}")
+                sip = s.ipiv.cpu().numpy()
+                bad = [b for b in np.nonzero(ok)[0] if not ipiv_match(sip[b], rs.ipiv[b], rs.gap[b], thr=tie_gap(dtype, n))[0]]
+                if bad:
+                    msgs.append(f"solve ipiv: {len(bad)} items")
+            gf = {k: (None if v is None else v.cpu().numpy()) for k, v in f._asdict().items()}
+            reff = oracle.invert_full_batched(A, tol=tol)
+            repf = compare(A, gf, reff, dtype, tol)
+            if repf.info_fail or repf.ipiv_fail or repf.sign_fail or repf.logdet_fail or repf.inv_kappa_fail:
+                msgs.append("full: " + repf.summary())
+        if msgs:
+            fails += 1
+            print(tag, "|", " ; ".join(msgs), flush=True)
+    print(f"fuzz: {trials} trials, {fails} failing", flush=True)
+    return fails
+
+
+if __name__ == "__main__":
+    import os
+    VERBOSE = bool(os.environ.get("FUZZ_VERBOSE"))
+    t = int(sys.argv[1]) if len(sys.argv) > 1 else 120
+    sd = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    sys.exit(1 if main(t, sd) else 0)
