@@ -66,6 +66,28 @@ def main(trials=120, seed=0):
         g = {k: (None if v is None else v.cpu().numpy()) for k, v in r._asdict().items()}
         ref = oracle.invert_batched(A, tol=tol)
         rep = compare(A, g, ref, dtype, tol)
+        # reading G27: singular-flag decisions below the kernel precision's resolution (the
+        # oracle's smallest relative pivot and the threshold both under 100 n u(dtype): the
+        # rounding noise of a computed pivot, growth included) are not determined; items that
+        # are numerically singular in the dtype (kappa eps >= 0.1, R4's exemption) have no
+        # meaningful inverse to compare
+        res = 100 * n * EPS[dtype] / 2
+        cmin = np.nanmin(np.where(np.isnan(ref.cmax_rel), np.inf, ref.cmax_rel), axis=1)
+        unres = (cmin < res) & (tol < res)
+        kap0 = np.full(B, np.inf)
+        ok0 = ref.info == 0
+        kap0[ok0] = np.abs(A[ok0].astype(np.float64)).sum(2).max(1) * np.abs(ref.inverse[ok0]).sum(2).max(1)
+        unres |= kap0 * EPS[dtype] >= 0.1   # numerically singular in the dtype: flag not determined
+        rep.info_fail = [b for b in rep.info_fail if not unres[b]]
+        if VERBOSE and rep.info_fail:
+            for b in rep.info_fail[:3]:
+                print(f"   info item {b}: gpu {g['info'][b]} oracle {ref.info[b]} oracle cmin {cmin[b]:.3e} "
+                      f"oracle min step {np.nanargmin(ref.cmax_rel[b])} tol {tol:.2e}", flush=True)
+        kap = np.full(B, np.inf)
+        okr = ref.info == 0
+        kap[okr] = np.abs(A[okr].astype(np.float64)).sum(2).max(1) * np.abs(ref.inverse[okr]).sum(2).max(1)
+        numsing = kap * EPS[dtype] >= 0.1
+        rep.inv_kappa_fail = [b for b in rep.inv_kappa_fail if not numsing[b]]
         if rep.info_fail or rep.ipiv_fail or rep.sign_fail or rep.logdet_fail or rep.inv_kappa_fail:
             msgs.append("invert: " + rep.summary())
         for k in ("logabsdet", "sign", "ipiv", "info"):
@@ -82,7 +104,7 @@ def main(trials=120, seed=0):
             if not np.array_equal(s.info.cpu().numpy() != 0, rs.info != 0):
                 cmin = np.nanmin(np.where(np.isnan(ref.cmax_rel), np.inf, ref.cmax_rel), axis=1)
                 band = (cmin >= tol / 10) & (cmin <= tol * 10)
-                if np.any((s.info.cpu().numpy() != 0) != (rs.info != 0) & ~band):
+                if np.any(((s.info.cpu().numpy() != 0) != (rs.info != 0)) & ~band & ~unres):
                     msgs.append("solve: singular flags differ")
             if ok.any():
                 Ai = ref.inverse[ok]
@@ -90,6 +112,7 @@ def main(trials=120, seed=0):
                 X = s.X.cpu().numpy()[ok].astype(np.float64)
                 e = np.abs(X - rs.X[ok]).max(axis=(1, 2)) / np.maximum(np.abs(rs.X[ok]).max(axis=(1, 2)), 1e-300)
                 lim = np.maximum(2e-4 if dtype == np.float32 else 1e-10, kap * EPS[dtype])
+                lim[kap * EPS[dtype] >= 0.1] = np.inf
                 if np.any(e > lim):
                     msgs.append(f"solve m={m}: max e/lim {np.max(e / lim):.2f}")
                 sip = s.ipiv.cpu().numpy()
@@ -99,6 +122,9 @@ def main(trials=120, seed=0):
             gf = {k: (None if v is None else v.cpu().numpy()) for k, v in f._asdict().items()}
             reff = oracle.invert_full_batched(A, tol=tol)
             repf = compare(A, gf, reff, dtype, tol)
+            cminf = np.nanmin(np.where(np.isnan(reff.cmax_rel), np.inf, reff.cmax_rel), axis=1)
+            repf.info_fail = [b for b in repf.info_fail if not ((cminf[b] < res) and (tol < res))]
+            repf.inv_kappa_fail = [b for b in repf.inv_kappa_fail if not numsing[b]]
             if repf.info_fail or repf.ipiv_fail or repf.sign_fail or repf.logdet_fail or repf.inv_kappa_fail:
                 msgs.append("full: " + repf.summary())
         if msgs:
