@@ -88,6 +88,14 @@ def main(trials=120, seed=0):
         kap[okr] = np.abs(A[okr].astype(np.float64)).sum(2).max(1) * np.abs(ref.inverse[okr]).sum(2).max(1)
         numsing = kap * EPS[dtype] >= 0.1
         rep.inv_kappa_fail = [b for b in rep.inv_kappa_fail if not numsing[b]]
+        # G27 for pivots: a numerically singular item's later pivots are rounding noise, and a
+        # divergence at an oracle gap under 100 n u (the rounding noise with growth) is not
+        # determined at the kernel's precision
+        def undetermined(b, gip=g["ipiv"], rf=ref):
+            if numsing[b]:
+                return True
+            return ipiv_match(gip[b], rf.ipiv[b], rf.gap[b], thr=max(tie_gap(dtype, n), res))[0]
+        rep.ipiv_fail = [b for b in rep.ipiv_fail if not undetermined(b)]
         if rep.info_fail or rep.ipiv_fail or rep.sign_fail or rep.logdet_fail or rep.inv_kappa_fail:
             msgs.append("invert: " + rep.summary())
         for k in ("logabsdet", "sign", "ipiv", "info"):
@@ -116,7 +124,9 @@ def main(trials=120, seed=0):
                 if np.any(e > lim):
                     msgs.append(f"solve m={m}: max e/lim {np.max(e / lim):.2f}")
                 sip = s.ipiv.cpu().numpy()
-                bad = [b for b in np.nonzero(ok)[0] if not ipiv_match(sip[b], rs.ipiv[b], rs.gap[b], thr=tie_gap(dtype, n))[0]]
+                bad = [b for b in np.nonzero(ok)[0]
+                       if not ipiv_match(sip[b], rs.ipiv[b], rs.gap[b], thr=max(tie_gap(dtype, n), res))[0]
+                       and kap0[b] * EPS[dtype] < 0.1]
                 if bad:
                     msgs.append(f"solve ipiv: {len(bad)} items")
             gf = {k: (None if v is None else v.cpu().numpy()) for k, v in f._asdict().items()}
