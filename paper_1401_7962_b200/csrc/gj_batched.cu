@@ -57,6 +57,17 @@ constexpr int kWarpsPerBlock = 4;
 // as a build-time option, -DGJ_K1_FAST_PIVOT=1)
 constexpr bool kFastPivot = GJ_K1_FAST_PIVOT != 0;
 // K1b block loop unrolling (build option -DGJ_K1B_UNROLL=n, A/B measurements)
+#ifndef GJ_K1B_LDS64
+#define GJ_K1B_LDS64 0
+#endif
+#ifndef GJ_K1B_WSYNC
+#define GJ_K1B_WSYNC 0
+#endif
+#if GJ_K1B_WSYNC
+#define K1B_SYNC() asm volatile("bar.warp.sync 0xffffffff;" ::: "memory")
+#else
+#define K1B_SYNC() __syncwarp()
+#endif
 #ifndef GJ_K1B_UNROLL
 #define GJ_K1B_UNROLL 1
 #endif
@@ -686,7 +697,14 @@ __device__ __forceinline__ void blk_trail_term(float (&T)[R][N], const float (&P
                                                int tofs) {
   constexpr int RW = 32 - BS;
   float Rs[J1 - J0];
-  ld_row<float, J1 - J0>(Rs, rbuf_g + s * RW + J0);
+  if constexpr (GJ_K1B_LDS64) {
+    const uint32_t ab = smem_u32(rbuf_g + s * RW + J0);
+#pragma unroll
+    for (int j = 0; j < J1 - J0; j += 2)
+      asm volatile("ld.volatile.shared.v2.f32 {%0, %1}, [%2];" : "=f"(Rs[j]), "=f"(Rs[j + 1]) : "r"(ab + 4u * j));
+  } else {
+    ld_row<float, J1 - J0>(Rs, rbuf_g + s * RW + J0);
+  }
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -737,7 +755,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  K1B_SYNC();
   if (lane == 0 && task0 < ntasks) {
     mbar_expect_tx(&bars[0], Geo::STAGE);
     tma_load_2d(stage0, &tm.a, 0, (int)(task0 * Geo::ROWS), &bars[0]);
@@ -773,7 +791,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
         for (int j = 0; j < 32; ++j) x[r][j] = (row == j) ? 1.0f : 0.0f;
       }
     }
-    __syncwarp();
+    K1B_SYNC();
     float rowmax = 0.0f;
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -804,7 +822,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
 #pragma unroll kK1bUnroll
     for (int kb = 0; kb + BS < 32; kb += BS) {
       blk_publish<R, BS>(T, bs, rbuf_g);
-      __syncwarp();
+      K1B_SYNC();
       float NP[R][BS];
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -822,7 +840,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
         else
           blk_trail_term<R, BS, BS, RW, RW, true>(T, P, s, rbuf_g, BS);   // + the rotation
       }
-      __syncwarp();   // every lane has read rbuf before the next publish
+      K1B_SYNC();   // every lane has read rbuf before the next publish
 #pragma unroll
       for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -834,7 +852,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     }
     // last block: its whole update, then x = [T | P] (register j = compact column j)
     blk_publish<R, BS>(T, bs, rbuf_g);
-    __syncwarp();
+    K1B_SYNC();
 #pragma unroll
     for (int s = 0; s < BS; ++s) blk_trail_term<R, BS, 0, RW, RW>(T, P, s, rbuf_g, 0);
 #pragma unroll
@@ -881,7 +899,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     if (a.Ainv != nullptr) {
 #pragma unroll
       for (int r = 0; r < R; ++r) perm_g[pos[r]] = (li + L * r) * 4;   // output column (bytes)
-      __syncwarp();
+      K1B_SYNC();
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const RowAddr<float, 32, true> dst(g * 32 + pos[r]);
@@ -897,13 +915,13 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
         *own = *own + myrp[r];
       }
       fence_async_smem();
-      __syncwarp();
+      K1B_SYNC();
       if (lane == 0) {
         tma_store_2d(&tm.x, 0, (int)(task * Geo::ROWS), stage);
         bulk_commit();
       }
     }
-    __syncwarp();
+    K1B_SYNC();
     if constexpr (NST == 1) {
       if (lane == 0 && nxt < ntasks) {
         bulk_wait_read0();   // the store has read the stage
