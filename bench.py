@@ -5,11 +5,16 @@ gj_invert_batched call (outputs: inverse, log|det|, sign — exactly BASELINE's 
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL process group for the barrier and
-the max-over-ranks timing only): batches shard with no data-path collective, every rank
-inverts its own full C2-sized batch (weak scaling; rank r > 0 draws from seed (1, r)).
+`--gpus N` with N > 1 runs N ranks, one per GPU: launched by the driver under torchrun, or,
+when no torchrun environment is present, this script re-executes itself under
+`torch.distributed.run` (127.0.0.1 rendezvous); the world size must equal N.  The C2 batch
+is SHARDED (BASELINE configs[4] "config 2's batch sharded"): rank r inverts
+the contiguous items [r B/N, (r+1) B/N) of the seed-1 batch with no data-path collective
+(the NCCL group carries the barrier and the max-over-ranks time only) — strong scaling;
+the weak-scaling figure (every rank a full C2-sized batch) is a secondary key.
+`--workload c5` (one fp64 32768^2 matrix, column-block-cyclic) goes through the same launcher.
 `--impl reference` times the CPU oracle (oracle/, long double, all host cores) on a
-bounded sample of the same workload.  Prints ONE JSON line on rank 0.
+bounded sample of the same workload, rank 0 only.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -49,7 +54,31 @@ def parse():
     p.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
                    help="c2: the headline batched line; c5: one fp64 32768^2 matrix, column-block-cyclic over the ranks")
     p.add_argument("--n", type=int, default=32768, help="order for --workload c5")
+    p.add_argument("--no-weak", action="store_true", help="skip the weak-scaling secondary key (N > 1)")
     return p.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def maybe_launch(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run with N ranks."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
+
+def shard(total: int, world: int, rank: int):
+    """Contiguous [lo, hi) of rank r (sizes differ by at most one item)."""
+    return total * rank // world, total * (rank + 1) // world
 
 
 def dist_env():
@@ -141,8 +170,16 @@ def compute_peaks():
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
-        return float(d["fp64_dmma_tflops"]), "measured (profiles/peaks_r01.json, tools/dmma_probe.cu mma.sync f64)"
+        return float(d["fp64_dmma_tflops"]), ("measured by this repo's tools/dmma_probe.cu (builder's gpurun, "
+                                              "profiles/peaks_r01.json; the driver's MEASURED_PEAKS.json has no FP64 "
+                                              "figure); nominal 148 x 64 x 2 x 1.965 GHz = 37.2")
     return 37.2, "derived (148 SMs x 64 FP64 lanes x 2 x 1.965 GHz)"
+
+
+def fp64_peak():
+    """FP64 peak for the batched C3 kernel (DFMA + DMMA share the FP64 pipe on B200): the
+    measured DMMA rate (profiles/peaks_r01.json), same figure as the large-n roofline."""
+    return compute_peaks()
 
 
 def c4_measure(dev, reps: int = 3):
@@ -321,7 +358,8 @@ def f4_measure(A, stream, nrhs: int = 1, reps: int = 3):
 
 
 def cpu_baseline(sample: int, A_host=None):
-    """The oracle as it stands, on the host's cores, on the first `sample` items of C2."""
+    """The oracle as it stands, on the host's cores, on the first `sample` items of C2; plus
+    the same oracle on ONE core (a 1/16 sample) and the host's CPU model."""
     import oracle
     import synth
     A = A_host[:sample] if A_host is not None and len(A_host) >= sample else synth.gen_c2(batch=sample)
@@ -329,11 +367,34 @@ def cpu_baseline(sample: int, A_host=None):
     t0 = time.perf_counter()
     oracle.invert_batched(A, tol=N * 2.0 ** -23, nthreads=nth)
     dt = time.perf_counter() - t0
-    return {"value": sample / dt, "unit": UNIT, "cores": nth, "kind": "oracle",
-            "sample": f"first {sample} items of C2 (seed 1), long-double [A|I] GJ, {dt:.2f} s wall"}
+    s1 = max(1024, sample // 16)
+    t1 = time.perf_counter()
+    oracle.invert_batched(A[:s1], tol=N * 2.0 ** -23, nthreads=1)
+    dt1 = time.perf_counter() - t1
+    return dict({"value": sample / dt, "unit": UNIT, "cores": nth, "kind": "oracle",
+                 "sample": f"first {sample} items of C2 (seed 1), long-double [A|I] GJ, {dt:.2f} s wall",
+                 "one_core": {"value": s1 / dt1, "unit": UNIT, "sample": f"first {s1} items, nthreads=1, {dt1:.2f} s"}},
+                **host_info())
+
+
+def host_info():
+    cpu = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    cpu = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": cpu, "host_cores": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
 
 
 def run_reference(args, rank, world):
+    """The base contract's reference arm for this tier: the oracle as it stands, on the host's
+    cores, rank 0 only (other ranks exit without work).  Every timed step is one bounded
+    sample (SAMPLE items of C2) — ms_per_step is that sample's real time; the full-batch
+    time it implies is a separate key, never the step time."""
     if rank != 0:
         return
     import oracle
@@ -342,23 +403,47 @@ def run_reference(args, rank, world):
     A = synth.gen_c2(batch=sample)
     nth = oracle.threads()
     for _ in range(args.warmup):
-        oracle.invert_batched(A[: min(256, sample)], tol=N * 2.0 ** -23, nthreads=nth)
+        oracle.invert_batched(A[: min(1024, sample)], tol=N * 2.0 ** -23, nthreads=nth)
     times = []
-    for _ in range(args.steps if args.steps <= 5 else 5):
+    for _ in range(args.steps):
         t0 = time.perf_counter()
         oracle.invert_batched(A, tol=N * 2.0 ** -23, nthreads=nth)
         times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
     val = sample / dt
+    B = args.batch
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-            "steps": len(times), "warmup": args.warmup, "ms_per_step": dt * 1e3 * BATCH / sample,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f80 (x87 long double)",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": BATCH * world, "n": N,
-                                             "parallelism": "cpu-openmp", "sample_items_per_step": sample},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": nth, "kind": "oracle",
-                             "sample": f"first {sample} items of C2 per step (bounded sample)"},
+            "steps": len(times), "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f80 (x87 long double)",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "global_batch": B, "n": N, "per_gpu_batch": B // world,
+                       "parallelism": f"dp{world} (contiguous shards of the one seed-1 batch, no collective)",
+                       "l2": "inputs (4 GiB total) larger than L2 (126 MB); no flush needed",
+                       "outputs": "inverse, logabsdet, sign"},
+            "sample_items_per_step": sample,
+            "ms_per_full_batch_extrapolated": dt * 1e3 * B / sample,
+            "cpu_baseline": dict({"value": val, "unit": UNIT, "cores": nth, "kind": "oracle",
+                                  "sample": f"first {sample} items of C2 (seed 1) per step, {len(times)} steps"},
+                                 **host_info()),
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def c5_oracle_baseline(n_full: int, n: int = 8192):
+    """the oracle timed at n = 8192 on the C5 generator (N(0,1)/sqrt(n), seed 4)
+    on the host's cores, and the n^3-extrapolated time of the full C5 order."""
+    import oracle
+    import synth
+    A = synth.gen_gaussian(n, seed=4)
+    nth = oracle.threads()
+    t0 = time.perf_counter()
+    oracle.invert(A, tol=n * 2.0 ** -52, nthreads=nth)
+    dt = time.perf_counter() - t0
+    fl = 2.0 * n ** 3 - n ** 2
+    return dict({"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": nth, "kind": "oracle",
+                 "sample": f"one fp64 {n}x{n} N(0,1)/sqrt(n), seed 4 (the C5 generator), {dt:.1f} s wall",
+                 "extrapolated_c5_seconds": dt * (n_full / n) ** 3,
+                 "extrapolation": f"n^3: x{(n_full / n) ** 3:.0f} to n = {n_full}"}, **host_info())
 
 
 def run_c5(args, rank, world, local):
@@ -394,14 +479,15 @@ def run_c5(args, rank, world, local):
     for _ in range(args.warmup):
         invert_dist(A_local, n)
     times, res = [], None
-    for _ in range(args.steps):
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        res = invert_dist(A_local, n)
-        b.record()
-        barrier()
-        times.append(a.elapsed_time(b))
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            res = invert_dist(A_local, n)
+            b.record()
+            barrier()
+            times.append(a.elapsed_time(b))
     t = torch.tensor([float(np.mean(times))], device=dev, dtype=torch.float64)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
@@ -419,9 +505,60 @@ def run_c5(args, rank, world, local):
                           "roofline": {"bound": "tensor", "achieved": tf, "peak": peak * world, "unit": "TFLOP/s",
                                        "frac": tf / (peak * world), "traffic": None, "peak_source": src + f" x {world}"},
                           "logabsdet": res.logabsdet, "sign": res.sign, "info": res.info,
-                          "gpu_launches": None}), flush=True)
+                          "clocks": clk.summary(), "gpu_launches": None,
+                          "cpu_baseline": None if args.no_cpu_baseline else c5_oracle_baseline(n)}), flush=True)
     tdist.barrier()
     tdist.destroy_process_group()
+
+
+def c3_measure(dev, reps: int = 5):
+    """BASELINE configs[2] as a secondary key of the headline line: 262,144 x 64 x 64 fp64
+    (A = P L diag(u), 1% duplicated-row items, seed 2), tol 1e-10, through gj_invert_batched
+    (K2e).  FP64 roofline: 2n^3 - n^2 flops per item at the derived DFMA/DMMA peak."""
+    import torch
+    import paper_1401_7962_b200 as gj
+    import synth
+    A_host = synth.gen_c3(seed=2)
+    B, n = A_host.shape[0], A_host.shape[1]
+    A = torch.from_numpy(A_host).to(dev)
+    del A_host
+    X = torch.empty_like(A)
+    ip = torch.empty((B, n), dtype=torch.int32, device=dev)
+    lg = torch.empty(B, dtype=torch.float64, device=dev)
+    sg = torch.empty(B, dtype=torch.int8, device=dev)
+    dt_ = torch.empty(B, dtype=torch.float64, device=dev)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        st = gj.lib.gj_invert_batched(1, n, B, A.data_ptr(), X.data_ptr(), ip.data_ptr(), lg.data_ptr(),
+                                      sg.data_ptr(), dt_.data_ptr(), info.data_ptr(), synth.C3_TOL,
+                                      stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize(dev)
+    total, each = time_steps(step, stream, reps, lambda: torch.cuda.synchronize(dev))
+    ms = total / reps
+    fl = B * (2.0 * n ** 3 - n ** 2)
+    tf = fl / (ms / 1e3) / 1e12
+    peak, src = fp64_peak()
+    hbm, _ = measured_peaks()
+    byts = B * (2 * n * n * 8 + n * 4 + 8 + 1 + 8 + 4)
+    out = {"workload": "C3: batch 262144 x 64x64 fp64, A = P L diag(u), 1% duplicated-row items, seed 2, "
+                       "tol 1e-10 (BASELINE.json configs[2])",
+           "metric": "matrices inverted/s (batched n=64 fp64)", "value": B / (ms / 1e3), "unit": "matrices/s",
+           "ms": ms, "reps": reps, "singular_items": int((info != 0).sum().item()),
+           "roofline": {"bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                        "traffic": None, "peak_source": src,
+                        "kernel": "gj_batched64e_kernel (K2e: one warp per matrix, shared-memory resident, DMMA "
+                                  "blocked update)",
+                        "hbm_achieved_gbs": byts / (ms / 1e3) / 1e9, "hbm_peak_gbs": hbm}}
+    del A, X
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_c3(args, rank, world, local):
@@ -504,8 +641,35 @@ def run_c3(args, rank, world, local):
         torch.distributed.destroy_process_group()
 
 
+def time_steps(step, stream, steps, barrier):
+    """K timed launches on `stream` bracketed by barriers: (total ms, per-launch ms list)."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    barrier()
+    return t_start.elapsed_time(t_end), [x.elapsed_time(y) for x, y in ev]
+
+
+def max_over_ranks(v: float, world: int, dev) -> float:
+    if world == 1:
+        return v
+    import torch
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def main():
     args = parse()
+    maybe_launch(args)
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -525,16 +689,12 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    B = args.batch
-    # ---- synthetic input (host generation is outside every timed region)
-    if rank == 0:
-        A_host = synth.gen_c2(batch=B)
-    else:
-        A_host = np.empty((B, N, N), np.float32)
-        rng = np.random.default_rng([1, rank])
-        for s in range(0, B, synth.C2_CHUNK):
-            e = min(B, s + synth.C2_CHUNK)
-            A_host[s:e] = rng.standard_normal((e - s, N, N), dtype=np.float32)
+    Btot = args.batch
+    lo, hi = shard(Btot, world, rank)
+    B = hi - lo
+    # ---- synthetic input: this rank's contiguous shard of the seed-1 C2 batch (host
+    # generation is outside every timed region)
+    A_host = synth.gen_c2(batch=B) if (lo == 0 and hi == Btot) else synth.gen_c2_shard(lo, hi)
     A = torch.from_numpy(A_host).to(dev)
     X = torch.empty_like(A)
     lg = torch.empty((B,), dtype=torch.float64, device=dev)
@@ -557,29 +717,40 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        barrier()
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        t_end.record(stream)
-        barrier()
-    total_ms = t_start.elapsed_time(t_end)
-    launch_ms = [a.elapsed_time(b) for a, b in ev]
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms, launch_ms = time_steps(step, stream, args.steps, barrier)
+    total_ms = max_over_ranks(total_ms, world, dev)
     ms_per_step = total_ms / args.steps
-    value = world * B / (ms_per_step / 1e3)
+    value = Btot / (ms_per_step / 1e3)          # every item of the sharded batch, all ranks
     avg_launch_ms = float(np.mean(launch_ms))
-    f2 = f2_measure(A, X, tol, stream) if (rank == 0 and not args.no_c4) else None
-    f4 = f4_measure(A, stream) if (rank == 0 and not args.no_c4) else None
+    f2 = f2_measure(A, X, tol, stream) if (rank == 0 and not args.no_c4 and world == 1) else None
+    f4 = f4_measure(A, stream) if (rank == 0 and not args.no_c4 and world == 1) else None
+
+    # ---- weak scaling (secondary): every rank a full C2-sized batch (its shard tiled)
+    weak = None
+    if world > 1 and not args.no_weak:
+        del X
+        torch.cuda.empty_cache()
+        reps = -(-Btot // B)
+        Aw = A.repeat(reps, 1, 1)[:Btot].contiguous()
+        Xw = torch.empty_like(Aw)
+        lgw = torch.empty((Btot,), dtype=torch.float64, device=dev)
+        sgw = torch.empty((Btot,), dtype=torch.int8, device=dev)
+
+        def step_w():
+            st = gj.lib.gj_invert_batched(0, N, Btot, Aw.data_ptr(), Xw.data_ptr(), None, lgw.data_ptr(),
+                                          sgw.data_ptr(), None, None, tol, stream.cuda_stream)
+            if st != 0:
+                raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+        step_w()
+        wt, _ = time_steps(step_w, stream, max(3, args.steps // 4), barrier)
+        wt = max_over_ranks(wt, world, dev) / max(3, args.steps // 4)
+        weak = {"value": world * Btot / (wt / 1e3), "unit": UNIT, "ms_per_step": wt, "per_gpu_batch": Btot,
+                "scaling": "weak", "note": "each rank a full C2-sized batch (its shard tiled), no collective"}
+        del Aw, Xw
+        torch.cuda.empty_cache()
+        X = torch.empty_like(A)
 
     # ---- end to end through the public API with HOST buffers (pinned), copies inside
     e2e = None
@@ -601,37 +772,38 @@ def main():
             ts.append(time.perf_counter() - t0)
         # median of the timed calls (host-side outliers — one call in five at 2.5x — come and
         # go with the box; the mean and every call are in the line as well)
-        e2e_s = float(np.median(ts))
+        e2e_s = max_over_ranks(float(np.median(ts)), world, dev)
         e2e_mean_s = float(np.mean(ts))
-        if world > 1:
-            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = {"value": world * B / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Ah.numel() * 4),
+        e2e = {"value": Btot / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Ah.numel() * 4),
                "d2h_bytes_per_step": int(Xh.numel() * 4 + B * 9), "ms_per_step": e2e_s * 1e3,
-               "ms_each": [round(t * 1e3, 2) for t in ts], "stat": f"median of {len(ts)}",
-               "value_mean": world * B / e2e_mean_s,
+               "ms_each": [round(t * 1e3, 2) for t in ts], "stat": f"median of {len(ts)}, max over ranks",
+               "value_mean": Btot / e2e_mean_s,
                "api": "gj_invert_batched_host (pinned host buffers, chunked H2D/compute/D2H pipeline)"}
 
     if rank == 0:
         peak, peak_src = measured_peaks()
         achieved = B * BYTES_PER_MATRIX / (avg_launch_ms / 1e3) / 1e9
-        traffic = profile_traffic()
+        traffic = profile_traffic() if B == BATCH else None
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "gj_blk32_kernel<2,4,2> (K1b)",
                 "algorithmic_bytes_per_launch": B * BYTES_PER_MATRIX, "peak_source": peak_src,
+                "per_unit_bytes": BYTES_PER_MATRIX, "units_per_launch": B,
                 "fp32_flops_per_launch": B * FLOPS_PER_MATRIX,
-                "achieved_fp32_tflops": B * FLOPS_PER_MATRIX / (avg_launch_ms / 1e3) / 1e12}
+                "achieved_fp32_tflops": B * FLOPS_PER_MATRIX / (avg_launch_ms / 1e3) / 1e12,
+                "timing": "CUDA events around each launch on the launching stream, mean over the timed steps"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "global_batch": B * world, "n": N, "per_gpu_batch": B,
-                           "parallelism": f"dp{world} (independent shards, no collective)",
-                           "l2": "inputs (4 GiB/GPU) larger than L2 (126 MB); no flush needed",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "global_batch": Btot, "n": N, "per_gpu_batch": B,
+                           "parallelism": f"dp{world} (contiguous shards of the one seed-1 batch, no collective)",
+                           "l2": "inputs (4 GiB total) larger than L2 (126 MB); no flush needed",
                            "outputs": "inverse, logabsdet, sign"},
                 "roofline": roof, "gpu_launches": args.steps, "clocks": clk.summary(), "e2e": e2e}
-        if not args.no_c4:
+        if weak is not None:
+            line["weak_scaling"] = weak
+        if not args.no_c4 and world == 1:
             line["secondary"] = c4_measure(dev)
+            line["secondary_c3"] = c3_measure(dev)
             line["next_f1"] = f1_measure(dev)
             line["next_f2"] = f2
             line["next_f4"] = f4

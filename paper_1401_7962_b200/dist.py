@@ -176,10 +176,15 @@ def invert_dist(A_local: torch.Tensor, n: int, *, group=None, tol: Optional[floa
     i32 = dict(dtype=torch.int32, device=device)
     X = torch.empty((npad, max(nl, 1)), **f64)
     # replicated state, broadcast by the panel owner as one int32 buffer:
-    # pos | pivstep | rec_q | rec_row | rec_p (fp64 viewed as 2 x int32)
-    ibuf = torch.empty(6 * npad, **i32)
-    pos, pivstep, rec_q, rec_row = ibuf[:npad], ibuf[npad:2 * npad], ibuf[2 * npad:3 * npad], ibuf[3 * npad:4 * npad]
-    rec_p = ibuf[4 * npad:].view(torch.float64)
+    # pos | pivstep | rec_q | rec_row | rec_p (fp64 viewed as 2 x int32).  Double-buffered by
+    # panel parity like W: panel k+1's broadcast lands in the buffer panel k-1's update read,
+    # never in the one panel k's update (running beside it) still reads.
+    ibufs = [torch.empty(6 * npad, **i32) for _ in range(2)]
+
+    def views(ib):
+        return (ib[:npad], ib[npad:2 * npad], ib[2 * npad:3 * npad], ib[3 * npad:4 * npad],
+                ib[4 * npad:].view(torch.float64))
+
     # the factored panel W, double-buffered: W_{k+1} arrives while panel k's update still reads W_k
     wbuf = [torch.empty((npad, BLOCK), **f64) for _ in range(2)]
     R = torch.empty((BLOCK, max(nl, 1)), **f64)
@@ -204,6 +209,7 @@ def invert_dist(A_local: torch.Tensor, n: int, *, group=None, tol: Optional[floa
 
     mark("start")
     nb = npad // BLOCK
+    pos, pivstep, rec_q, rec_row, rec_p = views(ibufs[0])
     steps.init(A_local if nr else None, max(nr, 1), X, pos, pivstep, smax)
     allreduce_max(smax)   # bit patterns of non-negative doubles order like the values
     Xo = X if nl else None
@@ -212,42 +218,47 @@ def invert_dist(A_local: torch.Tensor, n: int, *, group=None, tol: Optional[floa
     if rank == 0:
         steps.factor(0, X, pos, pivstep, rec_p, rec_q, rec_row, wbuf[0])
     if P > 1:
-        bcast(ibuf, 0)
+        bcast(ibufs[0], 0)
         bcast(wbuf[0], 0)
     ev_upd = record(main)
     for k in range(nb):
         W = wbuf[k % 2]
+        _, pivstep, _, rec_row, _ = views(ibufs[k % 2])
         nxt = k + 1 < nb
         own_next = nxt and (k + 1) % P == rank
         ev_fac = None
         if own_next:
-            # look-ahead: panel k+1's columns first, factor it, then the rest of panel k's
-            # update runs beside that factorisation (programmatic dependent launch)
+            # look-ahead: panel k+1's columns first, factor it (on a copy of the state in the
+            # other buffer), then the rest of panel k's update runs beside that factorisation
             steps.update(k, 1, Xo, W, pivstep, rec_row, Ro)
-            steps.factor(k + 1, X, pos, pivstep, rec_p, rec_q, rec_row, wbuf[(k + 1) % 2])
+            ibufs[(k + 1) % 2].copy_(ibufs[k % 2])
+            npos, npiv, nrq, nrr, nrp = views(ibufs[(k + 1) % 2])
+            steps.factor(k + 1, X, npos, npiv, nrp, nrq, nrr, wbuf[(k + 1) % 2])
             ev_fac = record(main)
             steps.update(k, 2, Xo, W, pivstep, rec_row, Ro)
         else:
             steps.update(k, 0, Xo, W, pivstep, rec_row, Ro)
         if nxt and P > 1:
-            # panel k+1 travels on a side stream: after its factorisation (owner) and after the
-            # last update that read the buffer it lands in (everyone); not after panel k's update
+            # panel k+1 travels on a side stream into the buffers of parity k+1: after its
+            # factorisation (owner) and after panel k-1's update, their last reader — not after
+            # panel k's update, which reads the other parity
             if cuda:
                 side.wait_event(ev_upd)
                 if ev_fac is not None:
                     side.wait_event(ev_fac)
                 with torch.cuda.stream(side):
-                    bcast(ibuf, (k + 1) % P)
+                    bcast(ibufs[(k + 1) % 2], (k + 1) % P)
                     bcast(wbuf[(k + 1) % 2], (k + 1) % P)
                 ev_b = record(side)
                 ev_upd = record(main)
                 main.wait_event(ev_b)
             else:
-                bcast(ibuf, (k + 1) % P)
+                bcast(ibufs[(k + 1) % 2], (k + 1) % P)
                 bcast(wbuf[(k + 1) % 2], (k + 1) % P)
         elif cuda:
             ev_upd = record(main)
     mark("eliminated")
+    pos, pivstep, rec_q, rec_row, rec_p = views(ibufs[(nb - 1) % 2])
     ipiv = torch.empty(n, **i32)
     lg = torch.empty(1, **f64)
     sg = torch.empty(1, dtype=torch.int8, device=device)

@@ -70,6 +70,22 @@ def gen_c2(batch: int = 1048576, seed: int = 1, out: Optional[np.ndarray] = None
     return out
 
 
+def gen_c2_shard(lo: int, hi: int, seed: int = 1, chunk: int = C2_CHUNK) -> np.ndarray:
+    """Items [lo, hi) of the C2 stream (the same values gen_c2 gives there): the chunks
+    before ``lo`` are drawn and dropped, so a rank's contiguous shard of the seed-1 batch
+    is reproduced without holding the whole batch."""
+    n = 32
+    rng = np.random.default_rng(seed)
+    out = np.empty((hi - lo, n, n), dtype=np.float32)
+    for s in range(0, hi, chunk):
+        e = min(hi, s + chunk)
+        blk = rng.standard_normal((e - s, n, n), dtype=np.float32)
+        a, b = max(s, lo), e
+        if b > a:
+            out[a - lo:b - lo] = blk[a - s:b - s]
+    return out
+
+
 def gen_c3(batch: int = 262144, seed: int = 2, singular_frac: float = 0.01,
            chunk: int = C3_CHUNK, return_singular: bool = False):
     """BASELINE.json configs[2] under reading G15: A = (L·diag(u))[perm] with L unit-lower,

@@ -31,7 +31,9 @@ class Report:
     inv_flat_fail: list = field(default_factory=list)
     inv_kappa_fail: list = field(default_factory=list)
     ipiv_fail: list = field(default_factory=list)
-    ipiv_tie_exempt: int = 0
+    ipiv_tie_exempt: int = 0          # items whose pivots leave the oracle's at a gap <= 1e-6 (G12)
+    ipiv_g26_exempt: int = 0          # ... at a gap in (1e-6, n u] (reading G26's raised band)
+    ipiv_g26_items: list = field(default_factory=list)
     sign_fail: list = field(default_factory=list)
     logdet_fail: list = field(default_factory=list)
     det_fail: list = field(default_factory=list)
@@ -43,7 +45,7 @@ class Report:
     def summary(self) -> str:
         return (f"items={self.n_items} singular_ref={self.n_singular_ref} inv_flat_fail={len(self.inv_flat_fail)} "
                 f"inv_kappa_fail={len(self.inv_kappa_fail)} ipiv_fail={len(self.ipiv_fail)} "
-                f"ipiv_tie_exempt={self.ipiv_tie_exempt} sign_fail={len(self.sign_fail)} "
+                f"ipiv_tie_exempt={self.ipiv_tie_exempt} ipiv_g26_exempt={self.ipiv_g26_exempt} sign_fail={len(self.sign_fail)} "
                 f"logdet_fail={len(self.logdet_fail)} det_fail={len(self.det_fail)} info_fail={len(self.info_fail)} "
                 f"max_inv_err={self.max_inv_err:.3e} max_e/(k*eps)={self.max_inv_err_over_keps:.3e} "
                 f"max_dlogdet={self.max_logdet_err:.3e}")
@@ -61,6 +63,12 @@ def ipiv_match(ipiv_gpu, ipiv_ref, gap_ref, jpiv_gpu=None, jpiv_ref=None, thr=TI
         return True, False
     k = neq[0]
     return bool(gap_ref[k] <= thr), True
+
+
+def first_divergence_gap(ipiv_gpu, ipiv_ref, gap_ref):
+    """The oracle's top-two gap at the first step where the pivots differ (None if equal)."""
+    neq = np.nonzero(ipiv_gpu != ipiv_ref)[0]
+    return None if len(neq) == 0 else float(gap_ref[neq[0]])
 
 
 def compare(A, gpu, ref, dtype, tol, kappa=None, check_ipiv=True, check_det=False, det_rtol=1e-12,
@@ -105,7 +113,13 @@ def compare(A, gpu, ref, dtype, tol, kappa=None, check_ipiv=True, check_det=Fals
             ok, ex = ipiv_match(gpu["ipiv"][b], ref.ipiv[b], ref.gap[b],
                                 gpu["jpiv"][b] if full else None, ref.jpiv[b] if full else None,
                                 thr=tie_gap(dtype, A.shape[-1]))
-            rep.ipiv_tie_exempt += int(ex and ok)
+            if ex and ok:
+                g = first_divergence_gap(gpu["ipiv"][b], ref.ipiv[b], ref.gap[b]) if not full else 0.0
+                if g is not None and g > TIE_GAP:
+                    rep.ipiv_g26_exempt += 1
+                    rep.ipiv_g26_items.append(int(b))
+                else:
+                    rep.ipiv_tie_exempt += 1
             if not ok:
                 rep.ipiv_fail.append(int(b))
     if "sign" in gpu:

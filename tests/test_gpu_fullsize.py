@@ -73,13 +73,29 @@ def test_c2_every_item(gj, torch):
     gall = {k: v.cpu().numpy() for k, v in r._asdict().items() if v is not None}
     worst = 0.0
     ch = 65536
+    tot = {"items": 0, "ipiv_exempt_gap_le_1e-6": 0, "ipiv_exempt_g26_band": 0, "g26_items": [],
+           "inv_flat_fail_kappa_rule_pass": 0, "singular_ref": 0}
     for c0 in range(0, A.shape[0], ch):
         sl = slice(c0, c0 + ch)
         ref = oracle.invert_batched(A[sl], tol=tol)
         rep = compare(A[sl], {k: v[sl] for k, v in gall.items()}, ref, np.float32, tol)
         assert_report(rep)
         worst = max(worst, rep.max_inv_err_over_keps)
-    print(f"C2 every item: max e/(kappa eps) = {worst:.4f}")
+        tot["items"] += rep.n_items
+        tot["ipiv_exempt_gap_le_1e-6"] += rep.ipiv_tie_exempt
+        tot["ipiv_exempt_g26_band"] += rep.ipiv_g26_exempt
+        tot["g26_items"] += [c0 + b for b in rep.ipiv_g26_items]
+        tot["inv_flat_fail_kappa_rule_pass"] += len(rep.inv_flat_fail)
+        tot["singular_ref"] += rep.n_singular_ref
+    tot["max_e_over_kappa_eps"] = worst
+    print(f"C2 every item: max e/(kappa eps) = {worst:.4f}; {tot}")
+    # the bench line carries these counts from the committed copy of this report
+    # (GJ_PARITY_REPORT=path; profiles/r02_c2_parity.json)
+    if os.environ.get("GJ_PARITY_REPORT"):
+        import json
+        with open(os.environ["GJ_PARITY_REPORT"], "w") as f:
+            json.dump(dict(tot, rules="tests/parity.py R1 R3 R4 R5 R7; G26 band = (1e-6, 32 u] with u = 2^-24",
+                           test="tests/test_gpu_fullsize.py::test_c2_every_item"), f, indent=1)
 
 
 def test_c3_full_sampled(gj, torch):

@@ -18,6 +18,7 @@ import paper_1401_7962_b200 as gj  # noqa: E402
 from tests.parity import compare, ipiv_match, tie_gap  # noqa: E402
 
 VERBOSE = False
+EXEMPT = {}   # pivot divergences exempted by G27, by rule (reported next to the strict result)
 EPS = {np.float32: 2.0 ** -23, np.float64: 2.0 ** -52}
 
 
@@ -88,14 +89,30 @@ def main(trials=120, seed=0):
         kap[okr] = np.abs(A[okr].astype(np.float64)).sum(2).max(1) * np.abs(ref.inverse[okr]).sum(2).max(1)
         numsing = kap * EPS[dtype] >= 0.1
         rep.inv_kappa_fail = [b for b in rep.inv_kappa_fail if not numsing[b]]
-        # G27 for pivots: a numerically singular item's later pivots are rounding noise, and a
-        # divergence at an oracle gap under 100 n u (the rounding noise with growth) is not
-        # determined at the kernel's precision
+        # G27 for pivots: a divergence at an oracle gap under 100 n u (the rounding
+        # noise with growth) is not determined at the kernel's precision, and neither is any step
+        # after the first one whose oracle pivot is below that resolution (its candidates are
+        # rounding noise); counted separately from the strict R3 / G26 result
+        def first_unresolved(b, rf=ref):
+            low = np.nonzero(np.nan_to_num(rf.cmax_rel[b], nan=np.inf) < res)[0]
+            return int(low[0]) if len(low) else n
+
         def undetermined(b, gip=g["ipiv"], rf=ref):
-            if numsing[b]:
-                return True
-            return ipiv_match(gip[b], rf.ipiv[b], rf.gap[b], thr=max(tie_gap(dtype, n), res))[0]
-        rep.ipiv_fail = [b for b in rep.ipiv_fail if not undetermined(b)]
+            k0 = first_unresolved(b)
+            if k0 < n:
+                ok, _ = ipiv_match(gip[b][:k0], rf.ipiv[b][:k0], rf.gap[b][:k0], thr=tie_gap(dtype, n))
+                if ok:
+                    return "after_unresolved_pivot"
+            if ipiv_match(gip[b], rf.ipiv[b], rf.gap[b], thr=max(tie_gap(dtype, n), res))[0]:
+                return "gap_under_100nu"
+            return None
+        strict_fail = len(rep.ipiv_fail)
+        kinds_ex = [undetermined(b) for b in rep.ipiv_fail]
+        rep.ipiv_fail = [b for b, kx in zip(rep.ipiv_fail, kinds_ex) if kx is None]
+        for kx in kinds_ex:
+            if kx is not None:
+                EXEMPT[kx] = EXEMPT.get(kx, 0) + 1
+        EXEMPT["strict_r3_g26_fail"] = EXEMPT.get("strict_r3_g26_fail", 0) + strict_fail
         if rep.info_fail or rep.ipiv_fail or rep.sign_fail or rep.logdet_fail or rep.inv_kappa_fail:
             msgs.append("invert: " + rep.summary())
         for k in ("logabsdet", "sign", "ipiv", "info"):
@@ -140,7 +157,8 @@ def main(trials=120, seed=0):
         if msgs:
             fails += 1
             print(tag, "|", " ; ".join(msgs), flush=True)
-    print(f"fuzz: {trials} trials, {fails} failing", flush=True)
+    print(f"fuzz: {trials} trials, {fails} failing; pivot divergences beyond R3/G26 and their G27 "
+          f"classification: {EXEMPT}", flush=True)
     return fails
 
 
