@@ -112,6 +112,20 @@ def profile_traffic():
     return None if best is None else float(best["dram_bytes_per_launch"])
 
 
+def c2_parity_report():
+    """Counts from the last committed every-item C2 parity run (profiles/*_c2_parity.json,
+    written by tests/test_gpu_fullsize.py::test_c2_every_item with GJ_PARITY_REPORT), so the
+    line carries how many items the R3 exemptions covered — the G26 band separately."""
+    pdir = os.path.join(ROOT, "profiles")
+    fns = sorted(f for f in os.listdir(pdir) if f.endswith("_c2_parity.json")) if os.path.isdir(pdir) else []
+    if not fns:
+        return None
+    with open(os.path.join(pdir, fns[-1])) as f:
+        d = json.load(f)
+    d["source"] = f"profiles/{fns[-1]}"
+    return d
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -801,6 +815,7 @@ def main():
                 "roofline": roof, "gpu_launches": args.steps, "clocks": clk.summary(), "e2e": e2e}
         if weak is not None:
             line["weak_scaling"] = weak
+        line["parity"] = c2_parity_report()
         if not args.no_c4 and world == 1:
             line["secondary"] = c4_measure(dev)
             line["secondary_c3"] = c3_measure(dev)

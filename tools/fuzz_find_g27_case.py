@@ -37,7 +37,7 @@ def replay(seed, trials=400):
 
 
 def main(seeds):
-    out = os.path.join(ROOT, "tests", "golden", "g27_fp32_n64_case.npz")
+    out = os.environ.get("G27_OUT", os.path.join(ROOT, "tests", "golden", "g27_fp32_n64_case.npz"))
     for seed in seeds:
         for tr, dtype, n, B, kind, tol, A in replay(seed):
             if not (dtype == np.float32 and n == 64 and kind == "int"):
