@@ -577,7 +577,7 @@ def c3_measure(dev, reps: int = 5):
 
 def run_c3(args, rank, world, local):
     """BASELINE configs[2]: 262,144 x 64 x 64 fp64 (A = P L diag(u), 1% of the items with a
-    duplicated row, seed 2), tol 1e-10 (reading G1), K2b.  Each rank inverts its own batch
+    duplicated row, seed 2), tol 1e-10 (reading G1), K2e.  Each rank inverts its own batch
     (weak scaling, no collective).  Roofline: the FP64 pipe (DFMA; 2n^3 - n^2 flops per item)
     and HBM (inputs + inverse + ipiv + det outputs)."""
     import torch

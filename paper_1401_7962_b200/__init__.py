@@ -93,6 +93,29 @@ def _ptr(t) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
+def _check_out(out, shape, dtype, device, name="out", contiguous=True, unit_col=False):
+    """A caller-provided output must match what the library writes (no silent
+    out-of-bounds writes through a raw pointer)."""
+    if out is None:
+        return
+    if tuple(out.shape) != tuple(shape) or out.dtype != dtype or out.device != device:
+        raise ValueError(f"{name} must be {dtype} {tuple(shape)} on {device}, got {out.dtype} "
+                         f"{tuple(out.shape)} on {out.device}")
+    if contiguous and not out.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if unit_col and out.dim() == 2 and out.stride(1) != 1:
+        raise ValueError(f"{name} must have unit column stride")
+
+
+def _check_square_batch(A, what="A"):
+    if not A.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if A.dim() != 3 or A.shape[1] != A.shape[2]:
+        raise ValueError(f"{what} must be [B, n, n]")
+    if not A.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+
+
 def _stream_ptr(stream) -> int:
     torch = _torch()
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -119,6 +142,9 @@ def invert_batched(A, tol: Optional[float] = None, *, out=None, inverse: bool = 
     dev = A.device
     X = None
     if inverse:
+        if out is not None and out.dim() == 2 and squeeze:
+            out = out.unsqueeze(0)
+        _check_out(out, A.shape, A.dtype, dev)
         X = out if out is not None else torch.empty_like(A)
     o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev) if ipiv else None
     o_lg = torch.empty((B,), dtype=torch.float64, device=dev) if logabsdet else None
@@ -154,6 +180,11 @@ def solve_batched(A, B, tol: Optional[float] = None, *, out=None, stream=None) -
         raise ValueError("A and B must be contiguous and of one dtype")
     bt, n, m = A.shape[0], A.shape[1], B.shape[2]
     dev = A.device
+    if B.device != dev:
+        raise ValueError("A and B must be on one device")
+    if out is not None and out.dim() == 2 and squeeze:
+        out = out.unsqueeze(0)
+    _check_out(out, B.shape, B.dtype, dev)
     X = out if out is not None else torch.empty_like(B)
     o_ipiv = torch.empty((bt, n), dtype=torch.int32, device=dev)
     o_lg = torch.empty((bt,), dtype=torch.float64, device=dev)
@@ -179,6 +210,9 @@ def solve(A, B, tol: Optional[float] = None, *, out=None, stream=None) -> "Solve
         raise ValueError("unit column stride and one dtype required")
     n, m = A.shape[0], B.shape[1]
     dev = A.device
+    if not (A.is_cuda and B.is_cuda) or B.device != dev:
+        raise ValueError("A and B must be CUDA tensors on one device")
+    _check_out(out, (n, m), A.dtype, dev, contiguous=False, unit_col=True)
     X = out if out is not None else torch.empty((n, m), dtype=A.dtype, device=dev)
     o_ipiv = torch.empty((n,), dtype=torch.int32, device=dev)
     o_lg = torch.empty((1,), dtype=torch.float64, device=dev)
@@ -212,6 +246,10 @@ def invert_batched_pivoting(A, strategy: str = "full", tol: Optional[float] = No
         raise ValueError("A must be a contiguous [B, n, n]")
     B, n = A.shape[0], A.shape[1]
     dev = A.device
+    if inverse and out is not None and out.dim() == 2 and squeeze:
+        out = out.unsqueeze(0)
+    if inverse:
+        _check_out(out, A.shape, A.dtype, dev)
     X = (out if out is not None else torch.empty_like(A)) if inverse else None
     o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev)
     o_jpiv = torch.empty((B, n), dtype=torch.int32, device=dev)
@@ -244,6 +282,7 @@ def det(A, tol: Optional[float] = None, *, stream=None) -> Result:
     squeeze = A.dim() == 2
     if squeeze:
         A = A.unsqueeze(0)
+    _check_square_batch(A)
     B, n = A.shape[0], A.shape[1]
     dev = A.device
     o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev)
@@ -268,8 +307,11 @@ def invert(A, tol: Optional[float] = None, *, out=None, stream=None) -> Result:
     torch = _torch()
     if A.dim() != 2 or A.shape[0] != A.shape[1] or A.stride(1) != 1:
         raise ValueError("A must be [n, n] with unit column stride")
+    if not A.is_cuda:
+        raise ValueError("A must be a CUDA tensor")
     n = A.shape[0]
     dev = A.device
+    _check_out(out, (n, n), A.dtype, dev, contiguous=False, unit_col=True)
     X = out if out is not None else torch.empty((n, n), dtype=A.dtype, device=dev)
     o_ipiv = torch.empty((n,), dtype=torch.int32, device=dev)
     o_lg = torch.empty((1,), dtype=torch.float64, device=dev)
@@ -297,12 +339,37 @@ def invert_batched_host(A, tol: Optional[float] = None, *, out=None, ipiv=None, 
             return t.data_ptr()
         return t.ctypes.data
     torch = _torch()
-    if hasattr(A, "dtype") and A.dtype in (torch.float32, torch.float64):
+    import numpy as np
+    if isinstance(A, torch.Tensor):
+        if A.is_cuda:
+            raise ValueError("invert_batched_host takes host tensors / arrays")
         dt = _dt(A)
+        fdt = A.dtype
+        contig = lambda t: t.is_contiguous()
+        same = lambda t, dtp: isinstance(t, torch.Tensor) and not t.is_cuda and t.dtype == dtp
+        tdt = {"i32": torch.int32, "f64": torch.float64, "i8": torch.int8}
     else:
-        import numpy as np
-        dt = GJ_F32 if A.dtype == np.float32 else GJ_F64
+        A = np.asarray(A)
+        if A.dtype == np.float32:
+            dt = GJ_F32
+        elif A.dtype == np.float64:
+            dt = GJ_F64
+        else:
+            raise TypeError(f"unsupported dtype {A.dtype} (float32 / float64)")
+        fdt = A.dtype
+        contig = lambda t: t.flags["C_CONTIGUOUS"]
+        same = lambda t, dtp: isinstance(t, np.ndarray) and t.dtype == dtp
+        tdt = {"i32": np.int32, "f64": np.float64, "i8": np.int8}
+    if A.ndim != 3 or A.shape[1] != A.shape[2] or not contig(A):
+        raise ValueError("A must be a C-contiguous [B, n, n] host array")
     B, n = A.shape[0], A.shape[1]
+    for t, name, shape, dtp in ((out, "out", (B, n, n), fdt), (ipiv, "ipiv", (B, n), tdt["i32"]),
+                                (logabsdet, "logabsdet", (B,), tdt["f64"]), (sign, "sign", (B,), tdt["i8"]),
+                                (det, "det", (B,), fdt), (info, "info", (B,), tdt["i32"])):
+        if t is None:
+            continue
+        if not same(t, dtp) or tuple(t.shape) != shape or not contig(t):
+            raise ValueError(f"{name} must be a C-contiguous host {dtp} {shape}")
     st = lib.gj_invert_batched_host(dt, n, B, ptr(A), ptr(out), ptr(ipiv), ptr(logabsdet), ptr(sign), ptr(det),
                                     ptr(info), TOL_DEFAULT if tol is None else float(tol), int(chunk))
     _check(st)

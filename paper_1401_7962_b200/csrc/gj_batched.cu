@@ -1272,62 +1272,6 @@ cudaError_t launch_blk32s_nr(const BlkSolveArgs& a, const TmaMaps& maps, cudaStr
   return launch_blk32s<8>(a, maps, s);
 }
 
-// K7 instead of K1s for n = 32 fp32 solves (GJ_SOLVE_K7=1, A/B measurement and tests)
-bool solve_force_k7() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GJ_SOLVE_K7");
-    v = (e != nullptr && atoi(e) != 0) ? 1 : 0;
-  }
-  return v == 1;
-}
-
-// K1t on/off (GJ_K1_TC=1).
-bool k1_tc() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GJ_K1_TC");
-    v = (e != nullptr && atoi(e) != 0) ? 1 : 0;
-  }
-  return v == 1;
-}
-
-// Variant of the fp32 n = 32 path: 0 = unblocked K1, 4 / 8 = K1b block size.  Fixed at
-// the best measured value; GJ_K1_BLOCK overrides it for A/B measurement only.
-int k1_block_size() {
-  static int v = -1;
-  if (v < 0) {
-    v = 4;
-    if (const char* e = getenv("GJ_K1_BLOCK")) {
-      const int t = atoi(e);
-      if (t == 0 || t == 4 || t == 8) v = t;
-    }
-  }
-  return v;
-}
-int k1_rows() {
-  static int v = -1;
-  if (v < 0) {
-    v = 2;
-    if (const char* e = getenv("GJ_K1_ROWS")) {
-      const int t = atoi(e);
-      if (t == 2 || t == 4) v = t;
-    }
-  }
-  return v;
-}
-int k1_stages() {
-  static int v = -1;
-  if (v < 0) {
-    v = 2;
-    if (const char* e = getenv("GJ_K1_STAGES")) {
-      const int t = atoi(e);
-      if (t == 1 || t == 2) v = t;
-    }
-  }
-  return v;
-}
-
 // ------------------------------------------------------------------ host side
 template <typename T, int NP, bool TMA>
 cudaError_t launch_warp(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
@@ -1366,13 +1310,8 @@ cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
     const uint64_t rows = (uint64_t)a.batch * NP;
     const int swz = TL::SPAN >= 32 ? TL::SPAN : 0;
     if constexpr (NP == 32 && sizeof(T) == 4) {
-      // K1t (tensor-core blocked update), selected by GJ_K1_TC=1 while it is being measured
-      if (full && k1_tc()) {
-        const cudaError_t e = launch_tc32(a, s);
-        if (e != cudaErrorNotSupported) return e;
-      }
       // determinant-only run: K1s without right-hand sides (no D half)
-      if (full && a.Ainv == nullptr && k1_block_size() != 0) {
+      if (full && a.Ainv == nullptr) {
         TmaMaps sm;
         if (blk32s_map(a.A, a.batch, sm)) {
           const BlkSolveArgs sa{a.batch, 0, nullptr, nullptr, a.ipiv, a.logabsdet, a.sign,
@@ -1380,18 +1319,12 @@ cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
           return launch_blk32s_nr(sa, sm, s);
         }
       }
-      // K1b (blocked): box of 32 * R rows (R matrices per warp task)
-      const int bsz = k1_block_size();
-      const int R = k1_rows();
-      if (full && aligned && rows_ok && bsz != 0) {
-        const uint32_t box_rows = 32u * R;
-        if (make_tma_map_2d(&maps.a, false, a.A, 32, rows, 128, 32, box_rows, 128) &&
-            (a.Ainv == nullptr || make_tma_map_2d(&maps.x, false, a.Ainv, 32, rows, 128, 32, box_rows, 128))) {
+      // K1b (blocked, BS = 4, two rows per lane, two TMA stages): box of 64 rows (2 matrices per warp task)
+      if (full && aligned && rows_ok) {
+        if (make_tma_map_2d(&maps.a, false, a.A, 32, rows, 128, 32, 64, 128) &&
+            (a.Ainv == nullptr || make_tma_map_2d(&maps.x, false, a.Ainv, 32, rows, 128, 32, 64, 128))) {
           if (a.Ainv == nullptr) maps.x = maps.a;
-          const bool one = k1_stages() == 1;
-          if (R == 4) return bsz == 8 ? launch_blk32<4, 8, 1>(a, maps, s) : launch_blk32<4, 4, 1>(a, maps, s);
-          if (bsz == 8) return one ? launch_blk32<2, 8, 1>(a, maps, s) : launch_blk32<2, 8, 2>(a, maps, s);
-          return one ? launch_blk32<2, 4, 1>(a, maps, s) : launch_blk32<2, 4, 2>(a, maps, s);
+          return launch_blk32<2, 4, 2>(a, maps, s);
         }
       }
     }
@@ -1419,7 +1352,7 @@ cudaError_t dispatch_np(const BatchedArgs& a, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_blk32_solve(const SolveArgs& a, cudaStream_t s) {
-  if (a.n != 32 || a.m < 1 || a.m > 8 || solve_force_k7()) return cudaErrorNotSupported;
+  if (a.n != 32 || a.m < 1 || a.m > 8) return cudaErrorNotSupported;
   TmaMaps maps;
   if (!blk32s_map(a.A, a.batch, maps)) return cudaErrorNotSupported;
   const BlkSolveArgs sa{a.batch, a.m, static_cast<const float*>(a.B), static_cast<float*>(a.X), a.ipiv,

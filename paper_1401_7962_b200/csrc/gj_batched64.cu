@@ -380,32 +380,13 @@ cudaError_t dispatch64(const BatchedArgs& a, cudaStream_t s) {
   return launch64<T, false>(a, maps, s);
 }
 
-// fp64 n = 64: 3 = K2e (one warp per matrix, shared-memory resident; default, C3 14.1 ms),
-// 2 = K2d (DMMA blocked update, matrix in four warps' registers; 18.7 ms), 1 = column-split
-// blocked K2b (20.7 ms), 0 = K2 (GJ_K2_VARIANT overrides for A/B measurement)
-int k2_variant() {
-  static int v = -1;
-  if (v < 0) {
-    v = 3;
-    if (const char* e = getenv("GJ_K2_VARIANT")) {
-      v = atoi(e);
-      if (v < 0 || v > 3) v = 1;
-    }
-  }
-  return v;
-}
-
 }  // namespace
 
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s) {
   if (a.batch == 0) return cudaSuccess;
-  if (dt == GJ_F64 && a.n == 64 && k2_variant() == 3) return launch_batched64e(a, s);
-  if (dt == GJ_F64 && a.n == 64 && k2_variant() == 2) {
-    const cudaError_t e = launch_batched64d(a, s);
-    if (e != cudaErrorNotSupported) return e;
-  }
-  if (dt == GJ_F64 && a.n == 64 && k2_variant() >= 1) {
-    const cudaError_t e = launch_batched64b(a, s);
+  if (dt == GJ_F64 && a.n == 64) {
+    // K2e (gj_batched64e.cu); an unaligned batch falls back to the generic K2 below
+    const cudaError_t e = launch_batched64e(a, s);
     if (e != cudaErrorNotSupported) return e;
   }
   return dt == GJ_F32 ? dispatch64<float>(a, s) : dispatch64<double>(a, s);

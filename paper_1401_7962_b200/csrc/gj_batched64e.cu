@@ -1,21 +1,25 @@
-// K2d — batched Gauss–Jordan for fp64 n = 64 (BASELINE configs[2], C3) with the blocked
-// trailing update on the FP64 tensor pipe (DMMA, mma.sync m8n8k4 f64).
+// K2e — the C3 hot path (BASELINE configs[2]): batched Gauss–Jordan for fp64 n = 64, one
+// warp per matrix, the matrix resident in SHARED MEMORY, the blocked trailing update on the
+// FP64 tensor pipe (DMMA, mma.sync m8n8k4 f64).
 //
-// One matrix per CTA of four warps.  The matrix lives in REGISTERS as DMMA accumulator
-// fragments: warp w owns rows 16w .. 16w + 15 (two 8-row tiles) x all 64 columns (eight
-// 8-column tiles); lane (g = lane / 4, t = lane % 4) holds C[g][2t, 2t + 1] of every tile.
 // The elimination (§2, Eqs. (14)-(15), L61-L72; Obs. 2-3 L59-L60; listing
-// L150-L177) runs in blocks of BS = 8 pivot steps, the aggregation K1b / K2b use:
-//   1. the block's 8 panel columns go to shared memory; warp 0 factors them (8 pivot
-//      steps: max |x_ik| over the un-pivoted rows, ties to the smallest physical position —
-//      reading G3 —, logical swaps, deferred normalisation, the pivot row's own compact
-//      entry held as W - S = 0) and writes back W - S and the block's record;
-//   2. every warp takes its rows' W - S back into the panel tile and publishes the rows it
-//      holds that were pivoted in this block (their values at the block's start) as R;
-//   3. every warp applies X[:, ~panel] += (W - S) R with DMMA: 2 x 7 x 2 = 28 m8n8k4 per
-//      warp per block (the FP64 tensor rate equals the FP64 FMA rate on B200, but one
-//      instruction does 256 FMAs, which frees the issue slots the per-step chain needs).
-// The un-permutation (L179-L198) and the deferred pivot-row scale happen in the store.
+// L150-L177) runs in blocks of BS = 8 pivot steps, the aggregation K1b uses:
+//   1. the warp loads the block's 8 panel columns (rows lane, lane + 32) into registers and
+//      factors them: max |x_ik| over the un-pivoted rows (fp64 keys: high word, then low
+//      word), ties to the smallest physical position (reading G3), logical swaps, deferred
+//      normalisation, the pivot row's own compact entry held as W - S = 0; the pivot row's
+//      panel values travel through a small shared buffer (one writer, broadcast reads,
+//      buffered by step parity) and 1/|p| starts from the winning key before the winner is
+//      known; W - S goes back to shared memory with the block's record;
+//   2. X[:, ~panel] += (W - S) R tile by tile: per 8-column tile the two B fragments are
+//      read from the block's pivot rows (before the tile is written, so no copy of R), then
+//      the eight m-tiles' C fragments go LDS.128 -> 2 DMMA -> STS.128.
+// Layout: row stride 64 doubles with the 16-byte chunk index XOR f(row), f = ((row & 1) << 2)
+// | ((row >> 1) & 3) — the panel's column access (8 rows per LDS.128 phase) and the
+// accumulator-fragment access (rows 2p, 2p + 1 x 4 lanes per phase) both hit 8 distinct
+// chunks.  A matrix costs ~34 KB of shared memory and 32 threads, so six run per SM.
+// The un-permutation (L179-L198) and the deferred pivot-row scale happen in the store, and
+// the next matrix's rows are loaded under this one's store.
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
@@ -32,28 +36,13 @@ using namespace rowops;
 
 constexpr int N64 = 64;
 constexpr int BSD = 8;             // block size = one 8-column tile
-constexpr int kWarpsD = 4;
-constexpr int PS = BSD + 2;        // panel buffer row stride (doubles): conflict-reduced reads
 #ifndef GJ_K2E_PSTORE
 #define GJ_K2E_PSTORE 1            // K2e pivot-row publish as predicated stores, no selects (12.04 -> 11.23 ms)
 #endif
 #ifndef GJ_K2E_PHASED
 #define GJ_K2E_PHASED 0            // loads / DMMA k0 / DMMA k1 / stores in phases: measured equal, off
 #endif
-#ifndef GJ_K2D_MINB
-#define GJ_K2D_MINB 4              // resident CTAs per SM the registers are sized for (build option)
-#endif
 
-struct SmemD {
-  static constexpr int PANEL = 0;                          // [64][PS] panel values, then W - S
-  static constexpr int R = PANEL + N64 * PS * 8;           // [8][64] the block's pivot rows
-  static constexpr int BS = R + BSD * N64 * 8;             // [64] int: block step of a row pivoted in the block, or -1
-  static constexpr int REC = BS + N64 * 4;                 // [64] (p, q) per step (16 B)
-  static constexpr int ROW = REC + N64 * 16;               // [64] int: row pivoted at step k
-  static constexpr int POS = ROW + N64 * 4;                // [64] int: step at which row i was pivoted
-  static constexpr int RED = POS + N64 * 4;                // [4] u64 reduction scratch
-  static constexpr int BYTES = RED + 4 * 8;
-};
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -75,21 +64,6 @@ __device__ __forceinline__ double rcp64d(double p) {
   return fma(r, e, r);
 }
 
-#ifdef GJ_K2D_PROF
-// diagnostic build only (tools/k2d_prof.py): per-phase cycle sums of warp 0's pivot step
-// (CTA 0, lane 0)
-__device__ unsigned long long g_k2d_prof[8];
-#define K2D_T(i)                                                                          \
-  do {                                                                                    \
-    if (lane == 0 && blockIdx.x == 0) {                                                   \
-      const long long t_ = clock64();                                                     \
-      if ((i) > 0) atomicAdd(&g_k2d_prof[(i)], (unsigned long long)(t_ - t_prev));       \
-      t_prev = t_;                                                                        \
-    }                                                                                     \
-  } while (0)
-#else
-#define K2D_T(i) do { } while (0)
-#endif
 
 // Warp 0's pivot step S (static) at global step k on the panel rows lane and lane + 32.
 // SROW (K2e): |p| is the winning key itself, so 1/|p| starts before the winner is known,
@@ -99,10 +73,6 @@ template <int S, bool SROW = false>
 __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
                                              int (&bs)[2], unsigned char* rec, int* rowk, int lane,
                                              double* prow = nullptr) {
-#ifdef GJ_K2D_PROF
-  long long t_prev = 0;
-#endif
-  K2D_T(0);
   uint32_t hi[2], lo[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -126,7 +96,6 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
   const int q = (int)(win >> 6);
   const int src = (int)((win >> 1) & 31u);
   const int slot = (int)(win & 1u);
-  K2D_T(1);
   double z[BSD];
   if constexpr (SROW) {
     double* pr = prow + (S & 1) * BSD;
@@ -158,14 +127,12 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
     for (int j = 0; j < BSD; ++j) z[j] = shfl_dd(slot ? x[1][j] : x[0][j], src);
   }
   const double p = z[S];
-  K2D_T(2);
   double rp;
   if constexpr (SROW) {
     rp = p < 0.0 ? -rap : rap;   // rcp64d is odd: bit-identical to rcp64d(p)
   } else {
     rp = rcp64d(p);
   }
-  K2D_T(3);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const bool pv = pos[r] == q && kmask[r] != 0u;
@@ -179,12 +146,10 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
     pos[r] = (pos[r] == k) ? q : pos[r];   // a3: the listing's swap of positions k and q (L156-L162)
     pos[r] = pv ? k : pos[r];
   }
-  K2D_T(4);
   if (lane == 0) {
     rec_store(rec, k, p, q);
     rowk[k] = src + 32 * slot;
   }
-  K2D_T(5);
 }
 template <int S, bool SROW = false>
 __device__ __forceinline__ void d_panel_steps(const int kb, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
@@ -195,185 +160,6 @@ __device__ __forceinline__ void d_panel_steps(const int kb, double (&x)[2][BSD],
     d_panel_steps<S + 1, SROW>(kb, x, kmask, pos, bs, rec, rowk, lane, prow);
   }
 }
-
-__global__ void __launch_bounds__(kWarpsD * 32, GJ_K2D_MINB) gj_batched64d_kernel(BatchedArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_d[];
-  double* pan = reinterpret_cast<double*>(smem_d + SmemD::PANEL);
-  double* R = reinterpret_cast<double*>(smem_d + SmemD::R);
-  int* bsm = reinterpret_cast<int*>(smem_d + SmemD::BS);
-  unsigned char* rec = smem_d + SmemD::REC;
-  int* rowk = reinterpret_cast<int*>(smem_d + SmemD::ROW);
-  int* posm = reinterpret_cast<int*>(smem_d + SmemD::POS);
-  unsigned long long* red = reinterpret_cast<unsigned long long*>(smem_d + SmemD::RED);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int r0 = 16 * warp + g;   // rows r0 (tile 0) and r0 + 8 (tile 1)
-  const double* __restrict__ Ag = static_cast<const double*>(a.A);
-  double* __restrict__ Xg = static_cast<double*>(a.Ainv);
-
-  for (int64_t item = blockIdx.x; item < a.batch; item += gridDim.x) {
-    const double* Ai = Ag + item * (N64 * N64);
-    // ---- a1: the fragments straight from global memory; max |a_ij| for tau
-    double acc[2][8][2];
-    double rm = 0.0;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        const double2 v = __ldcs(reinterpret_cast<const double2*>(Ai + (r0 + 8 * mt) * N64 + 8 * nt + 2 * t));
-        acc[mt][nt][0] = v.x;
-        acc[mt][nt][1] = v.y;
-        rm = fmax(rm, fmax(fabs(v.x), fabs(v.y)));
-      }
-    {
-      const unsigned long long rb = (unsigned long long)__double_as_longlong(rm);
-      const uint32_t mh = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32));
-      const uint32_t ml = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32) == mh ? (uint32_t)rb : 0u);
-      if (lane == 0) red[warp] = ((unsigned long long)mh << 32) | ml;
-    }
-    // warp 0's pivot state: rows lane and lane + 32
-    uint32_t kmask[2] = {0xffffffffu, 0xffffffffu};   // all ones: eligible (the low key word keeps bit 31)
-    int pos[2] = {lane, lane + 32};
-    __syncthreads();
-    double tau;
-    {
-      unsigned long long m = red[0];
-#pragma unroll
-      for (int w = 1; w < kWarpsD; ++w) m = red[w] > m ? red[w] : m;
-      tau = a.tol * __longlong_as_double((long long)m);
-    }
-
-#pragma unroll 1
-    for (int kb = 0; kb < N64 / BSD; ++kb) {
-      // ---- 1. the panel tile (column tile kb) -> shared memory
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        double v0 = acc[mt][0][0], v1 = acc[mt][0][1];
-#pragma unroll
-        for (int nt = 1; nt < 8; ++nt) {
-          v0 = nt == kb ? acc[mt][nt][0] : v0;
-          v1 = nt == kb ? acc[mt][nt][1] : v1;
-        }
-        *reinterpret_cast<double2*>(pan + (r0 + 8 * mt) * PS + 2 * t) = make_double2(v0, v1);
-      }
-      __syncthreads();
-      // ---- warp 0 factors the panel: BS pivot steps
-      if (warp == 0) {
-        double x[2][BSD];
-        int bs[2] = {-1, -1};
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int j = 0; j < BSD; j += 2) {
-            const double2 v = *reinterpret_cast<const double2*>(pan + (lane + 32 * r) * PS + j);
-            x[r][j] = v.x;
-            x[r][j + 1] = v.y;
-          }
-        d_panel_steps<0>(kb * BSD, x, kmask, pos, bs, rec, rowk, lane);
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-#pragma unroll
-          for (int j = 0; j < BSD; j += 2)
-            *reinterpret_cast<double2*>(pan + (lane + 32 * r) * PS + j) = make_double2(x[r][j], x[r][j + 1]);
-          bsm[lane + 32 * r] = bs[r];
-        }
-      }
-      __syncthreads();
-      // ---- 2. W - S back into the panel tile; A fragments; publish this warp's pivot rows
-      double af[2][2];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const double2 w2 = *reinterpret_cast<const double2*>(pan + (r0 + 8 * mt) * PS + 2 * t);
-        af[mt][0] = pan[(r0 + 8 * mt) * PS + t];       // A[g][t]     (k4 step 0)
-        af[mt][1] = pan[(r0 + 8 * mt) * PS + 4 + t];   // A[g][4 + t] (k4 step 1)
-        const int br = bsm[r0 + 8 * mt];
-        if (br >= 0) {   // the row's values at the block's start, all tiles but the panel
-#pragma unroll
-          for (int nt = 0; nt < 8; ++nt)
-            *reinterpret_cast<double2*>(R + br * N64 + 8 * nt + 2 * t) =
-                nt == kb ? make_double2(0.0, 0.0) : make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-        }
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-          acc[mt][nt][0] = nt == kb ? w2.x : acc[mt][nt][0];
-          acc[mt][nt][1] = nt == kb ? w2.y : acc[mt][nt][1];
-        }
-      }
-      __syncthreads();
-      // ---- 3. X[:, ~panel] += (W - S) R on the FP64 tensor pipe
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        if (nt == kb) continue;
-        const double b0 = R[t * N64 + 8 * nt + g];         // B[t][g]     (k4 step 0)
-        const double b1 = R[(4 + t) * N64 + 8 * nt + g];   // B[4 + t][g] (k4 step 1)
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt][0], b0);
-          dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt][1], b1);
-        }
-      }
-    }
-
-    // ---- a6: det / ipiv / singular flag from the record (warp 0: steps lane, lane + 32)
-    if (warp == 0) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) posm[lane + 32 * r] = pos[r];
-      unsigned fb0 = 0, fb1 = 0;
-      int nswap = 0, nneg = 0;
-      double lg = 0.0;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int k = lane + 32 * r;
-        double pk;
-        int qk;
-        rec_load(rec, k, pk, qk);
-        const unsigned fb = __ballot_sync(0xffffffffu, fabs(pk) <= tau);
-        if (r == 0) fb0 = fb; else fb1 = fb;
-        nswap += __popc(__ballot_sync(0xffffffffu, qk != k));
-        nneg += __popc(__ballot_sync(0xffffffffu, pk < 0.0));
-        lg += log(fabs(pk));
-        if (a.ipiv) a.ipiv[item * N64 + k] = qk + 1;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
-      const int info = fb0 ? __ffs(fb0) : (fb1 ? 32 + __ffs(fb1) : 0);
-      const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
-      if (lane == 0) {
-        if (a.info) a.info[item] = info;
-        if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
-        if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
-        if (a.det) static_cast<double*>(a.det)[item] = info ? 0.0 : (double)(sgn * exp(lg));
-      }
-    }
-    __syncthreads();
-    // ---- a7 + a8: Ainv[pos(i)][row(k)] = X[i][k] / p_pos(i) (+ 1 / p on the own entry)
-    if (Xg != nullptr) {
-      double* Xi = Xg + item * (N64 * N64);
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int row = r0 + 8 * mt;
-        const int ps = posm[row];
-        double pown;
-        int qd;
-        rec_load(rec, ps, pown, qd);
-        const double rp = 1.0 / pown;
-        double* orow = Xi + (int64_t)ps * N64;
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = 8 * nt + 2 * t + e;
-            const int oc = rowk[c];
-            const double v = acc[mt][nt][e] * rp + (c == ps ? rp : 0.0);
-            __stcs(orow + oc, v);
-          }
-      }
-    }
-    __syncthreads();   // the shared record / positions are rewritten by the next matrix
-  }
-}
-
 
 // ------------------------------------------------------------------ K2e: one warp per matrix
 // The same blocked elimination with the matrix resident in SHARED MEMORY (row stride 66
@@ -620,30 +406,12 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
 
 }  // namespace
 
-cudaError_t launch_batched64d(const BatchedArgs& a, cudaStream_t s) {
-  if (a.n != N64 || a.batch <= 0) return cudaErrorInvalidValue;
-  if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (a.Ainv && (reinterpret_cast<uintptr_t>(a.Ainv) & 15)))
-    return cudaErrorNotSupported;
-  const int smem = SmemD::BYTES;
-  static unsigned long long configured = 0;
-  const unsigned long long dbit = device_bit();
-  if (!(configured & dbit)) {
-    cudaError_t e = cudaFuncSetAttribute(gj_batched64d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured |= dbit;
-  }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_batched64d_kernel, kWarpsD * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t cap = (int64_t)device_sm_count() * per_sm;
-  const int grid = (int)(a.batch < cap ? a.batch : cap);
-  gj_batched64d_kernel<<<grid, kWarpsD * 32, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
   if (a.n != N64 || a.batch <= 0) return cudaErrorInvalidValue;
+  // 16-byte vector loads / stores of A and the inverse (__ldcs double2): an 8-byte-aligned
+  // batch (e.g. a 1-D buffer sliced at an odd element) goes to the generic K2 instead
+  if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (a.Ainv && (reinterpret_cast<uintptr_t>(a.Ainv) & 15)))
+    return cudaErrorNotSupported;
   const int smem = SmemE::BYTES;
   static unsigned long long configured = 0;
   const unsigned long long dbit = device_bit();
@@ -664,14 +432,3 @@ cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
 
 }  // namespace gj
 
-#ifdef GJ_K2D_PROF
-extern "C" int gj_debug_k2d_prof(unsigned long long* out8, int reset) {
-  cudaDeviceSynchronize();
-  if (cudaMemcpyFromSymbol(out8, gj::g_k2d_prof, 8 * sizeof(unsigned long long)) != cudaSuccess) return -1;
-  if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(gj::g_k2d_prof, z, sizeof(z));
-  }
-  return 0;
-}
-#endif

@@ -24,11 +24,9 @@ struct BatchedArgs {
 // Return cudaSuccess or the launch error.
 cudaError_t launch_batched(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
 cudaError_t launch_batched64(gj_dtype dt, const BatchedArgs& a, cudaStream_t s);
-// K2b, fp64 n = 64 (gj_batched64b.cu); cudaErrorNotSupported if the buffers do not suit it.
-cudaError_t launch_batched64b(const BatchedArgs& a, cudaStream_t s);
-// K2d, fp64 n = 64 with the DMMA blocked update (gj_batched64d.cu).
-cudaError_t launch_batched64d(const BatchedArgs& a, cudaStream_t s);
-cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s);   // K2e (one warp per matrix, shared-memory resident)
+// K2e, fp64 n = 64 (gj_batched64e.cu: one warp per matrix, shared-memory resident, DMMA
+// blocked update); cudaErrorNotSupported for a batch that is not 16-byte aligned.
+cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s);
 // K7, multi-RHS solve X = A^-1 B, n <= 32, m <= 32 (gj_solve.cu).
 struct SolveArgs {
   int n, m;             // order, right-hand sides
@@ -55,9 +53,6 @@ cudaError_t solve_large_f32(int n, int m, const float* A, int64_t lda, const flo
 cudaError_t solve_large_f64(int n, int m, const double* A, int64_t lda, const double* B, int64_t ldb, double* Xs,
                             int64_t ldx, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
                             void* ws, cudaStream_t s);
-// K1t, fp32 n = 32 with the blocked update on tcgen05 (gj_batched_tc.cu); cudaErrorNotSupported
-// if the buffers do not suit TMA.
-cudaError_t launch_tc32(const BatchedArgs& a, cudaStream_t s);
 // K6, n <= 32 (gj_fullpiv.cu): strategy 2 = full pivoting, 1 = partial, 0 = none; jpiv may be null.
 cudaError_t launch_batched_strategy(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, int strategy, cudaStream_t s);
 

@@ -2,12 +2,14 @@
 // of the per-step rank-1 updates of Eqs. (14)-(15):
 //
 //   for each panel P of b = 128 columns:
-//     for each leaf L of W columns inside P:
+//     for each leaf L of W columns inside P (W = 32, 16, 8, 4 for n <= 8192 / 16384 / 32768 / 65536):
 //       K3  leaf factorisation: W pivot steps (a2-a5) over ALL n rows but only the W leaf
-//           columns, by one thread-block cluster (8 or 16 CTAs x 1024 threads; every
-//           thread holds its rows' W values in registers; per step a CTA argmax, a
-//           DSMEM exchange of the CTA winners and one cluster barrier);
-//       K4  update the panel columns right of L:  X[:,T] += (W_L - S_L) R_L
+//           columns, by one thread-block cluster of 16 CTAs x 512 threads (every thread
+//           holds its rows' W values in registers; per step a warp redux argmax, a CTA
+//           winner among the warp winners, and one cp.async.bulk DSMEM copy of the CTA
+//           winner into every CTA of the cluster, completing on that CTA's mbarrier — no
+//           cluster barrier per step);
+//       the rest of P's columns right of L:  X[:,T] += (W_L - S_L) R_L  (inside K3)
 //     K4  trailing update of all columns outside P:  X[:,~P] += (W_P - S_P) R_P
 //   K5  un-permutation: Ainv[k][j] = X[perm[k]][step(j)]       (listing L179-L198)
 //   K6  log|det|, sign, singular flag, ipiv from the per-step record (Eq. (13), Obs. 2)
@@ -19,8 +21,9 @@
 // W = E S = S + (S - C) A11^-1, so E v = v + (W - S) v[S].
 //
 // K4 is an FP64 tensor-core GEMM: mma.sync.m16n8k16.f64 (SASS DMMA; tcgen05 has no f64
-// kind on sm_100a), 128x128 CTA tiles, 8 warps of 64x32, cp.async double-buffered
-// 16-deep K slabs.  Pivoting is logical (rows never move); ties go to the smallest
+// kind on sm_100a), 128x64 CTA tiles, 4 warps of 64x32, cp.async double-buffered K slabs,
+// persistent grid, launched with programmatic stream serialisation so that the next
+// panel's K3 runs beside it (look-ahead).  Pivoting is logical (rows never move); ties go to the smallest
 // physical position of the listing's swapped array (reading G3), so ipiv equals
 // LAPACK getrf's.  n is padded to a multiple of 32 with an identity block.
 #include <cuda.h>
@@ -88,10 +91,11 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ld, con
 // Ainv[k][j] = X[perm[k]][pivstep[j]]  (k, j < n); perm[k] = row pivoted at step k
 __global__ void unpermute_kernel(const double* __restrict__ X, int npad, const int* __restrict__ rec_row,
                                  const int* __restrict__ pivstep, int n, double* __restrict__ Y, int64_t ldy) {
-  const int k = blockIdx.y;
-  const double* src = X + (int64_t)rec_row[k] * npad;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-    Y[(int64_t)k * ldy + j] = src[pivstep[j]];
+  for (int k = blockIdx.y; k < n; k += gridDim.y) {   // gridDim.y <= 65535 < GJ_LARGE_MAX_N
+    const double* src = X + (int64_t)rec_row[k] * npad;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+      Y[(int64_t)k * ldy + j] = src[pivstep[j]];
+  }
 }
 
 // log|det|, sign, singular flag and ipiv from the per-step record (Eq. (13), Obs. 2, G4)
@@ -855,17 +859,21 @@ static bool leaf_cfg(int npad, LeafCfg* c) {
   return false;
 }
 
-static bool debug_sync() {
-  static int v = -1;
-  if (v < 0) v = getenv("GJ_DEBUG_SYNC") != nullptr ? 1 : 0;
-  return v == 1;
+// Diagnostic builds only (-DGJ_DEBUG_SYNC: synchronise and check after every launch;
+// -DGJ_LARGE_NO_PDL: no overlap of the trailing update with the next panel).
+static constexpr bool debug_sync() {
+#ifdef GJ_DEBUG_SYNC
+  return true;
+#else
+  return false;
+#endif
 }
-// GJ_LARGE_NO_PDL: launch the trailing update after the next panel (no overlap) — a
-// diagnostic switch
-static bool no_pdl() {
-  static int v = -1;
-  if (v < 0) v = getenv("GJ_LARGE_NO_PDL") != nullptr ? 1 : 0;
-  return v == 1;
+static constexpr bool no_pdl() {
+#ifdef GJ_LARGE_NO_PDL
+  return true;
+#else
+  return false;
+#endif
 }
 #define GJ_DBG(name)                                                                        \
   do {                                                                                      \
@@ -952,10 +960,11 @@ __global__ void gather_split_T_f32(const float* __restrict__ X, int64_t ld, cons
 
 __global__ void unpermute_f32(const float* __restrict__ X, int npad, const int* __restrict__ rec_row,
                               const int* __restrict__ pivstep, int n, float* __restrict__ Y, int64_t ldy) {
-  const int k = blockIdx.y;
-  const float* src = X + (int64_t)rec_row[k] * npad;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-    Y[(int64_t)k * ldy + j] = src[pivstep[j]];
+  for (int k = blockIdx.y; k < n; k += gridDim.y) {
+    const float* src = X + (int64_t)rec_row[k] * npad;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+      Y[(int64_t)k * ldy + j] = src[pivstep[j]];
+  }
 }
 
 __global__ void finalize_det_f32(const double* logabsdet, const int8_t* sign, float* det) {
@@ -1054,7 +1063,7 @@ cudaError_t invert_large_f32(int n, const float* A, int64_t lda, float* Ainv, in
     GJ_DBG("f32 panel");
   }
   if (Ainv != nullptr)
-    f32::unpermute_f32<<<dim3((n + 255) / 256, n), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
+    f32::unpermute_f32<<<dim3((n + 255) / 256, n < 65535 ? n : 65535), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
   large::finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet ? logabsdet : w.lg,
                                      sign ? sign : w.sg, nullptr, info);
   if (det != nullptr)
@@ -1101,9 +1110,10 @@ __global__ void copy_pad_solve_f32(const float* __restrict__ A, int64_t lda, con
 }
 __global__ void solve_gather_f32(const float* __restrict__ X, int ld, int npad, const int* __restrict__ rec_row, int n,
                                  int m, float* __restrict__ Xs, int64_t ldx) {
-  const int k = blockIdx.y;
-  const float* src = X + (int64_t)rec_row[k] * ld + npad;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) Xs[(int64_t)k * ldx + j] = src[j];
+  for (int k = blockIdx.y; k < n; k += gridDim.y) {
+    const float* src = X + (int64_t)rec_row[k] * ld + npad;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) Xs[(int64_t)k * ldx + j] = src[j];
+  }
 }
 }  // namespace f32
 
@@ -1174,7 +1184,7 @@ cudaError_t solve_large_f32(int n, int m, const float* A, int64_t lda, const flo
     const bool pdl = nxt && !large::no_pdl();
     if ((e = launch_tc_update(gb, pdl ? sms - lc.cl : 0, pdl, s)) != cudaSuccess) return e;
   }
-  f32::solve_gather_f32<<<dim3((m + 127) / 128, n), 128, 0, s>>>(w.X, ld, npad, w.rec_row, n, m, Xs, ldx);
+  f32::solve_gather_f32<<<dim3((m + 127) / 128, n < 65535 ? n : 65535), 128, 0, s>>>(w.X, ld, npad, w.rec_row, n, m, Xs, ldx);
   large::finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet ? logabsdet : w.lg,
                                      sign ? sign : w.sg, nullptr, info);
   return cudaGetLastError();
@@ -1238,7 +1248,7 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
     GJ_DBG("trailing gemm");
   }
   if (Ainv != nullptr)
-    unpermute_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
+    unpermute_kernel<<<dim3((n + 255) / 256, n < 65535 ? n : 65535), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
   finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet, sign, det, info);
   return cudaGetLastError();
 }
@@ -1275,9 +1285,10 @@ __global__ void copy_pad_solve_kernel(const double* __restrict__ A, int64_t lda,
 // Xs[k][j] = X[rec_row[k]][npad + j]
 __global__ void solve_gather_kernel(const double* __restrict__ X, int ld, int npad, const int* __restrict__ rec_row,
                                     int n, int m, double* __restrict__ Xs, int64_t ldx) {
-  const int k = blockIdx.y;
-  const double* src = X + (int64_t)rec_row[k] * ld + npad;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) Xs[(int64_t)k * ldx + j] = src[j];
+  for (int k = blockIdx.y; k < n; k += gridDim.y) {
+    const double* src = X + (int64_t)rec_row[k] * ld + npad;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) Xs[(int64_t)k * ldx + j] = src[j];
+  }
 }
 }  // namespace large
 
@@ -1338,7 +1349,7 @@ cudaError_t solve_large_f64(int n, int m, const double* A, int64_t lda, const do
     GemmArgs gb{w.X + P0, ld, w.R, ld, w.X, ld, npad, ld - P1 - pw1, pw, w.pivstep, P0, P0 + pw, 0, P1 + pw1};
     if ((e = launch_gemm(gb, s, pw1 > 0 ? sms - lc.cl : 0, pw1 > 0 && !debug_sync())) != cudaSuccess) return e;
   }
-  solve_gather_kernel<<<dim3((m + 127) / 128, n), 128, 0, s>>>(w.X, ld, npad, w.rec_row, n, m, Xs, ldx);
+  solve_gather_kernel<<<dim3((m + 127) / 128, n < 65535 ? n : 65535), 128, 0, s>>>(w.X, ld, npad, w.rec_row, n, m, Xs, ldx);
   finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet, sign, nullptr, info);
   return cudaGetLastError();
 }
