@@ -31,7 +31,12 @@ def _worker(rank, P, n, kind, port, outdir):
     torch.cuda.set_device(0)
     tdist.init_process_group("gloo", rank=rank, world_size=P, init_method=f"tcp://127.0.0.1:{port}")
     try:
-        A = synth.gen_gaussian(n, seed=70 + n) if kind == "gauss" else synth.hadamard_pd(n, seed=5)[0]
+        if kind == "gauss":
+            A = synth.gen_gaussian(n, seed=70 + n)
+        elif kind == "c5gen":
+            A = synth.gen_gaussian(n, seed=4)      # the C5 generator (N(0,1)/sqrt(n), seed 4)
+        else:
+            A = synth.hadamard_pd(n, seed=5)[0]
         cols = local_columns(n, P, rank)
         A_local = torch.from_numpy(np.ascontiguousarray(A[:, cols])).cuda()
         r = invert_dist(A_local, n)
@@ -89,3 +94,28 @@ def test_dist_hadamard_exact(P):
     A = synth.hadamard_pd(n, seed=5)[0]
     assert np.array_equal(X, A.T / n)
     assert abs(lg - (n / 2) * np.log(n)) <= 1e-9
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_dist_c5_generator_n8192_vs_stored_oracle(P):
+    """oracle parity of the distributed code at n = 8192 on the C5 generator
+    (seed 4): ipiv (R3), log|det| and sign (R4/R5), 64 sampled rows of the inverse (R1 kappa
+    rule) and their residual (R2), against tests/golden/c4_oracle_ref_n8192_s4.npz (written by
+    tools/make_c4_reference.py 8192 4: the long-double oracle, 1,174 s on 8 cores)."""
+    from tests.parity import TOL_RES, ipiv_match
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "c4_oracle_ref_n8192_s4.npz"))
+    n = int(ref["n"])
+    assert n == 8192 and int(ref["seed"]) == 4
+    X, lg, sg, info, ipiv = run_dist(P, n, kind="c5gen")
+    assert info == 0
+    ok, _ = ipiv_match(ipiv, ref["ipiv"], ref["gap"])
+    assert ok
+    kappa = float(ref["kappa_inf"])
+    rows = ref["rows"]
+    e = np.abs(X[rows] - ref["inv_rows"]).max() / np.abs(ref["inv_rows"]).max()
+    print(f"dist P={P} n=8192 seed 4: sampled-row rel err {e:.3e}, kappa_inf {kappa:.3e}")
+    assert e <= max(1e-10, kappa * 2.0 ** -52)
+    assert sg == int(ref["sign"])
+    assert abs(lg - float(ref["logabsdet"])) <= max(1e-10, kappa * 2.0 ** -52)
+    A = synth.gen_gaussian(n, seed=4)
+    assert oracle.residual(A, X, rows=rows) <= TOL_RES[np.float64]
