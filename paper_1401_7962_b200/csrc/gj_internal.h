@@ -56,6 +56,39 @@ cudaError_t solve_large_f64(int n, int m, const double* A, int64_t lda, const do
 // K6, n <= 32 (gj_fullpiv.cu): strategy 2 = full pivoting, 1 = partial, 0 = none; jpiv may be null.
 cudaError_t launch_batched_strategy(gj_dtype dt, const BatchedArgs& a, int32_t* jpiv, int strategy, cudaStream_t s);
 
+// K4b (gj_dgemm.cu): the K = 128 trailing update on the FP64 tensor pipe, TMA-fed and
+// warp-specialised.  C[i][c] = (replace(i) ? 0 : C[i][c]) + sum_s X[i][a_col0 + s] RT[c][s]
+// for i < M and the N compact columns c (c_base + nc, shifted past [skip_lo, skip_hi)).
+struct DgemmArgs {
+  const double* X;      // A = X[:, a_col0 .. a_col0 + K), row stride ldx; X is x_rows x x_cols
+  int64_t ldx;
+  int x_rows, x_cols, a_col0;
+  const double* RT;     // B^T: RT[c][s], row stride K (= 128), rt_rows rows
+  int rt_rows;
+  double* C;            // row stride ldc, real column index
+  int64_t ldc;
+  int M, N, K;
+  int c_base, skip_lo, skip_hi;
+  const int* pivstep;   // replace(i) = pivstep[i] in [rep_lo, rep_hi)
+  int rep_lo, rep_hi;
+};
+bool dgemm_tma_supported(const DgemmArgs& g);
+// cudaErrorNotSupported if the arguments do not suit it (the caller falls back to K4).
+// grid_sms: CTAs (one per SM; 0: every SM); each takes a contiguous range of the tiles.
+cudaError_t launch_dgemm_tma(const DgemmArgs& g, int grid_sms, bool pdl, cudaStream_t s);
+#ifdef GJ_TIMELINE
+// diagnostic builds only (%globaltimer ns): gj_large.cu keeps per panel k [0] leaf start,
+// [1] leaf end; gj_dgemm.cu [0] trailing-update first CTA start, [1] its end, [2] its last CTA start
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+#ifndef GJ_DGEMM_CW
+#define GJ_DGEMM_CW 8
+#endif
+
 // Large-n blocked path (gj_large.cu), fp64, one matrix; Ainv may be null (det only).
 size_t large_workspace_size(int n);
 cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, int64_t ldainv, int32_t* ipiv,

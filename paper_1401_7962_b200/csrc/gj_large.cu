@@ -38,6 +38,9 @@
 #include "gj_ptx.cuh"
 
 namespace gj {
+#ifdef GJ_TIMELINE
+__device__ unsigned long long g_tl[2][512];
+#endif
 namespace large {
 
 using namespace ptx;
@@ -86,6 +89,23 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ld, con
   double2* dst = reinterpret_cast<double2*>(R + (int64_t)s * ld + c_lo);
   const int m = (c_hi - c_lo) / 2;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) dst[j] = src[j];
+}
+
+// RT[c][s] = X[rows[s]][c] for s < 128, c < ncols (the pivot rows transposed, K-major, for
+// K4b's B operand); 32 x 32 tiles through shared memory, grid (ceil(ncols / 32), 4), block (32, 8)
+__global__ void gather_rows_T_kernel(const double* __restrict__ X, int64_t ld, const int* __restrict__ rows, int ncols,
+                                     double* __restrict__ RT) {
+  __shared__ double tile[32][33];
+  const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = c < ncols ? X[(int64_t)rows[s0 + i] * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i;
+    if (c < ncols) RT[(int64_t)c * 128 + s0 + threadIdx.x] = tile[threadIdx.x][i];
+  }
 }
 
 // Ainv[k][j] = X[perm[k]][pivstep[j]]  (k, j < n); perm[k] = row pivoted at step k
@@ -320,6 +340,9 @@ __device__ unsigned long long g_leaf_prof[8];
 template <typename T, int W, int RPT>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef GJ_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && a.c0 % 128 == 0) g_tl[0][a.c0 / 128] = gtime();
+#endif
   using LS = LeafSmem<T, W>;
   constexpr int EXW = LS::EXW;
   constexpr int KEYT = LS::KEYT;
@@ -568,6 +591,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     }
   }
   cluster_sync_all();   // no CTA leaves while a peer's bulk copy may still target it
+#ifdef GJ_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && a.c0 % 128 == 0) g_tl[1][a.c0 / 128] = gtime();
+#endif
 }
 
 // ============================================================================ K4: GEMM update
@@ -1230,21 +1256,49 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
     const int pw = width(P0);
     const int P1 = P0 + pw;
     const int pw1 = P1 < npad ? width(P1) : 0;
-    gather_rows_kernel<<<dim3((npad / 2 + 255) / 256, pw), 256, 0, s>>>(w.X, npad, w.rec_row + P0, pw, w.R, 0, npad);
+    // K4b (TMA-fed DMMA GEMM) takes full 128-column panels; a narrower last panel uses K4
+    DgemmArgs d{w.X, npad, npad, npad, P0, w.R, npad, w.X, npad, npad, 0, pw, 0, 0, 0, w.pivstep, P0, P0 + pw};
+    const bool tma_gemm = pw == PANEL && dgemm_tma_supported(d);
+    if (tma_gemm)
+      gather_rows_T_kernel<<<dim3((npad + 31) / 32, PANEL / 32), dim3(32, 8), 0, s>>>(w.X, npad, w.rec_row + P0, npad, w.R);
+    else
+      gather_rows_kernel<<<dim3((npad / 2 + 255) / 256, pw), 256, 0, s>>>(w.X, npad, w.rec_row + P0, pw, w.R, 0, npad);
     if (pw1 > 0) {
-      GemmArgs ga{w.X + P0, npad, w.R + P1, npad, w.X + P1, npad, npad, pw1, pw, w.pivstep, P0, P0 + pw, 0, 0};
-      if ((e = launch_gemm(ga, s)) != cudaSuccess) return e;
+      if (tma_gemm) {
+        DgemmArgs da = d;
+        da.N = pw1;
+        da.c_base = P1;
+        if ((e = launch_dgemm_tma(da, 0, false, s)) != cudaSuccess) return e;
+      } else {
+        GemmArgs ga{w.X + P0, npad, w.R + P1, npad, w.X + P1, npad, npad, pw1, pw, w.pivstep, P0, P0 + pw, 0, 0};
+        if ((e = launch_gemm(ga, s)) != cudaSuccess) return e;
+      }
       GJ_DBG("look-ahead gemm");
       if ((e = factor_panel(P1, pw1)) != cudaSuccess) return e;
     }
     // every column outside panels k and k+1 (the D columns on the left included)
-    GemmArgs gb{w.X + P0, npad, w.R, npad, w.X, npad, npad, npad - pw - pw1, pw, w.pivstep, P0, P0 + pw, P0, P1 + pw1};
-    if (det_only) {   // only the columns right of panel k+1
-      gb.N = npad - P1 - pw1;
-      gb.skip_lo = 0;
-      gb.skip_hi = P1 + pw1;
+    const int grid_sms = pw1 > 0 ? sms - lc.cl : 0;
+    const bool pdl = pw1 > 0 && !debug_sync();
+    if (tma_gemm) {
+      DgemmArgs db = d;
+      db.N = npad - pw - pw1;
+      db.c_base = 0;
+      db.skip_lo = P0;
+      db.skip_hi = P1 + pw1;
+      if (det_only) {   // only the columns right of panel k+1
+        db.N = npad - P1 - pw1;
+        db.skip_lo = 0;
+      }
+      if ((e = launch_dgemm_tma(db, grid_sms, pdl, s)) != cudaSuccess) return e;
+    } else {
+      GemmArgs gb{w.X + P0, npad, w.R, npad, w.X, npad, npad, npad - pw - pw1, pw, w.pivstep, P0, P0 + pw, P0, P1 + pw1};
+      if (det_only) {   // only the columns right of panel k+1
+        gb.N = npad - P1 - pw1;
+        gb.skip_lo = 0;
+        gb.skip_hi = P1 + pw1;
+      }
+      if ((e = launch_gemm(gb, s, grid_sms, pdl)) != cudaSuccess) return e;
     }
-    if ((e = launch_gemm(gb, s, pw1 > 0 ? sms - lc.cl : 0, pw1 > 0 && !debug_sync())) != cudaSuccess) return e;
     GJ_DBG("trailing gemm");
   }
   if (Ainv != nullptr)
@@ -1543,16 +1597,40 @@ cudaError_t dist_update(int n, int P, int rank, int k, int part, double* Xl, con
   if (part > 0 && (k + 1 >= nb || (k + 1) % P != rank)) return cudaErrorInvalidValue;
   if (nl == 0) return cudaSuccess;
   const int k0 = k * dist::DB;
-  if (part != 2)
-    gather_rows_kernel<<<dim3((nl / 2 + 255) / 256, dist::DB), 256, 0, s>>>(Xl, nl, rec_row + k0, dist::DB, R, 0, nl);
   const bool own = k % P == rank;
   const int c0 = (k / P) * dist::DB;             // local block of panel k (if owned)
   const int c1 = ((k + 1) / P) * dist::DB;       // local block of panel k+1 (if owned)
+  LeafCfg lc;
+  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
+  // K4b (TMA-fed DMMA GEMM) with the pivot rows transposed (RT, nl x 128); K4 otherwise
+  DgemmArgs d{W, dist::DB, npad, dist::DB, 0, R, nl, Xl, nl, npad, 0, dist::DB, 0, 0, 0, pivstep, k0, k0 + dist::DB};
+#ifdef GJ_NO_DGEMM_TMA
+  const bool tma_gemm = false;
+#else
+  const bool tma_gemm = dgemm_tma_supported(d);
+#endif
+  if (part != 2) {
+    if (tma_gemm)
+      gather_rows_T_kernel<<<dim3((nl + 31) / 32, dist::DB / 32), dim3(32, 8), 0, s>>>(Xl, nl, rec_row + k0, nl, R);
+    else
+      gather_rows_kernel<<<dim3((nl / 2 + 255) / 256, dist::DB), 256, 0, s>>>(Xl, nl, rec_row + k0, dist::DB, R, 0, nl);
+  }
   if (part == 1) {
+    if (tma_gemm) {
+      d.N = dist::DB;
+      d.c_base = c1;
+      return launch_dgemm_tma(d, 0, false, s);
+    }
     GemmArgs g{W, dist::DB, R + c1, nl, Xl + c1, nl, npad, dist::DB, dist::DB, pivstep, k0, k0 + dist::DB, 0, 0};
     return launch_gemm(g, s);
   }
   if (part == 0) {
+    if (tma_gemm) {
+      d.N = nl - (own ? dist::DB : 0);
+      d.skip_lo = own ? c0 : 0;
+      d.skip_hi = own ? c0 + dist::DB : 0;
+      return launch_dgemm_tma(d, 0, false, s);
+    }
     GemmArgs g{W, dist::DB, R, nl, Xl, nl, npad, nl - (own ? dist::DB : 0), dist::DB, pivstep, k0, k0 + dist::DB,
                own ? c0 : 0, own ? c0 + dist::DB : 0};
     return launch_gemm(g, s);
@@ -1564,9 +1642,13 @@ cudaError_t dist_update(int n, int P, int rank, int k, int part, double* Xl, con
     hi = (c0 > c1 ? c0 : c1) + dist::DB;
     if (hi - lo != 2 * dist::DB) return cudaErrorInvalidValue;   // only adjacent blocks (P == 1)
   }
+  if (tma_gemm) {
+    d.N = nl - (hi - lo);
+    d.skip_lo = lo;
+    d.skip_hi = hi;
+    return launch_dgemm_tma(d, device_sm_count() - lc.cl, true, s);
+  }
   GemmArgs g{W, dist::DB, R, nl, Xl, nl, npad, nl - (hi - lo), dist::DB, pivstep, k0, k0 + dist::DB, lo, hi};
-  LeafCfg lc;
-  if (!leaf_cfg(npad, &lc)) return cudaErrorInvalidValue;
   return launch_gemm(g, s, device_sm_count() - lc.cl, true);
 }
 
@@ -1612,5 +1694,18 @@ extern "C" int gj_debug_leaf_prof(unsigned long long* out8, int reset) {
     cudaMemcpyToSymbol(gj::large::g_leaf_prof, z, sizeof(z));
   }
   return 0;
+}
+#endif
+
+#ifdef GJ_TIMELINE
+extern "C" int gj_debug_timeline_gemm(unsigned long long* out, int reset);
+extern "C" int gj_debug_timeline(unsigned long long* out, int reset) {   // out: [5][512]
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, gj::g_tl, sizeof(gj::g_tl)) != cudaSuccess) return -1;
+  if (reset) {
+    static unsigned long long z[2][512];
+    cudaMemcpyToSymbol(gj::g_tl, z, sizeof(z));
+  }
+  return gj_debug_timeline_gemm(out + 2 * 512, reset);
 }
 #endif

@@ -34,4 +34,9 @@ for path in sys.argv[1:]:
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     print(f"{path}: median {np.median(ts):.2f} ms  min {min(ts):.2f}", flush=True)
+    if path == sys.argv[1]:
+        ref = (X.clone(), ip.clone())
+    else:
+        d = ((X - ref[0]).abs().max() / ref[0].abs().max()).item()
+        print(f"  vs {sys.argv[1]}: max rel diff {d:.3e}, ipiv equal {torch.equal(ip, ref[1])}", flush=True)
     del ws
