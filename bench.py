@@ -55,6 +55,8 @@ def parse():
                    help="c2: the headline batched line; c5: one fp64 32768^2 matrix, column-block-cyclic over the ranks")
     p.add_argument("--n", type=int, default=32768, help="order for --workload c5")
     p.add_argument("--no-weak", action="store_true", help="skip the weak-scaling secondary key (N > 1)")
+    p.add_argument("--dist-driver", default="library", choices=["library", "python"],
+                   help="c5: gj_invert_dist (NCCL inside libgjinv) or the dist.py schedule over torch.distributed")
     return p.parse_args()
 
 
@@ -466,7 +468,7 @@ def run_c5(args, rank, world, local):
     Rank 0 generates A and broadcasts it; every rank keeps its own columns."""
     import torch
     import torch.distributed as tdist
-    from paper_1401_7962_b200.dist import invert_dist, local_columns
+    from paper_1401_7962_b200.dist import DistContext, invert_dist, local_columns
     import synth
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -490,15 +492,19 @@ def run_c5(args, rank, world, local):
         tdist.barrier()
         torch.cuda.synchronize(dev)
 
+    # the product path: the library drives the per-panel NCCL exchange (gj_invert_dist);
+    # --dist-driver python runs the same schedule from paper_1401_7962_b200/dist.py instead
+    ctx = DistContext(device=dev) if args.dist_driver == "library" else None
+    run = (lambda: ctx.invert(A_local, n)) if ctx is not None else (lambda: invert_dist(A_local, n))
     for _ in range(args.warmup):
-        invert_dist(A_local, n)
+        run()
     times, res = [], None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            res = invert_dist(A_local, n)
+            res = run()
             b.record()
             barrier()
             times.append(a.elapsed_time(b))
@@ -515,7 +521,9 @@ def run_c5(args, rank, world, local):
                           "data": "synthetic",
                           "config": {"workload": f"C5: one fp64 {n}x{n} N(0,1)/sqrt(n), seed 4, column-block-cyclic "
                                                  f"(block 128) over {world} GPU(s) (BASELINE.json configs[4])",
-                                     "parallelism": f"column-block-cyclic x{world}, NCCL panel broadcast"},
+                                     "parallelism": f"column-block-cyclic x{world}, NCCL panel broadcast",
+                                     "driver": "gj_invert_dist (library-owned NCCL communicator)" if ctx is not None
+                                     else "paper_1401_7962_b200/dist.py over torch.distributed"},
                           "roofline": {"bound": "tensor", "achieved": tf, "peak": peak * world, "unit": "TFLOP/s",
                                        "frac": tf / (peak * world), "traffic": None, "peak_source": src + f" x {world}"},
                           "logabsdet": res.logabsdet, "sign": res.sign, "info": res.info,

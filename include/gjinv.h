@@ -221,9 +221,9 @@ gj_status gj_host_release(void);
  * on every rank, so the pivot search of a panel (the max-|a_ik| rule, Obs. 3 L60) is
  * local to the panel's owner.  The collectives are the caller's (NCCL via
  * torch.distributed in paper_1401_7962_b200/dist.py): per panel k the owner calls
- * gj_dist_factor, broadcasts W, pos, pivstep and the record of steps [k*B, (k+1)*B),
- * then every rank calls gj_dist_update; the un-permutation (listing L179-L198) is one
- * all-to-all of columns planned by gj_dist_unpermute_plan.  Same pivots, det and
+ * gj_dist_step_factor, broadcasts W, pos, pivstep and the record of steps [k*B, (k+1)*B),
+ * then every rank calls gj_dist_step_update; the un-permutation (listing L179-L198) is one
+ * all-to-all of columns planned by gj_dist_step_unpermute_plan.  Same pivots, det and
  * inverse as gj_invert (the aggregation of Eqs. (14)-(15), L61-L72, is identical).
  * All pointers are DEVICE pointers owned by the caller; work is enqueued on `stream`.
  * Replicated arrays (length npad, int32 unless stated): pos (physical position of each
@@ -244,46 +244,94 @@ gj_status gj_dist_sizes(int n, int nranks, int rank, int* npad, int* ncols_local
 /* X_local = this rank's columns of blockdiag(A, I); A_local holds the rank's ncols_local_real
  * real columns (n rows, row stride lda >= ncols_local_real).  pos/pivstep initialised;
  * *smax_bits = bit pattern of max |a_ij| over the local columns (reduce MAX over ranks
- * before gj_dist_finalize: the zero threshold of Obs. 2, L59, is relative to it, G1). */
-gj_status gj_dist_init(int n, int nranks, int rank, const double* A_local, int64_t lda, double* X_local,
+ * before gj_dist_step_finalize: the zero threshold of Obs. 2, L59, is relative to it, G1). */
+gj_status gj_dist_step_init(int n, int nranks, int rank, const double* A_local, int64_t lda, double* X_local,
                        int32_t* pos, int32_t* pivstep, uint64_t* smax_bits, void* stream);
 
 /* Owner of panel k (k % nranks == rank) only: GJ_DIST_BLOCK pivot steps (a2-a6) on the
  * panel's local columns, in place, updating pos / pivstep / rec_* and copying the
  * factored panel to W. */
-gj_status gj_dist_factor(int n, int nranks, int rank, int k, double* X_local, int32_t* pos, int32_t* pivstep,
+gj_status gj_dist_step_factor(int n, int nranks, int rank, int k, double* X_local, int32_t* pos, int32_t* pivstep,
                          double* rec_p, int32_t* rec_q, int32_t* rec_row, double* W, void* stream);
 
 /* Every rank, after the broadcast of panel k: X_local[:, c] += (W - S) R for the local
  * columns c outside panel k (R = the panel's pivot rows of X_local, staged in R).
  *   part 0: all of them (gathers R first);
  *   part 1: only the local columns of panel k+1 (gathers R first; the rank must own k+1);
- *   part 2: the rest, after part 1 and gj_dist_factor(k+1) on the same stream: launched as
+ *   part 2: the rest, after part 1 and gj_dist_step_factor(k+1) on the same stream: launched as
  *           a programmatic dependent of that factorisation so the two overlap (look-ahead).
  * Parts 1 and 2 need (k+1) % nranks == rank. */
-gj_status gj_dist_update(int n, int nranks, int rank, int k, int part, double* X_local, const double* W,
+gj_status gj_dist_step_update(int n, int nranks, int rank, int k, int part, double* X_local, const double* W,
                          const int32_t* pivstep, const int32_t* rec_row, double* R, void* stream);
 
 /* log|det|, sign, info and ipiv from the replicated record (Eq. (13) + G4); tol as
  * gj_invert (< 0: n * eps). Any rank; outputs may be NULL. */
-gj_status gj_dist_finalize(int n, const double* rec_p, const int32_t* rec_q, double tol, const uint64_t* smax_bits,
+gj_status gj_dist_step_finalize(int n, const double* rec_p, const int32_t* rec_q, double tol, const uint64_t* smax_bits,
                            int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, void* stream);
 
 /* Un-permutation plan: send_cols (<= ncols_local) = local compact columns ordered by
  * (destination rank, output column); recv_cols = local output columns ordered by
  * (source rank, output column); counts[0..P) columns sent to / counts[P..2P) received
  * from each rank. nranks <= GJ_DIST_MAX_RANKS. */
-gj_status gj_dist_unpermute_plan(int n, int nranks, int rank, const int32_t* pivstep, int32_t* send_cols,
+gj_status gj_dist_step_unpermute_plan(int n, int nranks, int rank, const int32_t* pivstep, int32_t* send_cols,
                                  int32_t* recv_cols, int32_t* counts, void* stream);
 
 /* sendbuf[t][i] = X_local[rec_row[i]][send_cols[t]], t < m, i < n (m columns of n). */
-gj_status gj_dist_unpermute_pack(int n, int nranks, int rank, const double* X_local, const int32_t* rec_row,
+gj_status gj_dist_step_unpermute_pack(int n, int nranks, int rank, const double* X_local, const int32_t* rec_row,
                                  const int32_t* send_cols, int m, double* sendbuf, void* stream);
 
 /* Ainv_local[i][recv_cols[t]] = recvbuf[t][i]: Ainv_local is n x (this rank's real output
  * columns, in increasing global order) with row stride ld. */
-gj_status gj_dist_unpermute_unpack(int n, const double* recvbuf, const int32_t* recv_cols, int m, double* Ainv_local,
+gj_status gj_dist_step_unpermute_unpack(int n, const double* recvbuf, const int32_t* recv_cols, int m, double* Ainv_local,
                                    int64_t ld, void* stream);
+
+/*
+ * ---------------------------------------------------------------------------------------
+ * Distributed large-n inversion, library-driven: the same column-block-cyclic method as the
+ * step functions above (Eqs. (14)-(15) aggregated over 128-column panels, PAPER.md L61-L72;
+ * the max-|a_ik| pivot search of Obs. 3, L60, local to each panel's owner; the
+ * un-permutation of the listing, L179-L198, as one all-to-all of columns), with the library
+ * owning the NCCL communicator and driving the per-panel exchange itself:
+ *   per panel k: the owner factors it; W (npad x 128 fp64) and the replicated state
+ *   (pos | pivstep | rec_q | rec_row | rec_p, 6 npad int32) are broadcast from the owner with
+ *   ncclBroadcast on an internal side stream, double-buffered by panel parity, while panel
+ *   k-1's update still runs (look-ahead: the owner of k+1 updates and factors k+1 first);
+ *   every rank applies the update to its local columns (K4b DMMA GEMM);
+ *   then ncclAllReduce (max) of max|a_ij| for the threshold, and grouped ncclSend/ncclRecv
+ *   for the un-permutation.
+ * NCCL is loaded at run time (dlopen "libnccl.so.2"; the copy torch loaded is reused), so
+ * the library has no link-time NCCL dependency; without it these return GJ_ERR_NCCL.
+ * ---------------------------------------------------------------------------------------
+ */
+typedef struct gj_dist_ctx* gj_dist_handle;
+#define GJ_DIST_UNIQUE_ID_BYTES 128
+
+/* A new NCCL unique id (rank 0 calls it and shares the 128 bytes with every rank out of
+ * band).  Returns GJ_OK or GJ_ERR_NCCL. */
+gj_status gj_dist_get_unique_id(unsigned char unique_id[GJ_DIST_UNIQUE_ID_BYTES]);
+
+/* Collective over the nranks processes (one GPU each, `device` = this rank's CUDA device):
+ * creates the communicator (ncclCommInitRank) and the internal stream / events.  *handle is
+ * owned by the caller until gj_dist_finalize.  Returns GJ_OK, GJ_ERR_ARG (nranks outside
+ * 1..GJ_DIST_MAX_RANKS, rank outside 0..nranks-1, NULL), GJ_ERR_CUDA or GJ_ERR_NCCL. */
+gj_status gj_dist_init(int nranks, int rank, const unsigned char unique_id[GJ_DIST_UNIQUE_ID_BYTES], int device,
+                       gj_dist_handle* handle);
+
+/* Collective: every rank calls it with the same n (> 64) and tol.  A_local: this rank's real
+ * columns of A (gj_dist_sizes' ncols_local_real of them, the global columns c with
+ * (c / GJ_DIST_BLOCK) % nranks == rank, increasing), n rows, row stride lda; Ainv_local: the
+ * same columns of A^-1, row stride ldainv (may not alias A_local).  ipiv [n], logabsdet,
+ * sign, info: replicated outputs on every rank (any may be NULL).  All DEVICE pointers on
+ * the handle's device; the work is enqueued on `stream`, and the call returns after one host
+ * synchronisation of it (the all-to-all sizes depend on the pivots) with the un-permutation
+ * enqueued.  Workspace is allocated stream-ordered (cudaMallocAsync) and freed by the call.
+ * Returns GJ_OK, GJ_ERR_ARG, GJ_ERR_CUDA or GJ_ERR_NCCL; a singular matrix is data (info). */
+gj_status gj_invert_dist(gj_dist_handle handle, int n, const double* A_local, int64_t lda, double* Ainv_local,
+                         int64_t ldainv, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,
+                         void* stream);
+
+/* Destroys the communicator and the handle (collective).  NULL is a no-op. */
+gj_status gj_dist_finalize(gj_dist_handle handle);
 
 /* Static description of a status code. */
 const char* gj_status_string(gj_status s);

@@ -57,6 +57,15 @@ def _load():
     L.gj_invert_batched_host.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, dbl, i64]
     L.gj_invert_batched_host.restype = i32
     L.gj_host_release.restype = i32
+    ub = ctypes.POINTER(ctypes.c_ubyte)
+    L.gj_dist_get_unique_id.argtypes = [ub]
+    L.gj_dist_get_unique_id.restype = i32
+    L.gj_dist_init.argtypes = [i32, i32, ub, i32, ctypes.POINTER(ctypes.c_void_p)]
+    L.gj_dist_init.restype = i32
+    L.gj_invert_dist.argtypes = [vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, dbl, vp]
+    L.gj_invert_dist.restype = i32
+    L.gj_dist_finalize.argtypes = [vp]
+    L.gj_dist_finalize.restype = i32
     L.gj_status_string.argtypes = [i32]
     L.gj_status_string.restype = ctypes.c_char_p
     L.gj_version.restype = ctypes.c_char_p

@@ -10,7 +10,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgjinv.so")
 ROOT = os.path.dirname(PKG)
 
-SOURCES = ["gj_api.cu", "gj_batched.cu", "gj_batched64.cu", "gj_batched64e.cu", "gj_fullpiv.cu", "gj_solve.cu", "gj_large.cu", "gj_dgemm.cu", "gj_tcgemm.cu", "gj_tma.cu"]
+SOURCES = ["gj_api.cu", "gj_batched.cu", "gj_batched64.cu", "gj_batched64e.cu", "gj_fullpiv.cu", "gj_solve.cu", "gj_large.cu", "gj_dgemm.cu", "gj_dist.cu", "gj_tcgemm.cu", "gj_tma.cu"]
 HEADERS = ["gj_internal.h", "gj_ptx.cuh", "gj_rowops.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

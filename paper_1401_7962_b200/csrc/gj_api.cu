@@ -324,7 +324,7 @@ gj_status gj_dist_sizes(int n, int nranks, int rank, int* npad, int* ncols_local
   return GJ_OK;
 }
 
-gj_status gj_dist_init(int n, int nranks, int rank, const double* A_local, int64_t lda, double* X_local,
+gj_status gj_dist_step_init(int n, int nranks, int rank, const double* A_local, int64_t lda, double* X_local,
                        int32_t* pos, int32_t* pivstep, uint64_t* smax_bits, void* stream) {
   if (!dist_args_ok(n, nranks, rank) || !X_local || !pos || !pivstep || !smax_bits) return GJ_ERR_ARG;
   int npad, nl, nr;
@@ -334,7 +334,7 @@ gj_status gj_dist_init(int n, int nranks, int rank, const double* A_local, int64
                    static_cast<cudaStream_t>(stream)) == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_dist_factor(int n, int nranks, int rank, int k, double* X_local, int32_t* pos, int32_t* pivstep,
+gj_status gj_dist_step_factor(int n, int nranks, int rank, int k, double* X_local, int32_t* pos, int32_t* pivstep,
                          double* rec_p, int32_t* rec_q, int32_t* rec_row, double* W, void* stream) {
   if (!dist_args_ok(n, nranks, rank) || !X_local || !pos || !pivstep || !rec_p || !rec_q || !rec_row || !W) return GJ_ERR_ARG;
   int npad, nl, nr;
@@ -344,7 +344,7 @@ gj_status gj_dist_factor(int n, int nranks, int rank, int k, double* X_local, in
                      static_cast<cudaStream_t>(stream)) == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_dist_update(int n, int nranks, int rank, int k, int part, double* X_local, const double* W,
+gj_status gj_dist_step_update(int n, int nranks, int rank, int k, int part, double* X_local, const double* W,
                          const int32_t* pivstep, const int32_t* rec_row, double* R, void* stream) {
   if (!dist_args_ok(n, nranks, rank) || !W || !pivstep || !rec_row || part < 0 || part > 2) return GJ_ERR_ARG;
   int npad, nl, nr;
@@ -358,28 +358,28 @@ gj_status gj_dist_update(int n, int nranks, int rank, int k, int part, double* X
                  cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_dist_finalize(int n, const double* rec_p, const int32_t* rec_q, double tol, const uint64_t* smax_bits,
+gj_status gj_dist_step_finalize(int n, const double* rec_p, const int32_t* rec_q, double tol, const uint64_t* smax_bits,
                            int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, void* stream) {
   if (n < 1 || !rec_p || !rec_q || !smax_bits) return GJ_ERR_ARG;
   return dist_finalize(n, rec_p, rec_q, resolve_tol(GJ_F64, n, tol), reinterpret_cast<const unsigned long long*>(smax_bits),
                        ipiv, logabsdet, sign, info, static_cast<cudaStream_t>(stream)) == cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_dist_unpermute_plan(int n, int nranks, int rank, const int32_t* pivstep, int32_t* send_cols,
+gj_status gj_dist_step_unpermute_plan(int n, int nranks, int rank, const int32_t* pivstep, int32_t* send_cols,
                                  int32_t* recv_cols, int32_t* counts, void* stream) {
   if (!dist_args_ok(n, nranks, rank) || !pivstep || !send_cols || !recv_cols || !counts) return GJ_ERR_ARG;
   return dist_unpermute_plan(n, nranks, rank, pivstep, send_cols, recv_cols, counts, static_cast<cudaStream_t>(stream)) ==
                  cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_dist_unpermute_pack(int n, int nranks, int rank, const double* X_local, const int32_t* rec_row,
+gj_status gj_dist_step_unpermute_pack(int n, int nranks, int rank, const double* X_local, const int32_t* rec_row,
                                  const int32_t* send_cols, int m, double* sendbuf, void* stream) {
   if (!dist_args_ok(n, nranks, rank) || m < 0 || (m > 0 && (!X_local || !rec_row || !send_cols || !sendbuf))) return GJ_ERR_ARG;
   return dist_unpermute_pack(n, nranks, rank, X_local, rec_row, send_cols, m, sendbuf, static_cast<cudaStream_t>(stream)) ==
                  cudaSuccess ? GJ_OK : GJ_ERR_CUDA;
 }
 
-gj_status gj_dist_unpermute_unpack(int n, const double* recvbuf, const int32_t* recv_cols, int m, double* Ainv_local,
+gj_status gj_dist_step_unpermute_unpack(int n, const double* recvbuf, const int32_t* recv_cols, int m, double* Ainv_local,
                                    int64_t ld, void* stream) {
   if (n < 1 || m < 0 || (m > 0 && (!recvbuf || !recv_cols || !Ainv_local))) return GJ_ERR_ARG;
   return dist_unpermute_unpack(n, recvbuf, recv_cols, m, Ainv_local, ld, static_cast<cudaStream_t>(stream)) == cudaSuccess

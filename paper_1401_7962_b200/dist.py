@@ -8,11 +8,11 @@ with ``torch.distributed`` (NCCL over NVLink on a GPU box):
 * global column block j (``BLOCK`` = 128 columns, the panel width) lives on rank j % P;
   rows are complete on every rank, so a panel's max-|a_ik| pivot search (PAPER.md Obs. 3,
   L60) is local to the panel's owner;
-* per panel k: the owner factors it (``gj_dist_factor``: the panel's 128 pivot steps,
+* per panel k: the owner factors it (``gj_dist_step_factor``: the panel's 128 pivot steps,
   Eqs. (14)-(15) restricted to the panel), then ONE broadcast of W (the factored panel)
   and the replicated step record / row positions goes from the owner to every rank, and
   every rank applies the panel's aggregated rank-128 update to its own columns
-  (``gj_dist_update``: DMMA GEMM);
+  (``gj_dist_step_update``: DMMA GEMM);
 * the listing's un-permutation (L179-L198) is one all-to-all of columns at the end.
 
 The step functions are reached through a ``steps`` object so that the host logic can be
@@ -60,13 +60,13 @@ class CudaSteps:
         self.n, self.P, self.rank = n, P, rank
         for name, args in (
             ("gj_dist_sizes", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3),
-            ("gj_dist_init", [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 5),
-            ("gj_dist_factor", [ctypes.c_int] * 4 + [ctypes.c_void_p] * 8),
-            ("gj_dist_update", [ctypes.c_int] * 5 + [ctypes.c_void_p] * 6),
-            ("gj_dist_finalize", [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double] + [ctypes.c_void_p] * 6),
-            ("gj_dist_unpermute_plan", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 5),
-            ("gj_dist_unpermute_pack", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
-            ("gj_dist_unpermute_unpack", [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+            ("gj_dist_step_init", [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 5),
+            ("gj_dist_step_factor", [ctypes.c_int] * 4 + [ctypes.c_void_p] * 8),
+            ("gj_dist_step_update", [ctypes.c_int] * 5 + [ctypes.c_void_p] * 6),
+            ("gj_dist_step_finalize", [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double] + [ctypes.c_void_p] * 6),
+            ("gj_dist_step_unpermute_plan", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 5),
+            ("gj_dist_step_unpermute_pack", [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+            ("gj_dist_step_unpermute_unpack", [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                           ctypes.c_int64, ctypes.c_void_p]),
         ):
             f = getattr(lib, name)
@@ -81,32 +81,32 @@ class CudaSteps:
         return torch.cuda.current_stream().cuda_stream
 
     def init(self, A_local, lda, X, pos, pivstep, smax):
-        self._check(self.lib.gj_dist_init(self.n, self.P, self.rank, self._p(A_local), lda, X.data_ptr(), pos.data_ptr(),
+        self._check(self.lib.gj_dist_step_init(self.n, self.P, self.rank, self._p(A_local), lda, X.data_ptr(), pos.data_ptr(),
                                           pivstep.data_ptr(), smax.data_ptr(), self._s()))
 
     def factor(self, k, X, pos, pivstep, rec_p, rec_q, rec_row, W):
-        self._check(self.lib.gj_dist_factor(self.n, self.P, self.rank, k, X.data_ptr(), pos.data_ptr(), pivstep.data_ptr(),
+        self._check(self.lib.gj_dist_step_factor(self.n, self.P, self.rank, k, X.data_ptr(), pos.data_ptr(), pivstep.data_ptr(),
                                             rec_p.data_ptr(), rec_q.data_ptr(), rec_row.data_ptr(), W.data_ptr(), self._s()))
 
     def update(self, k, part, X, W, pivstep, rec_row, R):
-        self._check(self.lib.gj_dist_update(self.n, self.P, self.rank, k, part, self._p(X), W.data_ptr(),
+        self._check(self.lib.gj_dist_step_update(self.n, self.P, self.rank, k, part, self._p(X), W.data_ptr(),
                                             pivstep.data_ptr(), rec_row.data_ptr(), self._p(R), self._s()))
 
     def finalize(self, rec_p, rec_q, tol, smax, ipiv, logabsdet, sign, info):
-        self._check(self.lib.gj_dist_finalize(self.n, rec_p.data_ptr(), rec_q.data_ptr(), tol, smax.data_ptr(),
+        self._check(self.lib.gj_dist_step_finalize(self.n, rec_p.data_ptr(), rec_q.data_ptr(), tol, smax.data_ptr(),
                                               ipiv.data_ptr(), logabsdet.data_ptr(), sign.data_ptr(), info.data_ptr(),
                                               self._s()))
 
     def plan(self, pivstep, send_cols, recv_cols, counts):
-        self._check(self.lib.gj_dist_unpermute_plan(self.n, self.P, self.rank, pivstep.data_ptr(), send_cols.data_ptr(),
+        self._check(self.lib.gj_dist_step_unpermute_plan(self.n, self.P, self.rank, pivstep.data_ptr(), send_cols.data_ptr(),
                                                     recv_cols.data_ptr(), counts.data_ptr(), self._s()))
 
     def pack(self, X, rec_row, send_cols, m, sendbuf):
-        self._check(self.lib.gj_dist_unpermute_pack(self.n, self.P, self.rank, self._p(X), rec_row.data_ptr(),
+        self._check(self.lib.gj_dist_step_unpermute_pack(self.n, self.P, self.rank, self._p(X), rec_row.data_ptr(),
                                                     send_cols.data_ptr(), m, self._p(sendbuf), self._s()))
 
     def unpack(self, recvbuf, recv_cols, m, Y, ld):
-        self._check(self.lib.gj_dist_unpermute_unpack(self.n, self._p(recvbuf), recv_cols.data_ptr(), m, self._p(Y), ld,
+        self._check(self.lib.gj_dist_step_unpermute_unpack(self.n, self._p(recvbuf), recv_cols.data_ptr(), m, self._p(Y), ld,
                                                       self._s()))
 
 
@@ -287,3 +287,58 @@ def invert_dist(A_local: torch.Tensor, n: int, *, group=None, tol: Optional[floa
         t0 = ev[0][1]
         times = {name: t0.elapsed_time(e) for name, e in ev[1:]}
     return DistResult(Y, float(lg.item()), int(sg.item()), int(info.item()), ipiv, times)
+
+
+class DistContext:
+    """The library-driven NCCL path (``gj_dist_init`` / ``gj_invert_dist`` /
+    ``gj_dist_finalize``): the same schedule as :func:`invert_dist`, with the communicator and
+    the per-panel exchange inside ``libgjinv.so``.  Collective over ``group`` (default: the
+    world); rank 0 creates the NCCL unique id and the group broadcasts it."""
+
+    def __init__(self, group=None, device: Optional[torch.device] = None):
+        from . import lib, _check
+        self.lib, self._check = lib, _check
+        self.P = tdist.get_world_size(group)
+        self.rank = tdist.get_rank(group)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        uid = (ctypes.c_ubyte * 128)()
+        if self.rank == 0:
+            _check(lib.gj_dist_get_unique_id(uid))
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+        if tdist.get_backend(group) == "nccl":
+            t = t.to(dev)
+        tdist.broadcast(t, src=tdist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        buf = (ctypes.c_ubyte * 128)(*t.cpu().tolist())
+        self.handle = ctypes.c_void_p()
+        _check(lib.gj_dist_init(self.P, self.rank, buf, dev.index, ctypes.byref(self.handle)))
+
+    def invert(self, A_local: torch.Tensor, n: int, tol: Optional[float] = None, stream=None) -> "DistResult":
+        """This rank's columns of A^-1 (``local_columns(n, P, rank)``), fp64, on the context's device."""
+        npad, nl, nr = sizes(n, self.P, self.rank)
+        if A_local.dtype != torch.float64 or A_local.shape != (n, nr) or A_local.device != self.device or \
+                (nr and A_local.stride(1) != 1):
+            raise ValueError(f"A_local must be float64 [{n}, {nr}] on {self.device} with unit column stride")
+        f64 = dict(dtype=torch.float64, device=self.device)
+        Y = torch.empty((n, nr), **f64)
+        ipiv = torch.empty(n, dtype=torch.int32, device=self.device)
+        lg = torch.empty(1, **f64)
+        sg = torch.empty(1, dtype=torch.int8, device=self.device)
+        info = torch.empty(1, dtype=torch.int32, device=self.device)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._check(self.lib.gj_invert_dist(self.handle, n, A_local.data_ptr() if nr else None, max(A_local.stride(0), 1),
+                                            Y.data_ptr() if nr else None, max(nr, 1), ipiv.data_ptr(), lg.data_ptr(),
+                                            sg.data_ptr(), info.data_ptr(), -1.0 if tol is None else float(tol),
+                                            s.cuda_stream))
+        return DistResult(Y, float(lg.item()), int(sg.item()), int(info.item()), ipiv, {})
+
+    def close(self):
+        if self.handle:
+            self._check(self.lib.gj_dist_finalize(self.handle))
+            self.handle = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -104,3 +104,22 @@ def test_large_order_limit(gj):
     assert L.gj_invert(1, n, 1, n, 1, n, None, None, None, None, -1.0, 1, 1 << 40, None) == 2
     assert L.gj_det(1, n, 1, 1, None, None, None, None, None, -1.0, 1, 1 << 40, None) == 2
     assert L.gj_solve(1, n, 1, 1, n, 1, 1, 1, 1, None, None, None, None, -1.0, 1, 1 << 40, None) == 2
+
+
+def test_dist_handle_entry_points_check_arguments():
+    """gj_dist_init / gj_invert_dist / gj_dist_finalize refuse bad arguments before touching
+    NCCL or the GPU (include/gjinv.h)."""
+    import ctypes
+    import paper_1401_7962_b200 as gj
+    L = gj.lib
+    h = ctypes.c_void_p()
+    uid = (ctypes.c_ubyte * 128)()
+    assert L.gj_dist_init(0, 0, uid, 0, ctypes.byref(h)) == 1          # nranks < 1
+    assert L.gj_dist_init(9, 0, uid, 0, ctypes.byref(h)) == 1          # > GJ_DIST_MAX_RANKS
+    assert L.gj_dist_init(2, 2, uid, 0, ctypes.byref(h)) == 1          # rank out of range
+    assert L.gj_dist_init(1, 0, None, 0, ctypes.byref(h)) == 1         # no unique id
+    assert L.gj_dist_init(1, 0, uid, -1, ctypes.byref(h)) == 1         # device
+    assert L.gj_dist_init(1, 0, uid, 0, None) == 1                     # no handle
+    assert L.gj_invert_dist(None, 1000, None, 1, None, 1, None, None, None, None, -1.0, None) == 1
+    assert L.gj_dist_finalize(None) == 0
+    assert L.gj_dist_get_unique_id(None) == 1

@@ -119,3 +119,44 @@ def test_dist_c5_generator_n8192_vs_stored_oracle(P):
     assert abs(lg - float(ref["logabsdet"])) <= max(1e-10, kappa * 2.0 ** -52)
     A = synth.gen_gaussian(n, seed=4)
     assert oracle.residual(A, X, rows=rows) <= TOL_RES[np.float64]
+
+
+def _lib_worker(rank, P, n, kind, port, outdir):
+    """The library-driven path (gj_dist_init / gj_invert_dist / gj_dist_finalize): the
+    communicator and every collective inside libgjinv.so (NCCL)."""
+    import torch
+    import torch.distributed as tdist
+    from paper_1401_7962_b200.dist import DistContext, local_columns
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=P, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        A = synth.gen_gaussian(n, seed=70 + n) if kind == "gauss" else synth.hadamard_pd(n, seed=5)[0]
+        cols = local_columns(n, P, rank)
+        A_local = torch.from_numpy(np.ascontiguousarray(A[:, cols])).cuda()
+        with DistContext() as ctx:
+            r = ctx.invert(A_local, n)
+            r2 = ctx.invert(A_local, n)          # the handle is reusable
+        torch.cuda.synchronize()
+        assert torch.equal(r.inverse_local, r2.inverse_local)
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), inv=r.inverse_local.cpu().numpy(), cols=np.array(cols),
+                 lg=r.logabsdet, sign=r.sign, info=r.info, ipiv=r.ipiv.cpu().numpy())
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,kind", [(300, "gauss"), (1000, "gauss"), (1024, "hadamard")])
+def test_library_driven_dist_one_rank(n, kind):
+    """gj_invert_dist at P = 1 (one GPU): bitwise the single-GPU gj_invert (same panels, pivots
+    and K-loop order) and exact on the Hadamard pin."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_lib_worker, args=(1, n, kind, _free_port(), d), nprocs=1, join=True, start_method="spawn")
+        o = np.load(os.path.join(d, "r0.npz"))
+    X = o["inv"]
+    A = synth.gen_gaussian(n, seed=70 + n) if kind == "gauss" else synth.hadamard_pd(n, seed=5)[0]
+    Xs, lgs, sgs, ipivs = single(n, A)
+    assert int(o["info"]) == 0
+    assert np.array_equal(X, Xs)
+    assert np.array_equal(o["ipiv"], ipivs) and int(o["sign"]) == sgs and float(o["lg"]) == lgs
+    if kind == "hadamard":
+        assert np.array_equal(X, A.T / n)
