@@ -55,6 +55,7 @@ def parse():
                    help="c2: the headline batched line; c5: one fp64 32768^2 matrix, column-block-cyclic over the ranks")
     p.add_argument("--n", type=int, default=32768, help="order for --workload c5")
     p.add_argument("--no-weak", action="store_true", help="skip the weak-scaling secondary key (N > 1)")
+    p.add_argument("--c5-oracle-n", type=int, default=4096, help="order of the oracle timing in the c5 line")
     p.add_argument("--dist-driver", default="library", choices=["library", "python"],
                    help="c5: gj_invert_dist (NCCL inside libgjinv) or the dist.py schedule over torch.distributed")
     return p.parse_args()
@@ -445,9 +446,11 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def c5_oracle_baseline(n_full: int, n: int = 8192):
-    """the oracle timed at n = 8192 on the C5 generator (N(0,1)/sqrt(n), seed 4)
-    on the host's cores, and the n^3-extrapolated time of the full C5 order."""
+def c5_oracle_baseline(n_full: int, n: int = 4096):
+    """the oracle timed on the C5 generator (N(0,1)/sqrt(n), seed 4) on the host's
+    cores at order n, and the n^3-extrapolated time of the full C5 order.  Default n = 4096
+    (~35 s on 16 cores) keeps the line bounded; --c5-oracle-n 8192 reproduces SURVEY's size
+    (285 s on the box's 16 cores, 18,245 s extrapolated: profiles/r02_bench_c5.json)."""
     import oracle
     import synth
     A = synth.gen_gaussian(n, seed=4)
@@ -528,7 +531,8 @@ def run_c5(args, rank, world, local):
                                        "frac": tf / (peak * world), "traffic": None, "peak_source": src + f" x {world}"},
                           "logabsdet": res.logabsdet, "sign": res.sign, "info": res.info,
                           "clocks": clk.summary(), "gpu_launches": None,
-                          "cpu_baseline": None if args.no_cpu_baseline else c5_oracle_baseline(n)}), flush=True)
+                          "cpu_baseline": None if args.no_cpu_baseline else c5_oracle_baseline(n, args.c5_oracle_n)}),
+              flush=True)
     tdist.barrier()
     tdist.destroy_process_group()
 

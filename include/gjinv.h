@@ -324,7 +324,8 @@ gj_status gj_dist_init(int nranks, int rank, const unsigned char unique_id[GJ_DI
  * sign, info: replicated outputs on every rank (any may be NULL).  All DEVICE pointers on
  * the handle's device; the work is enqueued on `stream`, and the call returns after one host
  * synchronisation of it (the all-to-all sizes depend on the pivots) with the un-permutation
- * enqueued.  Workspace is allocated stream-ordered (cudaMallocAsync) and freed by the call.
+ * enqueued.  The device workspace (~(npad x local columns + 3 npad x 128) doubles) is kept in the
+ * handle between calls and freed by gj_dist_finalize.
  * Returns GJ_OK, GJ_ERR_ARG, GJ_ERR_CUDA or GJ_ERR_NCCL; a singular matrix is data (info). */
 gj_status gj_invert_dist(gj_dist_handle handle, int n, const double* A_local, int64_t lda, double* Ainv_local,
                          int64_t ldainv, int32_t* ipiv, double* logabsdet, int8_t* sign, int32_t* info, double tol,

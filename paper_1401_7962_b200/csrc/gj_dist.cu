@@ -81,6 +81,8 @@ struct gj_dist_ctx {
   ncclComm_t comm = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_upd = nullptr, ev_fac = nullptr, ev_b = nullptr;
+  void* ws = nullptr;      // device workspace, kept between calls (grown on demand)
+  size_t ws_bytes = 0;
 };
 
 namespace {
@@ -103,20 +105,16 @@ struct DeviceScope {   // run on the handle's device, restore the caller's
     if ((x) != 0) return GJ_ERR_NCCL;                \
   } while (0)
 
-// Stream-ordered device allocations released on the stream at scope exit.
-struct Scratch {
-  cudaStream_t s;
-  std::vector<void*> ptrs;
-  explicit Scratch(cudaStream_t st) : s(st) {}
+// Carves 256-byte aligned pieces from one workspace (a dry run sizes it).
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(void* b) : base(static_cast<char*>(b)) {}
   template <typename T>
   T* get(size_t count) {
-    void* p = nullptr;
-    if (cudaMallocAsync(&p, count * sizeof(T) + 16, s) != cudaSuccess) return nullptr;
-    ptrs.push_back(p);
-    return static_cast<T*>(p);
-  }
-  ~Scratch() {
-    for (void* p : ptrs) cudaFreeAsync(p, s);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += (count * sizeof(T) + 255) / 256 * 256;
+    return p;
   }
 };
 
@@ -170,6 +168,7 @@ gj_status gj_dist_finalize(gj_dist_handle c) {
   const Nccl& N = nccl();
   gj_status st = GJ_OK;
   if (c->comm && N.ok && N.CommDestroy(c->comm) != 0) st = GJ_ERR_NCCL;
+  if (c->ws) cudaFree(c->ws);
   if (c->side) cudaStreamDestroy(c->side);
   for (cudaEvent_t e : {c->ev_upd, c->ev_fac, c->ev_b})
     if (e) cudaEventDestroy(e);
@@ -192,21 +191,60 @@ gj_status gj_invert_dist(gj_dist_handle c, int n, const double* A_local, int64_t
   const int nb = npad / GJ_DIST_BLOCK;
   const int B = GJ_DIST_BLOCK;
 
-  Scratch sc(s);
-  double* X = sc.get<double>((size_t)npad * (nl > 0 ? nl : 1));
-  int32_t* ibuf[2] = {sc.get<int32_t>(6 * (size_t)npad), sc.get<int32_t>(6 * (size_t)npad)};
-  double* wbuf[2] = {sc.get<double>((size_t)npad * B), sc.get<double>((size_t)npad * B)};
-  double* R = sc.get<double>((size_t)B * (nl > 0 ? nl : 1));
-  uint64_t* smax = sc.get<uint64_t>(1);
-  int32_t* o_ipiv = ipiv ? ipiv : sc.get<int32_t>(n);
-  double* o_lg = logabsdet ? logabsdet : sc.get<double>(1);
-  int8_t* o_sg = sign ? sign : sc.get<int8_t>(1);
-  int32_t* o_info = info ? info : sc.get<int32_t>(1);
-  int32_t* send_cols = sc.get<int32_t>(nl > 0 ? nl : 1);
-  int32_t* recv_cols = sc.get<int32_t>(nr > 0 ? nr : 1);
-  int32_t* counts = sc.get<int32_t>(2 * P);
-  for (void* p : sc.ptrs)
-    if (!p) return GJ_ERR_CUDA;
+  // workspace (kept in the handle): X, state x 2, W x 2, R, smax, outputs, plan, buffers
+  auto carve = [&](Carve& cv, int ms, int mr) {
+    struct Parts {
+      double *X, *w0, *w1, *R, *lg, *sendbuf, *recvbuf;
+      int32_t *i0, *i1, *ipiv, *info, *send_cols, *recv_cols, *counts;
+      uint64_t* smax;
+      int8_t* sg;
+    } p;
+    p.X = cv.get<double>((size_t)npad * (nl > 0 ? nl : 1));
+    p.i0 = cv.get<int32_t>(6 * (size_t)npad);
+    p.i1 = cv.get<int32_t>(6 * (size_t)npad);
+    p.w0 = cv.get<double>((size_t)npad * B);
+    p.w1 = cv.get<double>((size_t)npad * B);
+    p.R = cv.get<double>((size_t)B * (nl > 0 ? nl : 1));
+    p.smax = cv.get<uint64_t>(1);
+    p.ipiv = cv.get<int32_t>(n);
+    p.lg = cv.get<double>(1);
+    p.sg = cv.get<int8_t>(1);
+    p.info = cv.get<int32_t>(1);
+    p.send_cols = cv.get<int32_t>(nl > 0 ? nl : 1);
+    p.recv_cols = cv.get<int32_t>(nr > 0 ? nr : 1);
+    p.counts = cv.get<int32_t>(2 * P);
+    p.sendbuf = cv.get<double>((size_t)(ms > 0 ? ms : 1) * n);
+    p.recvbuf = cv.get<double>((size_t)(mr > 0 ? mr : 1) * n);
+    return p;
+  };
+  // the all-to-all buffers are at most one local column block set each: size for the worst
+  // case (every local column / every output column) so the workspace is sized up front
+  Carve dry(nullptr);
+  carve(dry, nl, nr);
+  if (dry.off > c->ws_bytes) {
+    if (c->ws) {
+      GJ_CU(cudaStreamSynchronize(s));
+      cudaFree(c->ws);
+      c->ws = nullptr;
+      c->ws_bytes = 0;
+    }
+    GJ_CU(cudaMalloc(&c->ws, dry.off));
+    c->ws_bytes = dry.off;
+  }
+  Carve cv(c->ws);
+  const auto pp = carve(cv, nl, nr);
+  double* X = pp.X;
+  int32_t* ibuf[2] = {pp.i0, pp.i1};
+  double* wbuf[2] = {pp.w0, pp.w1};
+  double* R = pp.R;
+  uint64_t* smax = pp.smax;
+  int32_t* o_ipiv = ipiv ? ipiv : pp.ipiv;
+  double* o_lg = logabsdet ? logabsdet : pp.lg;
+  int8_t* o_sg = sign ? sign : pp.sg;
+  int32_t* o_info = info ? info : pp.info;
+  int32_t* send_cols = pp.send_cols;
+  int32_t* recv_cols = pp.recv_cols;
+  int32_t* counts = pp.counts;
   // replicated state views: pos | pivstep | rec_q | rec_row | rec_p (fp64 as 2 x int32)
   struct View {
     int32_t *pos, *piv, *rq, *rr;
@@ -276,9 +314,8 @@ gj_status gj_invert_dist(gj_dist_handle c, int n, const double* A_local, int64_t
     ms += cnt[p];
     mr += cnt[P + p];
   }
-  double* sendbuf = sc.get<double>((size_t)(ms > 0 ? ms : 1) * n);
-  double* recvbuf = P > 1 ? sc.get<double>((size_t)(mr > 0 ? mr : 1) * n) : sendbuf;
-  if (!sendbuf || !recvbuf) return GJ_ERR_CUDA;
+  double* sendbuf = pp.sendbuf;
+  double* recvbuf = P > 1 ? pp.recvbuf : sendbuf;
   if (ms > 0) GJ_CU(gj::dist_unpermute_pack(n, P, rank, X, vf.rr, send_cols, ms, sendbuf, s));
   if (P > 1) {
     GJ_NC(N.GroupStart());
