@@ -151,6 +151,89 @@ __device__ __forceinline__ void d_panel_step(const int k, double (&x)[2][BSD], u
     rowk[k] = src + 32 * slot;
   }
 }
+// Warp barrier with memory ordering among the lanes that ptxas does not turn into a
+// divergence check + branch (as __syncwarp does): the panel step stays one basic block, so
+// the interleaved trailing update (work) can be scheduled into its latency.
+__device__ __forceinline__ void wsync() { asm volatile("bar.warp.sync 0xffffffff;" ::: "memory"); }
+__device__ __forceinline__ void st2_if(bool p, double* addr, double a, double b) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.v2.f64 [%1], {%2, %3};\n}" ::"r"(p ? 1u : 0u),
+               "r"((uint32_t)__cvta_generic_to_shared(addr)), "d"(a), "d"(b)
+               : "memory");
+}
+
+struct NoWork {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+
+// K2e's pivot step S with a work hook: work(S) runs between the key reductions and the pivot
+// row exchange (independent instructions for the scheduler to interleave with the chain).
+template <int S, class Wk>
+__device__ __forceinline__ void e_panel_step(const int k, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
+                                             unsigned char* rec, int* rowk, int lane, double* prow, const Wk& work) {
+  uint32_t hi[2], lo[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x[r][S]);
+    hi[r] = (uint32_t)(b >> 32) & 0x7fffffffu & kmask[r];
+    lo[r] = (uint32_t)b & kmask[r];
+  }
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, max(hi[0], hi[1]));
+  const uint32_t lm = max(hi[0] == mh ? lo[0] : 0u, hi[1] == mh ? lo[1] : 0u);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, lm);
+  const double rap = rcp64d(__longlong_as_double((long long)(((unsigned long long)mh << 32) | ml)));
+  uint32_t c = 0xffffffu;
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    c = min(c, (hi[r] == mh && lo[r] == ml && kmask[r] != 0u) ? ((uint32_t)pos[r] << 6 | (uint32_t)lane << 1 | (uint32_t)r)
+                                                               : 0xffffffu);
+  const uint32_t win = __reduce_min_sync(0xffffffffu, c);
+  const int q = (int)(win >> 6);
+  const int src = (int)((win >> 1) & 31u);
+  const int slot = (int)(win & 1u);
+  work(S);
+  double* pr = prow + (S & 1) * BSD;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const bool me = lane == src && slot == r;
+#pragma unroll
+    for (int j = 0; j < BSD; j += 2) st2_if(me, pr + j, x[r][j], x[r][j + 1]);
+  }
+  wsync();
+  double z[BSD];
+#pragma unroll
+  for (int j = 0; j < BSD; j += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(pr + j);
+    z[j] = v.x;
+    z[j + 1] = v.y;
+  }
+  const double p = z[S];
+  const double rp = p < 0.0 ? -rap : rap;   // rcp64d is odd: bit-identical to rcp64d(p)
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const bool pv = pos[r] == q && kmask[r] != 0u;
+    const double nf = pv ? 0.0 : -(x[r][S] * rp);
+#pragma unroll
+    for (int j = 0; j < BSD; ++j)
+      if (j != S) x[r][j] = fma(nf, z[j], x[r][j]);
+    x[r][S] = nf;   // compact D entry; 0 on the pivot row (W - S)
+    kmask[r] = pv ? 0u : kmask[r];
+    pos[r] = (pos[r] == k) ? q : pos[r];   // a3: the listing's swap of positions k and q (L156-L162)
+    pos[r] = pv ? k : pos[r];
+  }
+  if (lane == 0) {
+    rec_store(rec, k, p, q);
+    rowk[k] = src + 32 * slot;
+  }
+}
+template <int S, class Wk>
+__device__ __forceinline__ void e_panel_steps(const int kb, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
+                                              unsigned char* rec, int* rowk, int lane, double* prow, const Wk& work) {
+  if constexpr (S < BSD) {
+    e_panel_step<S>(kb + S, x, kmask, pos, rec, rowk, lane, prow, work);
+    e_panel_steps<S + 1>(kb, x, kmask, pos, rec, rowk, lane, prow, work);
+  }
+}
+
 template <int S, bool SROW = false>
 __device__ __forceinline__ void d_panel_steps(const int kb, double (&x)[2][BSD], uint32_t (&kmask)[2], int (&pos)[2],
                                               int (&bs)[2], unsigned char* rec, int* rowk, int lane,
@@ -204,10 +287,46 @@ struct SmemE {
 #define GJ_K2E_NTU 2               // tile-loop unroll (measured: 1 13.5, 2 13.1, 4 13.2, 8 13.6 ms)
 #endif
 constexpr int kK2eNtu = GJ_K2E_NTU;
+#ifndef GJ_K2E_TWO_WARPS
+#define GJ_K2E_TWO_WARPS 1         // K2f: panel warp + trailing warp per matrix
+#endif
+#ifndef GJ_K2E_LA
+#define GJ_K2E_LA 1                // look-ahead: panel kb + 1 factored under block kb's update (inverse)
+#endif
 #ifndef GJ_K2E_OVERLAP
 #define GJ_K2E_OVERLAP 1           // load the next matrix under this one's store
 #endif
 
+// One 8-column tile of the block update: X[:, tile nt] += (W - S) R with the block's A
+// fragments af and pivot rows rk0 / rk1 (B read before the tile is written: the pivot rows are
+// rows of the tile).
+__device__ __forceinline__ void e_tile_update(double* M, int nt, const double (&af)[8][2], int rk0, int rk1, int g,
+                                              int t) {
+  const double b0 = M[mix(rk0, 8 * nt + g)];   // B[t][g]: pivot row of step t, block start
+  const double b1 = M[mix(rk1, 8 * nt + g)];
+  wsync();
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    double2* cp = reinterpret_cast<double2*>(M + mix(8 * mt + g, 8 * nt + 2 * t));
+    double2 c = *cp;
+    dmma884(c.x, c.y, af[mt][0], b0);
+    dmma884(c.x, c.y, af[mt][1], b1);
+    *cp = c;
+  }
+}
+
+// The six tiles other than the block's own and the look-ahead one, one per pivot step of the
+// next panel (steps 0..5), in the order kb + 2, kb + 3, ... (mod 8).
+struct TrailE {
+  double* M;
+  const double (&af)[8][2];
+  int rk0, rk1, kb, g, t;
+  __device__ __forceinline__ void operator()(int s) const {
+    if (s < 6) e_tile_update(M, (kb + 2 + s) & 7, af, rk0, rk1, g, t);
+  }
+};
+
+template <bool LA>
 __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_e[];
   double* M = reinterpret_cast<double*>(smem_e + SmemE::M);
@@ -252,6 +371,53 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
     uint32_t kmask[2] = {0xffffffffu, 0xffffffffu};
     int pos[2] = {lane, lane + 32};
 
+    if constexpr (LA) {
+      // look-ahead (inverse): block kb's update reaches tile kb + 1 first, then panel kb + 1
+      // is factored while the other six tiles take block kb's update, one per pivot step
+      double x[2][BSD];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < BSD; j += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(M + mix(lane + 32 * r, j));
+          x[r][j] = v.x;
+          x[r][j + 1] = v.y;
+        }
+      e_panel_steps<0>(0, x, kmask, pos, rec, rowk, lane, prow, NoWork{});
+#pragma unroll 1
+      for (int kb = 0; kb < N64 / BSD; ++kb) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int j = 0; j < BSD; j += 2)
+            *reinterpret_cast<double2*>(M + mix(lane + 32 * r, 8 * kb + j)) = make_double2(x[r][j], x[r][j + 1]);
+        wsync();
+        double af[8][2];
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          af[mt][0] = M[mix(8 * mt + g, 8 * kb + t)];       // A[g][t]
+          af[mt][1] = M[mix(8 * mt + g, 8 * kb + 4 + t)];   // A[g][4 + t]
+        }
+        const int rk0 = rowk[kb * BSD + t], rk1 = rowk[kb * BSD + 4 + t];
+        if (kb + 1 < N64 / BSD) {
+          e_tile_update(M, kb + 1, af, rk0, rk1, g, t);
+          wsync();
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int j = 0; j < BSD; j += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(M + mix(lane + 32 * r, 8 * (kb + 1) + j));
+              x[r][j] = v.x;
+              x[r][j + 1] = v.y;
+            }
+          e_panel_steps<0>((kb + 1) * BSD, x, kmask, pos, rec, rowk, lane, prow, TrailE{M, af, rk0, rk1, kb, g, t});
+        } else {
+#pragma unroll 1
+          for (int j = 1; j < 8; ++j) e_tile_update(M, (kb + j) & 7, af, rk0, rk1, g, t);
+        }
+        wsync();
+      }
+    } else {
 #pragma unroll 1
     for (int kb = 0; kb < N64 / BSD; ++kb) {
       // ---- the panel: rows lane, lane + 32 of column tile kb
@@ -312,6 +478,7 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
       }
       __syncwarp();
     }
+    }   // LA
 
     // ---- a6: det / ipiv / singular flag from the record (steps lane, lane + 32)
 #pragma unroll
@@ -404,6 +571,237 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
   }
 }
 
+
+// ------------------------------------------------------------------ K2f: two warps per matrix
+// K2e's layout and arithmetic with the panel chain and the trailing update on different warps
+// of one CTA (64 threads per matrix, the same ~34 KB of shared memory): warp P factors panel
+// kb + 1 while warp T applies block kb's update to the six other tiles — the update of tile
+// kb + 1 comes first, and named barriers pass "panel kb stored" (P -> T) and "tile kb + 1
+// updated" (T -> P).  Every output is bitwise K2e's (same operations in the same order per
+// element); what changes is that the latency-bound chain and the DMMA work overlap, with two
+// warps per matrix in flight on the SM instead of one.
+__device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+constexpr int BAR_PANEL = 1, BAR_TILE = 2;
+
+// NTL tiles of the block update at once, phased for the trailing warp's ILP: every B, a warp
+// barrier, every C fragment load, the k = 0..3 DMMAs, the k = 4..7 DMMAs, every store — so 8 x
+// NTL independent accumulator chains are in flight instead of one tile's 8.
+template <int NTL>
+__device__ __forceinline__ void f_tiles_update(double* M, const int (&nts)[NTL], const double (&af)[8][2], int rk0,
+                                               int rk1, int g, int t) {
+  double b0[NTL], b1[NTL];
+#pragma unroll
+  for (int u = 0; u < NTL; ++u) {
+    b0[u] = M[mix(rk0, 8 * nts[u] + g)];
+    b1[u] = M[mix(rk1, 8 * nts[u] + g)];
+  }
+  wsync();   // every lane has its B (pivot rows are rows of the tiles) before any tile is written
+  double2 c[NTL][8];
+#pragma unroll
+  for (int u = 0; u < NTL; ++u)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) c[u][mt] = *reinterpret_cast<const double2*>(M + mix(8 * mt + g, 8 * nts[u] + 2 * t));
+#pragma unroll
+  for (int u = 0; u < NTL; ++u)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) dmma884(c[u][mt].x, c[u][mt].y, af[mt][0], b0[u]);
+#pragma unroll
+  for (int u = 0; u < NTL; ++u)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) dmma884(c[u][mt].x, c[u][mt].y, af[mt][1], b1[u]);
+#pragma unroll
+  for (int u = 0; u < NTL; ++u)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) *reinterpret_cast<double2*>(M + mix(8 * mt + g, 8 * nts[u] + 2 * t)) = c[u][mt];
+}
+
+__global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_e[];
+  double* M = reinterpret_cast<double*>(smem_e + SmemE::M);
+  unsigned char* rec = smem_e + SmemE::REC;
+  int* rowk = reinterpret_cast<int*>(smem_e + SmemE::ROW);
+  int* posm = reinterpret_cast<int*>(smem_e + SmemE::POS);
+  double* rpm = reinterpret_cast<double*>(smem_e + SmemE::RP);
+  double* prow = reinterpret_cast<double*>(smem_e + SmemE::PROW);
+  double* rmx = rpm;   // [2] per-warp max |a_ij| (rpm is free until the epilogue)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const double* __restrict__ Ag = static_cast<const double*>(a.A);
+  double* __restrict__ Xg = static_cast<double*>(a.Ainv);
+  const int r0 = warp * 32;   // this warp's half of the rows for the load / store
+
+  bool loaded = false;
+  double rm_next = 0.0;
+  for (int64_t item = blockIdx.x; item < a.batch; item += gridDim.x) {
+    const double* Ai = Ag + item * (N64 * N64);
+    if (item + gridDim.x < a.batch && threadIdx.x == 0) bulk_prefetch_l2(Ag + (item + gridDim.x) * (N64 * N64), N64 * N64 * 8);
+    // ---- a1: this warp's 32 rows -> shared memory, max |a_ij|
+    double rm = rm_next;
+#pragma unroll 2
+    for (int i0 = r0; i0 < (loaded ? r0 : r0 + 32); i0 += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Ai + (i0 + u) * N64) + lane);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        *reinterpret_cast<double2*>(M + mix(i0 + u, 2 * lane)) = v[u];
+        rm = fmax(rm, fmax(fabs(v[u].x), fabs(v[u].y)));
+      }
+    }
+    {
+      const unsigned long long rb = (unsigned long long)__double_as_longlong(rm);
+      const uint32_t mh = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32));
+      const uint32_t ml = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32) == mh ? (uint32_t)rb : 0u);
+      if (lane == 0) rmx[warp] = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+    }
+    __syncthreads();   // the whole matrix and both maxima are in shared memory
+    const double tau = a.tol * fmax(rmx[0], rmx[1]);
+    uint32_t kmask[2] = {0xffffffffu, 0xffffffffu};
+    int pos[2] = {lane, lane + 32};
+
+    if (warp == 0) {
+      // ------------------------------------------------------------ P: the panels
+#pragma unroll 1
+      for (int kb = 0; kb < N64 / BSD; ++kb) {
+        if (kb > 0) nbar_sync(BAR_TILE);   // tile kb has block kb - 1's update
+        double x[2][BSD];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int j = 0; j < BSD; j += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(M + mix(lane + 32 * r, 8 * kb + j));
+            x[r][j] = v.x;
+            x[r][j + 1] = v.y;
+          }
+        e_panel_steps<0>(kb * BSD, x, kmask, pos, rec, rowk, lane, prow, NoWork{});
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int j = 0; j < BSD; j += 2)
+            *reinterpret_cast<double2*>(M + mix(lane + 32 * r, 8 * kb + j)) = make_double2(x[r][j], x[r][j + 1]);
+        nbar_arrive(BAR_PANEL);              // panel kb (W - S) and its record are stored
+      }
+    } else {
+      // ------------------------------------------------------------ T: the block updates
+#pragma unroll 1
+      for (int kb = 0; kb < N64 / BSD; ++kb) {
+        nbar_sync(BAR_PANEL);
+        double af[8][2];
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          af[mt][0] = M[mix(8 * mt + g, 8 * kb + t)];       // A[g][t]
+          af[mt][1] = M[mix(8 * mt + g, 8 * kb + 4 + t)];   // A[g][4 + t]
+        }
+        const int rk0 = rowk[kb * BSD + t], rk1 = rowk[kb * BSD + 4 + t];
+        if (kb + 1 < N64 / BSD) {
+          const int la[1] = {kb + 1};
+          f_tiles_update<1>(M, la, af, rk0, rk1, g, t);
+          wsync();
+          nbar_arrive(BAR_TILE);
+        }
+        if (Xg != nullptr) {
+          // the six other tiles (and at the last block tile 0 too), two at a time
+#pragma unroll 1
+          for (int j = 2; j < 8; j += 2) {
+            const int pr[2] = {(kb + j) & 7, (kb + j + 1) & 7};
+            f_tiles_update<2>(M, pr, af, rk0, rk1, g, t);
+          }
+          if (kb + 1 == N64 / BSD) {
+            const int z0[1] = {0};
+            f_tiles_update<1>(M, z0, af, rk0, rk1, g, t);
+          }
+        } else {
+          // determinant-only run: only the tiles right of the next panel
+#pragma unroll 1
+          for (int nt = kb + 2; nt < 8; ++nt) {
+            const int one[1] = {nt};
+            f_tiles_update<1>(M, one, af, rk0, rk1, g, t);
+          }
+        }
+      }
+    }
+    __syncthreads();   // the elimination is complete
+
+    // ---- a6 (warp P holds the positions): det / ipiv / singular flag from the record
+    if (warp == 0) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        posm[lane + 32 * r] = pos[r];
+        double pk;
+        int qk;
+        rec_load(rec, lane + 32 * r, pk, qk);
+        rpm[lane + 32 * r] = 1.0 / pk;
+      }
+      unsigned fb0 = 0, fb1 = 0;
+      int nswap = 0, nneg = 0;
+      double lg = 0.0;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int k = lane + 32 * r;
+        double pk;
+        int qk;
+        rec_load(rec, k, pk, qk);
+        const unsigned fb = __ballot_sync(0xffffffffu, fabs(pk) <= tau);
+        if (r == 0) fb0 = fb; else fb1 = fb;
+        nswap += __popc(__ballot_sync(0xffffffffu, qk != k));
+        nneg += __popc(__ballot_sync(0xffffffffu, pk < 0.0));
+        lg += log(fabs(pk));
+        if (a.ipiv) a.ipiv[item * N64 + k] = qk + 1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+      const int info = fb0 ? __ffs(fb0) : (fb1 ? 32 + __ffs(fb1) : 0);
+      const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
+      if (lane == 0) {
+        if (a.info) a.info[item] = info;
+        if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
+        if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
+        if (a.det) static_cast<double*>(a.det)[item] = info ? 0.0 : (double)(sgn * exp(lg));
+      }
+    }
+    __syncthreads();
+    // ---- a7 + a8: Ainv[pos(i)][row(k)] = X[i][k] / p_pos(i) (+ 1 / p on the own entry); each
+    // warp stores its half of the rows and loads the next matrix's same half under the store
+    loaded = false;
+    rm_next = 0.0;
+    if (Xg != nullptr) {
+      double* Xi = Xg + item * (N64 * N64);
+      const int oc0 = rowk[lane], oc1 = rowk[lane + 32];
+      const int64_t nitem = item + gridDim.x;
+      const bool pre = nitem < a.batch;
+      const double* An = Ag + nitem * (N64 * N64);
+#pragma unroll 1
+      for (int i0 = r0; i0 < r0 + 32; i0 += 8) {
+        double2 v[8];
+        if (pre) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(An + (i0 + u) * N64) + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u;
+          const int ps = posm[i];
+          const double rp = rpm[ps];
+          double* orow = Xi + (int64_t)ps * N64;
+          __stcs(orow + oc0, M[mix(i, lane)] * rp + (lane == ps ? rp : 0.0));
+          __stcs(orow + oc1, M[mix(i, lane + 32)] * rp + (lane + 32 == ps ? rp : 0.0));
+        }
+        __syncwarp();
+        if (pre) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            *reinterpret_cast<double2*>(M + mix(i0 + u, 2 * lane)) = v[u];
+            rm_next = fmax(rm_next, fmax(fabs(v[u].x), fabs(v[u].y)));
+          }
+        }
+      }
+      loaded = pre;
+    }
+    __syncthreads();   // shared state is rewritten by the next matrix
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
@@ -416,17 +814,28 @@ cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
   static unsigned long long configured = 0;
   const unsigned long long dbit = device_bit();
   if (!(configured & dbit)) {
-    cudaError_t e = cudaFuncSetAttribute(gj_batched64e_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    for (auto kern : {gj_batched64e_kernel<true>, gj_batched64e_kernel<false>}) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e2 = cudaFuncSetAttribute(gj_batched64f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e2 != cudaSuccess) return e2;
     configured |= dbit;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_batched64e_kernel, 32, smem);
+#if GJ_K2E_TWO_WARPS
+  auto kern = gj_batched64f_kernel;
+  const int threads = 64;
+#else
+  auto kern = a.Ainv != nullptr ? gj_batched64e_kernel<GJ_K2E_LA != 0> : gj_batched64e_kernel<false>;
+  const int threads = 32;
+#endif
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = (int64_t)device_sm_count() * per_sm;
   const int grid = (int)(a.batch < cap ? a.batch : cap);
-  gj_batched64e_kernel<<<grid, 32, smem, s>>>(a);
+  kern<<<grid, threads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
