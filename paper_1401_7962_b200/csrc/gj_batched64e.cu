@@ -580,8 +580,12 @@ __global__ void __launch_bounds__(32, 6) gj_batched64e_kernel(BatchedArgs a) {
 // updated" (T -> P).  Every output is bitwise K2e's (same operations in the same order per
 // element); what changes is that the latency-bound chain and the DMMA work overlap, with two
 // warps per matrix in flight on the SM instead of one.
-__device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+#ifndef GJ_K2F_WARPS
+#define GJ_K2F_WARPS 2             // warps per matrix: panel + 1 or 2 trailing warps
+#endif
+constexpr int kFW = GJ_K2F_WARPS;
 constexpr int BAR_PANEL = 1, BAR_TILE = 2;
 
 // NTL tiles of the block update at once, phased for the trailing warp's ILP: every B, a warp
@@ -616,7 +620,7 @@ __device__ __forceinline__ void f_tiles_update(double* M, const int (&nts)[NTL],
     for (int mt = 0; mt < 8; ++mt) *reinterpret_cast<double2*>(M + mix(8 * mt + g, 8 * nts[u] + 2 * t)) = c[u][mt];
 }
 
-__global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
+__global__ void __launch_bounds__(32 * kFW, 6) gj_batched64f_kernel(BatchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_e[];
   double* M = reinterpret_cast<double*>(smem_e + SmemE::M);
   unsigned char* rec = smem_e + SmemE::REC;
@@ -629,7 +633,8 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
   const int g = lane >> 2, t = lane & 3;
   const double* __restrict__ Ag = static_cast<const double*>(a.A);
   double* __restrict__ Xg = static_cast<double*>(a.Ainv);
-  const int r0 = warp * 32;   // this warp's half of the rows for the load / store
+  const int r0 = warp * 32;   // warps 0 and 1: their half of the rows for the load / store
+  const bool io = warp < 2;
 
   bool loaded = false;
   double rm_next = 0.0;
@@ -639,7 +644,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
     // ---- a1: this warp's 32 rows -> shared memory, max |a_ij|
     double rm = rm_next;
 #pragma unroll 2
-    for (int i0 = r0; i0 < (loaded ? r0 : r0 + 32); i0 += 8) {
+    for (int i0 = r0; i0 < (loaded || !io ? r0 : r0 + 32); i0 += 8) {
       double2 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Ai + (i0 + u) * N64) + lane);
@@ -653,7 +658,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
       const unsigned long long rb = (unsigned long long)__double_as_longlong(rm);
       const uint32_t mh = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32));
       const uint32_t ml = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32) == mh ? (uint32_t)rb : 0u);
-      if (lane == 0) rmx[warp] = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+      if (lane == 0 && io) rmx[warp] = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
     }
     __syncthreads();   // the whole matrix and both maxima are in shared memory
     const double tau = a.tol * fmax(rmx[0], rmx[1]);
@@ -664,7 +669,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
       // ------------------------------------------------------------ P: the panels
 #pragma unroll 1
       for (int kb = 0; kb < N64 / BSD; ++kb) {
-        if (kb > 0) nbar_sync(BAR_TILE);   // tile kb has block kb - 1's update
+        if (kb > 0) nbar_sync(BAR_TILE, 64);   // tile kb has block kb - 1's update
         double x[2][BSD];
 #pragma unroll
         for (int r = 0; r < 2; ++r)
@@ -680,13 +685,16 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
 #pragma unroll
           for (int j = 0; j < BSD; j += 2)
             *reinterpret_cast<double2*>(M + mix(lane + 32 * r, 8 * kb + j)) = make_double2(x[r][j], x[r][j + 1]);
-        nbar_arrive(BAR_PANEL);              // panel kb (W - S) and its record are stored
+        nbar_arrive(BAR_PANEL, 32 * kFW);    // panel kb (W - S) and its record are stored
       }
     } else {
       // ------------------------------------------------------------ T: the block updates
+      // (T1 = warp 1 takes the look-ahead tile first; with three warps T2 = warp 2 takes the
+      // larger half of the rest)
+      const int tw = warp - 1;
 #pragma unroll 1
       for (int kb = 0; kb < N64 / BSD; ++kb) {
-        nbar_sync(BAR_PANEL);
+        nbar_sync(BAR_PANEL, 32 * kFW);
         double af[8][2];
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
@@ -694,27 +702,43 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
           af[mt][1] = M[mix(8 * mt + g, 8 * kb + 4 + t)];   // A[g][4 + t]
         }
         const int rk0 = rowk[kb * BSD + t], rk1 = rowk[kb * BSD + 4 + t];
-        if (kb + 1 < N64 / BSD) {
+        if (tw == 0 && kb + 1 < N64 / BSD) {
           const int la[1] = {kb + 1};
           f_tiles_update<1>(M, la, af, rk0, rk1, g, t);
           wsync();
-          nbar_arrive(BAR_TILE);
+          nbar_arrive(BAR_TILE, 64);
         }
         if (Xg != nullptr) {
           // the six other tiles (and at the last block tile 0 too), two at a time
+          if constexpr (kFW == 2) {
 #pragma unroll 1
-          for (int j = 2; j < 8; j += 2) {
-            const int pr[2] = {(kb + j) & 7, (kb + j + 1) & 7};
-            f_tiles_update<2>(M, pr, af, rk0, rk1, g, t);
-          }
-          if (kb + 1 == N64 / BSD) {
-            const int z0[1] = {0};
-            f_tiles_update<1>(M, z0, af, rk0, rk1, g, t);
+            for (int j = 2; j < 8; j += 2) {
+              const int pr[2] = {(kb + j) & 7, (kb + j + 1) & 7};
+              f_tiles_update<2>(M, pr, af, rk0, rk1, g, t);
+            }
+            if (kb + 1 == N64 / BSD) {
+              const int z0[1] = {0};
+              f_tiles_update<1>(M, z0, af, rk0, rk1, g, t);
+            }
+          } else {
+            if (tw == 0) {
+              const int pr[2] = {(kb + 2) & 7, (kb + 3) & 7};
+              f_tiles_update<2>(M, pr, af, rk0, rk1, g, t);
+              if (kb + 1 == N64 / BSD) {
+                const int z0[1] = {0};
+                f_tiles_update<1>(M, z0, af, rk0, rk1, g, t);
+              }
+            } else {
+              const int p1[2] = {(kb + 4) & 7, (kb + 5) & 7};
+              f_tiles_update<2>(M, p1, af, rk0, rk1, g, t);
+              const int p2[2] = {(kb + 6) & 7, (kb + 7) & 7};
+              f_tiles_update<2>(M, p2, af, rk0, rk1, g, t);
+            }
           }
         } else {
           // determinant-only run: only the tiles right of the next panel
 #pragma unroll 1
-          for (int nt = kb + 2; nt < 8; ++nt) {
+          for (int nt = kb + 2 + (kFW == 3 ? tw : 0); nt < 8; nt += kFW - 1) {
             const int one[1] = {nt};
             f_tiles_update<1>(M, one, af, rk0, rk1, g, t);
           }
@@ -765,7 +789,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
     // warp stores its half of the rows and loads the next matrix's same half under the store
     loaded = false;
     rm_next = 0.0;
-    if (Xg != nullptr) {
+    if (Xg != nullptr && io) {
       double* Xi = Xg + item * (N64 * N64);
       const int oc0 = rowk[lane], oc1 = rowk[lane + 32];
       const int64_t nitem = item + gridDim.x;
@@ -825,7 +849,7 @@ cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
   int per_sm = 0;
 #if GJ_K2E_TWO_WARPS
   auto kern = gj_batched64f_kernel;
-  const int threads = 64;
+  const int threads = 32 * kFW;
 #else
   auto kern = a.Ainv != nullptr ? gj_batched64e_kernel<GJ_K2E_LA != 0> : gj_batched64e_kernel<false>;
   const int threads = 32;
