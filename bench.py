@@ -234,12 +234,53 @@ def c4_measure(dev, reps: int = 3):
     fl = 2.0 * n ** 3 - n ** 2
     peak, src = compute_peaks()
     tf = fl / (ms / 1e3) / 1e12
+    k4b = k4b_measure(dev, A, n, peak, src)
     return {"workload": "C4: one fp64 8192x8192 N(0,1)/sqrt(n), seed 3 (BASELINE.json configs[3])",
             "metric": "fp64 GFLOP/s at n=8192", "value": tf * 1e3, "unit": "GFLOP/s", "ms": ms, "reps": reps,
             "logabsdet": float(outs[1].item()), "sign": int(outs[2].item()), "info": int(outs[3].item()),
             "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
                          "traffic": None, "peak_source": src,
-                         "kernel": "whole gj_invert (leaf_kernel panels overlapped with gemm_update_kernel DMMA)"}}
+                         "kernel": "whole gj_invert (leaf_kernel panels overlapped with the K4b DMMA trailing update)"},
+            "roofline_dominant_kernel": k4b}
+
+
+def k4b_measure(dev, A, n, peak, src, reps: int = 5):
+    """The dominant kernel of C4 alone: K4b (dgemm_tma_kernel), one panel's trailing update
+    at n = 8192 through gj_dist_step_update (one rank: the same kernel gj_invert launches per
+    panel, with its 128-row transposed gather), timed with CUDA events on the launching stream."""
+    import torch
+    from paper_1401_7962_b200.dist import BLOCK, CudaSteps, sizes
+    npad, nl, nr = sizes(n, 1, 0)
+    st = CudaSteps(n, 1, 0)
+    X = torch.empty((npad, nl), dtype=torch.float64, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    pos, piv, rq, rr = (torch.empty(npad, **i32) for _ in range(4))
+    rp = torch.empty(npad, dtype=torch.float64, device=dev)
+    W = torch.empty((npad, BLOCK), dtype=torch.float64, device=dev)
+    R = torch.empty((BLOCK, nl), dtype=torch.float64, device=dev)
+    smax = torch.zeros(1, dtype=torch.int64, device=dev)
+    st.init(A, n, X, pos, piv, smax)
+    st.factor(0, X, pos, piv, rp, rq, rr, W)
+    st.update(0, 0, X, W, piv, rr, R)
+    torch.cuda.synchronize(dev)
+    s = torch.cuda.current_stream(dev)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        st.update(0, 0, X, W, piv, rr, R)
+        b.record(s)
+        torch.cuda.synchronize(dev)
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    fl = 2.0 * npad * (nl - BLOCK) * BLOCK
+    tf = fl / (ms / 1e3) / 1e12
+    del X, W, R
+    torch.cuda.empty_cache()
+    return {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak, "traffic": None,
+            "peak_source": src, "kernel": "dgemm_tma_kernel<8> (K4b) incl. gather_rows_T_kernel, all 148 SMs",
+            "flops_per_launch": fl, "ms_per_launch": ms,
+            "algorithmic": "2 * 8192 * 8064 * 128 flops: one 128-column panel's update of the other columns"}
 
 
 def f1_measure(dev, reps: int = 3):
