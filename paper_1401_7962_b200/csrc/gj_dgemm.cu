@@ -89,8 +89,10 @@ __device__ __forceinline__ int real_col(const DgemmArgs& g, int nc) {
   return (g.skip_hi > g.skip_lo && c >= g.skip_lo) ? c + (g.skip_hi - g.skip_lo) : c;
 }
 
-// Tile schedule: CTA b takes the contiguous range [T b / G, T (b + 1) / G) of the M-major tile
-// order, so it reloads its A block about once.  (Measured and dropped: a counter-based dynamic
+// Tile schedule: CTA b takes a contiguous range of the M-major tile order, so it reloads its A
+// block about once.  The ranges are weighted (DgemmArgs::late_from / late_w): launched beside
+// the panel kernel, the last CTAs of the grid wait for the panel kernel's SMs and get shorter
+// ranges sized to the time left after it ends.  (Measured and dropped: a counter-based dynamic
 // schedule and work stealing from the back of the ranges, meant to put the panel kernel's 16
 // SMs to work once it ends — the A reloads they cost outweighed the gain: C4 40.8 / 44.4 ms
 // against 40.6 ms static; tools/timeline_large.py.)
@@ -124,14 +126,25 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) dgemm_tma_kernel(DgemmArgs g
     fence_mbar_init();
   }
   __syncthreads();
+#ifdef GJ_TIMELINE
+  const bool tl = g.N > TK && g.rep_lo % 128 == 0;   // trailing updates only: per panel
+  if (threadIdx.x == 0 && tl) {
+    atomicMin(&g_tlg[0][g.rep_lo / 128], gtime());
+    atomicMax(&g_tlg[2][g.rep_lo / 128], gtime());
+  }
+#endif
 
   if (warp == CW) {
     // ---------------------------------------------------------------- producer
     if (lane == 0) {
       // the range as one chunk; the next tile is known one chunk ahead, so the consumers can
       // prefetch its C
-      int64_t static_next = T * blockIdx.x / gridDim.x;
-      const int64_t static_end = T * (blockIdx.x + 1) / gridDim.x;
+      auto wcum = [&](int64_t b) -> int64_t {
+        return b <= g.late_from ? b * 1024 : (int64_t)g.late_from * 1024 + (b - g.late_from) * g.late_w;
+      };
+      const int64_t wtot = wcum(gridDim.x);
+      int64_t static_next = T * wcum(blockIdx.x) / wtot;
+      const int64_t static_end = T * wcum(blockIdx.x + 1) / wtot;
       auto claim = [&](int64_t& a, int64_t& b) {
         a = static_next;
         b = static_end;

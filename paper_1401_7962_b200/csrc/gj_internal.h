@@ -71,6 +71,10 @@ struct DgemmArgs {
   int c_base, skip_lo, skip_hi;
   const int* pivstep;   // replace(i) = pivstep[i] in [rep_lo, rep_hi)
   int rep_lo, rep_hi;
+  // Tile-range weights: CTAs [0, late_from) take weight 1024 each, CTAs from late_from on
+  // take late_w each (late_from >= the grid: uniform ranges).  The late CTAs are the ones
+  // that only become resident when the panel kernel beside this launch frees its SMs.
+  int late_from = 1 << 30, late_w = 1024;
 };
 bool dgemm_tma_supported(const DgemmArgs& g);
 // cudaErrorNotSupported if the arguments do not suit it (the caller falls back to K4).

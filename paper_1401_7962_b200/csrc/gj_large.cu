@@ -53,13 +53,34 @@ __global__ void init_perm_kernel(int n, int* pos, int* pivstep) {
   }
 }
 
-// X (npad x npad, ld npad) = blockdiag(A, I)
-__global__ void copy_pad_kernel(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ X, int npad) {
-  const int64_t tot = (int64_t)npad * npad;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / npad), j = (int)(e - (int64_t)i * npad);
-    X[e] = (i < n && j < n) ? A[(int64_t)i * lda + j] : (i == j ? 1.0 : 0.0);
+// X (npad x npad, ld npad) = blockdiag(A, I) and max |a_ij| (the bit pattern of a non-negative
+// double, atomicMax on u64 is monotone; fmax: a NaN never wins) in one pass over A: one row of
+// X per CTA iteration (coalesced)
+__global__ void copy_pad_absmax_kernel(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ X,
+                                       int npad, unsigned long long* out) {
+  double m = 0.0;
+  for (int i = blockIdx.x; i < npad; i += gridDim.x) {
+    const double* a = A + (int64_t)i * lda;
+    double* x = X + (int64_t)i * npad;
+    if (i < n) {
+#pragma unroll 4
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double v = __ldcs(a + j);
+        m = fmax(m, fabs(v));
+        x[j] = v;
+      }
+      for (int j = n + threadIdx.x; j < npad; j += blockDim.x) x[j] = 0.0;
+    } else {
+      for (int j = threadIdx.x; j < npad; j += blockDim.x) x[j] = i == j ? 1.0 : 0.0;
+    }
   }
+  unsigned long long b = (unsigned long long)__double_as_longlong(m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+    b = ob > b ? ob : b;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, b);
 }
 
 // max |a_ij| as the bit pattern of a non-negative double (atomicMax on u64 is monotone)
@@ -115,6 +136,24 @@ __global__ void unpermute_kernel(const double* __restrict__ X, int npad, const i
     const double* src = X + (int64_t)rec_row[k] * npad;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
       Y[(int64_t)k * ldy + j] = src[pivstep[j]];
+  }
+}
+
+// unpermute_kernel with the source row staged in shared memory (npad doubles): the row is read
+// once, coalesced, and the column gather runs out of shared memory
+constexpr int kUnpermSmemMaxN = 26624;   // 208 KB
+__global__ void __launch_bounds__(512) unpermute_smem_kernel(const double* __restrict__ X, int npad,
+                                                             const int* __restrict__ rec_row,
+                                                             const int* __restrict__ pivstep, int n,
+                                                             double* __restrict__ Y, int64_t ldy) {
+  extern __shared__ double srow[];
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const double2* src = reinterpret_cast<const double2*>(X + (int64_t)rec_row[k] * npad);
+    for (int j = threadIdx.x; j < npad / 2; j += blockDim.x) reinterpret_cast<double2*>(srow)[j] = __ldcs(src + j);
+    __syncthreads();
+    double* y = Y + (int64_t)k * ldy;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) __stcs(y + j, srow[__ldg(pivstep + j)]);
+    __syncthreads();
   }
 }
 
@@ -885,6 +924,28 @@ static bool leaf_cfg(int npad, LeafCfg* c) {
   return false;
 }
 
+// K4b launched beside the panel kernel: the whole grid, its last `cl` CTAs (resident only once
+// the panel kernel's SMs are free) weighted by the share of the update left when it ends.
+// The panel kernel's time relative to the update's (ncols columns) is modelled from the
+// tools/timeline_large.py measurements on B200 (leaf / update on the other SMs: 400 / 592 us
+// at n = 8192, 3175 / 9503 us at n = 32768: the leaf grows as npad^1.5, the update as
+// npad * ncols); 0.9 covers a late CTA's start (its A block, the pipeline fill).  A wrong
+// weight only moves time between CTAs: the tiles and their arithmetic are the same.
+#ifndef GJ_DGEMM_LATE_W
+#define GJ_DGEMM_LATE_W -1
+#endif
+static void late_ranges(DgemmArgs& d, int sms, int cl, int npad) {
+  d.late_from = sms - cl;
+  if (GJ_DGEMM_LATE_W >= 0) {   // A/B builds
+    d.late_w = GJ_DGEMM_LATE_W;
+    return;
+  }
+  const double ncols = d.N > 0 ? (double)d.N : 1.0;
+  const double leaf_over_update = 0.675 * sqrt(8192.0 * npad) / ncols;
+  const double w = 1024.0 * 0.9 * (1.0 - leaf_over_update);
+  d.late_w = w > 0.0 ? (int)w : 0;
+}
+
 // Diagnostic builds only (-DGJ_DEBUG_SYNC: synchronise and check after every launch;
 // -DGJ_LARGE_NO_PDL: no overlap of the trailing update with the next panel).
 static constexpr bool debug_sync() {
@@ -1230,9 +1291,8 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
   cudaError_t e;
   const int sms = device_sm_count();
   init_perm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(npad, w.pos, w.pivstep);
-  copy_pad_kernel<<<sms * 8, 256, 0, s>>>(A, lda, n, w.X, npad);
   cudaMemsetAsync(w.smax, 0, 8, s);
-  absmax_kernel<<<sms * 8, 256, 0, s>>>(A, lda, n, w.smax);
+  copy_pad_absmax_kernel<<<sms * 8, 256, 0, s>>>(A, lda, n, w.X, npad, w.smax);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   GJ_DBG("setup");
 
@@ -1289,7 +1349,8 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
         db.N = npad - P1 - pw1;
         db.skip_lo = 0;
       }
-      if ((e = launch_dgemm_tma(db, grid_sms, pdl, s)) != cudaSuccess) return e;
+      if (pdl) late_ranges(db, sms, lc.cl, npad);
+      if ((e = launch_dgemm_tma(db, pdl ? sms : 0, pdl, s)) != cudaSuccess) return e;
     } else {
       GemmArgs gb{w.X + P0, npad, w.R, npad, w.X, npad, npad, npad - pw - pw1, pw, w.pivstep, P0, P0 + pw, P0, P1 + pw1};
       if (det_only) {   // only the columns right of panel k+1
@@ -1301,8 +1362,24 @@ cudaError_t invert_large_f64(int n, const double* A, int64_t lda, double* Ainv, 
     }
     GJ_DBG("trailing gemm");
   }
-  if (Ainv != nullptr)
-    unpermute_kernel<<<dim3((n + 255) / 256, n < 65535 ? n : 65535), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n, Ainv, ldainv);
+  if (Ainv != nullptr) {
+    if (npad <= kUnpermSmemMaxN) {
+      const int smem = npad * 8;
+      static unsigned long long configured = 0;
+      const unsigned long long dbit = device_bit();
+      if (!(configured & dbit)) {
+        if ((e = cudaFuncSetAttribute(unpermute_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kUnpermSmemMaxN * 8)) != cudaSuccess)
+          return e;
+        configured |= dbit;
+      }
+      unpermute_smem_kernel<<<sms * (smem <= 72 * 1024 ? 3 : 1), 512, smem, s>>>(w.X, npad, w.rec_row, w.pivstep, n,
+                                                                                  Ainv, ldainv);
+    } else {
+      unpermute_kernel<<<dim3((n + 255) / 256, n < 65535 ? n : 65535), 256, 0, s>>>(w.X, npad, w.rec_row, w.pivstep, n,
+                                                                                     Ainv, ldainv);
+    }
+  }
   finalize_kernel<<<1, 1024, 0, s>>>(n, w.rec_p, w.rec_q, tol, w.smax, ipiv, logabsdet, sign, det, info);
   return cudaGetLastError();
 }
@@ -1646,7 +1723,8 @@ cudaError_t dist_update(int n, int P, int rank, int k, int part, double* Xl, con
     d.N = nl - (hi - lo);
     d.skip_lo = lo;
     d.skip_hi = hi;
-    return launch_dgemm_tma(d, device_sm_count() - lc.cl, true, s);
+    late_ranges(d, device_sm_count(), lc.cl, npad);
+    return launch_dgemm_tma(d, device_sm_count(), true, s);
   }
   GemmArgs g{W, dist::DB, R, nl, Xl, nl, npad, nl - (hi - lo), dist::DB, pivstep, k0, k0 + dist::DB, lo, hi};
   return launch_gemm(g, s, device_sm_count() - lc.cl, true);

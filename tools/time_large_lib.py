@@ -8,7 +8,8 @@ import torch
 sys.path.insert(0, ".")
 import synth  # noqa: E402
 
-n = 8192
+import os
+n = int(os.environ.get("GJ_N", "8192"))
 A = torch.from_numpy(synth.gen_gaussian(n, seed=3)).cuda()
 X = torch.empty_like(A)
 ip = torch.empty(n, dtype=torch.int32, device="cuda")
