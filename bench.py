@@ -581,7 +581,7 @@ def run_c5(args, rank, world, local):
 def c3_measure(dev, reps: int = 5):
     """BASELINE configs[2] as a secondary key of the headline line: 262,144 x 64 x 64 fp64
     (A = P L diag(u), 1% duplicated-row items, seed 2), tol 1e-10, through gj_invert_batched
-    (K2e).  FP64 roofline: 2n^3 - n^2 flops per item at the derived DFMA/DMMA peak."""
+    (K2f).  FP64 roofline: 2n^3 - n^2 flops per item at the derived DFMA/DMMA peak."""
     import torch
     import paper_1401_7962_b200 as gj
     import synth
@@ -620,7 +620,7 @@ def c3_measure(dev, reps: int = 5):
            "ms": ms, "reps": reps, "singular_items": int((info != 0).sum().item()),
            "roofline": {"bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
                         "traffic": None, "peak_source": src,
-                        "kernel": "gj_batched64e_kernel (K2e: one warp per matrix, shared-memory resident, DMMA "
+                        "kernel": "gj_batched64f_kernel (K2f: panel warp + trailing warp per matrix, shared-memory resident, DMMA "
                                   "blocked update)",
                         "hbm_achieved_gbs": byts / (ms / 1e3) / 1e9, "hbm_peak_gbs": hbm}}
     del A, X
@@ -630,7 +630,7 @@ def c3_measure(dev, reps: int = 5):
 
 def run_c3(args, rank, world, local):
     """BASELINE configs[2]: 262,144 x 64 x 64 fp64 (A = P L diag(u), 1% of the items with a
-    duplicated row, seed 2), tol 1e-10 (reading G1), K2e.  Each rank inverts its own batch
+    duplicated row, seed 2), tol 1e-10 (reading G1), K2f.  Each rank inverts its own batch
     (weak scaling, no collective).  Roofline: the FP64 pipe (DFMA; 2n^3 - n^2 flops per item)
     and HBM (inputs + inverse + ipiv + det outputs)."""
     import torch
@@ -698,7 +698,7 @@ def run_c3(args, rank, world, local):
                        "n": n, "parallelism": f"dp{world} (independent shards, no collective)",
                        "l2": "inputs (8 GiB/GPU) larger than L2 (126 MB); no flush needed"},
             "roofline": {"bound": "fp64", "achieved": tf, "peak": dfma_peak, "unit": "TFLOP/s",
-                         "frac": tf / dfma_peak, "traffic": None, "kernel": "gj_batched64e_kernel (K2e: one warp per matrix, shared-memory resident, DMMA blocked update)",
+                         "frac": tf / dfma_peak, "traffic": None, "kernel": "gj_batched64f_kernel (K2f: panel warp + trailing warp per matrix, shared-memory resident, DMMA blocked update)",
                          "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md unit counts)",
                          "hbm_achieved_gbs": byts / (ms / 1e3) / 1e9, "hbm_peak_gbs": hbm},
             "singular_items": int((info != 0).sum().item()), "gpu_launches": args.steps, "clocks": clk.summary()}),

@@ -202,7 +202,7 @@ def test_zero_pivot_not_singular(gj, torch):
 # ------------------------------------------------------------------ other entry points
 @pytest.mark.parametrize("n,dtype", [(20, np.float64), (64, np.float64), (32, np.float32), (48, np.float32)])
 def test_det_entry_matches_invert(gj, torch, n, dtype):
-    """gj_det (Ainv = NULL) — the det-only kernels (K1s for fp32 n = 32, K2e skipping the
+    """gj_det (Ainv = NULL) — the det-only kernels (K1s for fp32 n = 32, K2f skipping the
     compact D columns for fp64 n = 64) give bitwise the inverting path's pivots and dets."""
     A = synth.gen_normal_batch(700, n, seed=9, dtype=dtype)
     A[5, 3] = A[5, 1]   # a singular item

@@ -1,6 +1,6 @@
 """Edge cases added in round 2:
 
-* an 8-byte-aligned (not 16-byte-aligned) fp64 n = 64 batch — K2e's 16-byte vector loads
+* an 8-byte-aligned (not 16-byte-aligned) fp64 n = 64 batch — K2f's 16-byte vector loads
   cannot take it, the launcher must route it to the generic K2 (same oracle rules), not fault;
 * the largest order the large-n path accepts, n = GJ_LARGE_MAX_N = 65536, through the
   C-ABI gj_invert: the Sylvester-Hadamard pin P6 (every pivot step an exact tie; the exact

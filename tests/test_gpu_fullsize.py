@@ -6,7 +6,7 @@ size (exact pins, library cross-checks of det / pivots, residual rows).
   (the bench's K1b kernel), oracle on a sample spread over the batch incl. its ragged end.
 * C2 and C3 also EVERY item against the oracle (chunked; SURVEY §8d's oracle plan: "every
   report run, all items").
-* C3 (configs[2]): the whole 262,144-item fp64 batch (K2e), every singular flag against the
+* C3 (configs[2]): the whole 262,144-item fp64 batch (K2f), every singular flag against the
   generator's list (R7), oracle on a sample incl. singular items.
 * C5 (configs[4]) at 32768: the P6 Sylvester–Hadamard pin (exact inverse A^T / n, every
   pivot step an exact tie) through the single-GPU path and through the distributed driver
@@ -115,7 +115,7 @@ def test_c3_full_sampled(gj, torch):
 
 
 def test_c3_every_item(gj, torch):
-    """The whole C3 batch (262,144 fp64 64 x 64, 1% singular) in one call (K2e), EVERY item
+    """The whole C3 batch (262,144 fp64 64 x 64, 1% singular) in one call (K2f), EVERY item
     against the oracle with the flat fp64 bounds (C3 is well-conditioned under
     reading G15) and every singular flag exact."""
     A, S = synth.gen_c3(return_singular=True)

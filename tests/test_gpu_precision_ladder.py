@@ -11,7 +11,7 @@ element division, no FMA) on 2,000 Gaussian items and gets max e/(kappa eps) = 0
 textbook algorithm's own level, not above it.  The large-n paths (blocked, 128-column
 panels) are much lower because kappa_inf of an n = 300..1024 Gaussian matrix grows faster
 than the max-entry error.
-Measured on Gaussian inputs through each kernel family (K1/K1b, K2/K2e, K6, K7/K1s, the
+Measured on Gaussian inputs through each kernel family (K1/K1b, K2/K2f, K6, K7/K1s, the
 blocked large-n path in both dtypes)."""
 import numpy as np
 import pytest

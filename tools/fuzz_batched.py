@@ -3,7 +3,7 @@ not a test: `python tools/fuzz_batched.py [trials] [seed]`).  Per trial: a dtype
 n in 1..64, a batch size (ragged against every kernel's task size) and an input family —
 Gaussian, graded rows (1e-6..1e6), small integers (exact ties), near-singular (a row
 duplicated and perturbed by 1e-9), exactly singular items mixed in, diagonally dominant,
-scaled signed permutations, all-zero items — through gj_invert_batched (K1/K1b/K2/K2e),
+scaled signed permutations, all-zero items — through gj_invert_batched (K1/K1b/K2/K2f),
 gj_det, gj_solve_batched (K1s/K7, n <= 32) and full pivoting (K6, n <= 32), compared with
 the oracle under the rules of tests/parity.py.  Prints one line per failing trial and a
 summary."""

@@ -1,4 +1,4 @@
-"""C3-sized fp64 n = 64 batch: det-only (gj_det, K2e without the D columns) vs the inverse; bitwise equality of the det outputs and both times."""
+"""C3-sized fp64 n = 64 batch: det-only (gj_det, K2f without the D columns) vs the inverse; bitwise equality of the det outputs and both times."""
 import sys, numpy as np, torch
 sys.path.insert(0, ".")
 import paper_1401_7962_b200 as gj, synth
