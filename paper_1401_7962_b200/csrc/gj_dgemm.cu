@@ -192,6 +192,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) dgemm_tma_kernel(DgemmArgs g
   // ------------------------------------------------------------------ consumers
   const int wm = warp / WN, wn = warp % WN;
   const int gq = lane >> 2, tq = lane & 3;
+  // Fragment row of lane group gq: rho(gq) = 0, 2, 4, 6, 1, 3, 5, 7.  An 8-byte fragment load
+  // is served per half-warp (gq 0..3, 4..7); under the 128-byte swizzle (chunk ^ row mod 8)
+  // rows r and r ^ 1 use the same two chunks, so the four rows of a half-warp must differ in
+  // (r >> 1): with rho the A loads (and the B loads, whose rows gather_rows_T_kernel stores in
+  // the same order) are conflict-free — ncu: half the shared wavefronts were bank conflicts.
+  // A row permutation of the warp tile is free for A and C (rows are independent).
+  const int gr = ((gq & 3) << 1) | (gq >> 2);
   double acc[2][NT][4], cpre[2][NT][4];
   int kpre[2][2];   // pivstep of the prefetched rows (replace test applied when C is consumed)
 
@@ -205,7 +212,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) dgemm_tma_kernel(DgemmArgs g
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = m * TM + wm * 32 + mt * 16 + gq + 8 * h;
+        const int r = m * TM + wm * 32 + mt * 16 + gr + 8 * h;
         const bool in = r < g.M;
         kp[mt][h] = in ? __ldg(g.pivstep + r) : g.rep_lo;   // rows outside: "replaced" (0)
 #pragma unroll
@@ -259,13 +266,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) dgemm_tma_kernel(DgemmArgs g
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          af[mt][2 * i] = lds64(ab + boxoff(wm * 32 + mt * 16 + gq, tq + 4 * i));
-          af[mt][2 * i + 1] = lds64(ab + boxoff(wm * 32 + mt * 16 + gq + 8, tq + 4 * i));
+          af[mt][2 * i] = lds64(ab + boxoff(wm * 32 + mt * 16 + gr, tq + 4 * i));
+          af[mt][2 * i + 1] = lds64(ab + boxoff(wm * 32 + mt * 16 + gr + 8, tq + 4 * i));
         }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) bf[nt][i] = lds64(bb + boxoff(wn * WTN + nt * 8 + gq, tq + 4 * i));
+        for (int i = 0; i < 4; ++i) bf[nt][i] = lds64(bb + boxoff(wn * WTN + nt * 8 + gr, tq + 4 * i));
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) dgemm_tma_kernel(DgemmArgs g
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = m * TM + wm * 32 + mt * 16 + gq + 8 * h;
+        const int r = m * TM + wm * 32 + mt * 16 + gr + 8 * h;
         if (r >= g.M) continue;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {

@@ -112,8 +112,11 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ld, con
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) dst[j] = src[j];
 }
 
-// RT[c][s] = X[rows[s]][c] for s < 128, c < ncols (the pivot rows transposed, K-major, for
-// K4b's B operand); 32 x 32 tiles through shared memory, grid (ceil(ncols / 32), 4), block (32, 8)
+// RT[rt(c)][s] = X[rows[s]][c] for s < 128, c < ncols (the pivot rows transposed, K-major, for
+// K4b's B operand), with column c of each aligned group of 8 stored at position
+// rt(c) = (c & ~7) | rho(c & 7), rho = 0, 2, 4, 6, 1, 3, 5, 7: K4b's lane group g reads
+// position rho(g) of its 8-row group, which keeps its fragment loads conflict-free
+// (gj_dgemm.cu); 32 x 32 tiles through shared memory, grid (ceil(ncols / 32), 4), block (32, 8)
 __global__ void gather_rows_T_kernel(const double* __restrict__ X, int64_t ld, const int* __restrict__ rows, int ncols,
                                      double* __restrict__ RT) {
   __shared__ double tile[32][33];
@@ -125,7 +128,8 @@ __global__ void gather_rows_T_kernel(const double* __restrict__ X, int64_t ld, c
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int c = c0 + i;
-    if (c < ncols) RT[(int64_t)c * 128 + s0 + threadIdx.x] = tile[threadIdx.x][i];
+    const int rc = (c & ~7) | (((c & 3) << 1) | ((c >> 2) & 1));
+    if (c < ncols) RT[(int64_t)rc * 128 + s0 + threadIdx.x] = tile[threadIdx.x][i];
   }
 }
 
