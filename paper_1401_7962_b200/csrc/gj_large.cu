@@ -933,8 +933,10 @@ static bool leaf_cfg(int npad, LeafCfg* c) {
 // The panel kernel's time relative to the update's (ncols columns) is modelled from the
 // tools/timeline_large.py measurements on B200 (leaf / update on the other SMs: 400 / 592 us
 // at n = 8192, 3175 / 9503 us at n = 32768: the leaf grows as npad^1.5, the update as
-// npad * ncols); 0.9 covers a late CTA's start (its A block, the pipeline fill).  A wrong
-// weight only moves time between CTAs: the tiles and their arithmetic are the same.
+// npad * ncols); 0.85 covers a late CTA's start (its A block, the pipeline fill) and keeps a
+// margin: at n = 8192 weights 240..300 measure alike but 330 costs 4% (the late CTAs then
+// finish last).  A wrong weight only moves time between CTAs: the tiles and their
+// arithmetic are the same.
 #ifndef GJ_DGEMM_LATE_W
 #define GJ_DGEMM_LATE_W -1
 #endif
@@ -946,7 +948,7 @@ static void late_ranges(DgemmArgs& d, int sms, int cl, int npad) {
   }
   const double ncols = d.N > 0 ? (double)d.N : 1.0;
   const double leaf_over_update = 0.675 * sqrt(8192.0 * npad) / ncols;
-  const double w = 1024.0 * 0.9 * (1.0 - leaf_over_update);
+  const double w = 1024.0 * 0.85 * (1.0 - leaf_over_update);
   d.late_w = w > 0.0 ? (int)w : 0;
 }
 
