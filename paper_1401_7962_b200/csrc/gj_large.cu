@@ -343,13 +343,82 @@ __device__ __forceinline__ void leaf_update(T (&x)[W], const T* y, T nf, T dcol)
   }
 }
 
+// Row stride (elements) of the leaf's pivot rows Rs in shared memory: the B-fragment loads of
+// leaf_update_mma (lanes (g, t) read Rs[t][c + g]) then hit distinct banks per half-warp (fp64)
+// or per warp (fp32)
+template <typename T>
+constexpr int rs_ld() {
+  return sizeof(T) == 8 ? 132 : 136;
+}
+
+__device__ __forceinline__ void dmma884_leaf(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// The leaf's update of the panel's other columns for one warp's 32 rows [r0, r0 + 32) (the
+// aggregated Eqs. (14)-(15) within a panel, as in K4b):
+//     X[i][P0 + c] = (rep_i ? 0 : X[i][P0 + c]) + sum_s x_i[s] Rs[s][c]
+// for c in [0, pw) outside the leaf's columns [off, off + W), rep_i = row i was pivoted in this
+// leaf.  FP64 m8n8k4 MMAs (fp32 data converted exactly, accumulated in fp64): A = the rows'
+// leaf columns (just written back to X by this warp), B = the leaf's pivot rows (Rs), C = X,
+// NCH 8-column tiles at a time.  Why: as per-thread FMAs every Rs element was a broadcast
+// shared load feeding two FMAs, and these updates took more of the panel kernel than its
+// pivot steps (232 against 168 us per n = 8192 panel, fp64; tools/leaf_prof.sh).
+template <typename T, int W>
+__device__ __forceinline__ void leaf_update_mma(T* X, int64_t ld, int npad, int P0, int pw, int off, int r0,
+                                                bool rep_mine, const T* Rs, int lane) {
+  constexpr int RSLD = rs_ld<T>();
+  constexpr int NCH = 8;    // 8-column tiles per pass (one pass covers 64 columns)
+  constexpr int KS = W / 4; // k4 steps
+  const int g = lane >> 2, t = lane & 3;
+  const int ntiles = pw / 8;
+  const int lt0 = (off + 7) / 8, lt1 = (off + W) / 8;   // tiles wholly inside the leaf
+#pragma unroll 1
+  for (int mt = 0; mt < 4; ++mt) {
+    const int row = r0 + 8 * mt + g;
+    const bool ok = row < npad;
+    const bool rep = __shfl_sync(0xffffffffu, rep_mine, 8 * mt + g);
+    T* cr = X + (int64_t)(ok ? row : 0) * ld + P0;
+#pragma unroll 1
+    for (int nt0 = 0; nt0 < ntiles; nt0 += NCH) {
+      // A (the row's leaf columns k = 4 kk + t) and C of every tile of the pass: all loads
+      // issue together, one memory latency per pass
+      double av[KS];
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) av[kk] = ok ? (double)cr[off + 4 * kk + t] : 0.0;
+      double c[NCH][2];
+      bool act[NCH], wr[NCH];
+#pragma unroll
+      for (int u = 0; u < NCH; ++u) {
+        const int nt = nt0 + u, col = 8 * nt + 2 * t;
+        act[u] = nt < ntiles && !(nt >= lt0 && nt < lt1);
+        wr[u] = act[u] && ok && !(col >= off && col < off + W);   // W = 4: the leaf's half of a tile
+        T v0 = T(0), v1 = T(0);
+        if (wr[u] && !rep) ld2(cr + col, v0, v1);
+        c[u][0] = (double)v0;
+        c[u][1] = (double)v1;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int u = 0; u < NCH; ++u)
+          if (act[u]) dmma884_leaf(c[u][0], c[u][1], av[kk], (double)Rs[(4 * kk + t) * RSLD + 8 * (nt0 + u) + g]);
+#pragma unroll
+      for (int u = 0; u < NCH; ++u)
+        if (wr[u]) st2(cr + 8 * (nt0 + u) + 2 * t, (T)c[u][0], (T)c[u][1]);
+    }
+  }
+}
+
 // Shared-memory layout of the leaf kernel (bytes); T elements
 template <typename T, int W>
 struct LeafSmem {
   static constexpr int KEYT = 16 / (int)sizeof(T);        // the 16-byte key in T units
   static constexpr int EXW = W + KEYT;                    // entry: key + W row values (T units)
-  static constexpr int RS = 0;                            // [W][PANEL_MAX] pivot rows of a leaf
-  static constexpr int PROW = RS + W * 128 * (int)sizeof(T);   // [W] pivot row ids of the current leaf
+  static constexpr int RS = 0;                            // [W][rs_ld] pivot rows of a leaf (panel columns)
+  static constexpr int PROW = RS + W * rs_ld<T>() * (int)sizeof(T);   // [W] pivot row ids of the current leaf
   // [2][kLeafThreads/32][EXW] warp winners, double-buffered by step parity: the bulk copies
   // of step k read their source asynchronously, and only the wait of step k+1 proves (via
   // the peers' step-(k+1) entries) that every peer has received — so the copy has read —
@@ -383,6 +452,9 @@ __device__ unsigned long long g_leaf_prof[8];
 template <typename T, int W, int RPT>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef GJ_LEAF_PROF
+  const long long tk0 = clock64();
+#endif
 #ifdef GJ_TIMELINE
   if (threadIdx.x == 0 && blockIdx.x == 0 && a.c0 % 128 == 0) g_tl[0][a.c0 / 128] = gtime();
 #endif
@@ -570,6 +642,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
       for (int j = 0; j < W; j += 2) st2(dst + j, x[i][j], x[i][j + 1]);
     }
     if (pw > W) {
+#ifdef GJ_LEAF_PROF
+      const long long tu0 = clock64();
+#endif
       // the leaf's transformation on the panel's other columns (left: D columns of earlier
       // leaves, right: columns still to be factored), for this CTA's rows
       cluster_sync_all();   // every CTA's earlier updates of the pivot rows are visible
@@ -578,44 +653,20 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         const int sidx = e / half, cc2 = e - sidx * half;
         T u0, u1;
         ld2(X + (int64_t)prow[sidx] * ld + P0 + 2 * cc2, u0, u1);
-        st2(Rs + sidx * 128 + 2 * cc2, u0, u1);
+        st2(Rs + sidx * rs_ld<T>() + 2 * cc2, u0, u1);
       }
       cluster_sync_all();   // every CTA has its copy before any CTA rewrites a pivot row
-      constexpr int CH = W < 8 ? W : 8;   // columns per chunk: never straddles the leaf
-#pragma unroll 1
-      for (int t0 = 0; t0 < pw; t0 += CH) {
-        if (t0 >= c0 - P0 && t0 < c0 - P0 + W) continue;
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          if (!valid[i]) continue;
-          const bool rep = pst[i] >= s0 && pst[i] < s0 + W;   // pivot row of this leaf: replaced
-          T* row = X + (int64_t)rowid[i] * ld + P0 + t0;
-          T v[CH];
-#pragma unroll
-          for (int j = 0; j < CH; j += 2) {
-            if (rep) {
-              v[j] = T(0);
-              v[j + 1] = T(0);
-            } else {
-              ld2(row + j, v[j], v[j + 1]);
-            }
-          }
-#pragma unroll
-          for (int sidx = 0; sidx < W; ++sidx) {
-            const T* rr = Rs + sidx * 128 + t0;
-#pragma unroll
-            for (int j = 0; j < CH; j += 2) {
-              T r0, r1;
-              ld2(rr + j, r0, r1);
-              v[j] = fma(x[i][sidx], r0, v[j]);
-              v[j + 1] = fma(x[i][sidx], r1, v[j + 1]);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < CH; j += 2) st2(row + j, v[j], v[j + 1]);
-        }
+      for (int i = 0; i < RPT; ++i) {
+        const int r0 = (int)(rank * (kLeafThreads * RPT)) + i * kLeafThreads + warp * 32;
+        if (r0 >= npad) continue;   // warp-uniform
+        const bool rep = valid[i] && pst[i] >= s0 && pst[i] < s0 + W;   // pivot row of this leaf: replaced
+        leaf_update_mma<T, W>(X, ld, npad, P0, pw, c0 - P0, r0, rep, Rs, lane);
       }
       __syncthreads();   // Rs / prow are rewritten by the next leaf
+#ifdef GJ_LEAF_PROF
+      if (tid == 0 && rank == 0) atomicAdd(&g_leaf_prof[7], (unsigned long long)(clock64() - tu0));
+#endif
     }
   }
 #pragma unroll
@@ -634,6 +685,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     }
   }
   cluster_sync_all();   // no CTA leaves while a peer's bulk copy may still target it
+#ifdef GJ_LEAF_PROF
+  if (threadIdx.x == 0 && cluster_rank() == 0) atomicAdd(&g_leaf_prof[0], (unsigned long long)(clock64() - tk0));
+#endif
 #ifdef GJ_TIMELINE
   if (threadIdx.x == 0 && blockIdx.x == 0 && a.c0 % 128 == 0) g_tl[1][a.c0 / 128] = gtime();
 #endif

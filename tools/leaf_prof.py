@@ -33,3 +33,6 @@ for dt, tdt in ((1, torch.float64), (0, torch.float32)):
     print(f"{tdt} n={n}: cycles per step (thread 0, CTA 0), total {tot / n:.0f}")
     for i in range(1, 7):
         print(f"  {names[i]:28s} {out[i] / n:8.0f}  {out[i] / tot * 100:5.1f}%")
+    npan = n // 128
+    print(f"  per panel (us at 1.965 GHz): whole leaf kernel {out[0] / npan / 1965:8.1f}, steps {tot / npan / 1965:8.1f}, "
+          f"intra-panel updates {out[7] / npan / 1965:8.1f}")
