@@ -734,9 +734,19 @@ def max_over_ranks(v: float, world: int, dev) -> float:
     return float(t.item())
 
 
+def json_only_stdout():
+    """Native code writes to fd 1 too (NCCL's version banner on communicator creation, ...):
+    point fd 1 at stderr and keep the original stdout for the JSON line alone."""
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(json_fd, "w", buffering=1)
+
+
 def main():
     args = parse()
     maybe_launch(args)
+    json_only_stdout()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)

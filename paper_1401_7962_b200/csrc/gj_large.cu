@@ -984,13 +984,12 @@ static bool leaf_cfg(int npad, LeafCfg* c) {
 
 // K4b launched beside the panel kernel: the whole grid, its last `cl` CTAs (resident only once
 // the panel kernel's SMs are free) weighted by the share of the update left when it ends.
-// The panel kernel's time relative to the update's (ncols columns) is modelled from the
-// tools/timeline_large.py measurements on B200 (leaf / update on the other SMs: 400 / 592 us
-// at n = 8192, 3175 / 9503 us at n = 32768: the leaf grows as npad^1.5, the update as
-// npad * ncols); 0.85 covers a late CTA's start (its A block, the pipeline fill) and keeps a
-// margin: at n = 8192 weights 240..300 measure alike but 330 costs 4% (the late CTAs then
-// finish last).  A wrong weight only moves time between CTAs: the tiles and their
-// arithmetic are the same.
+// The panel kernel's time relative to the update's (ncols columns) is modelled from
+// tools/timeline_large.py measurements on B200 (leaf / update on the other SMs: 308 / 581 us
+// at n = 8192, 528 / 2334 at 16384, 1365 / 9386 at 32768: the ratio falls as ~npad^-0.935,
+// the update grows as npad * ncols).  0.9 keeps a margin below the measured cliff (n = 8192:
+// weights 400..450 measure alike, 500 costs 3%: the late CTAs then finish last).  A wrong
+// weight only moves time between CTAs: the tiles and their arithmetic are the same.
 #ifndef GJ_DGEMM_LATE_W
 #define GJ_DGEMM_LATE_W -1
 #endif
@@ -1001,8 +1000,8 @@ static void late_ranges(DgemmArgs& d, int sms, int cl, int npad) {
     return;
   }
   const double ncols = d.N > 0 ? (double)d.N : 1.0;
-  const double leaf_over_update = 0.675 * sqrt(8192.0 * npad) / ncols;
-  const double w = 1024.0 * 0.85 * (1.0 - leaf_over_update);
+  const double leaf_over_update = 0.53 * (8192.0 / ncols) * pow(npad / 8192.0, 0.065);
+  const double w = 1024.0 * 0.9 * (1.0 - leaf_over_update);
   d.late_w = w > 0.0 ? (int)w : 0;
 }
 
