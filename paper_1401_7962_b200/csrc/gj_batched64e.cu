@@ -53,6 +53,14 @@ static_assert(BS == 8 || BS == 16, "block size");
 #define GJ_K2_NTL (BS == 8 ? 2 : 1)  // tiles per T phase (register budget)
 #endif
 constexpr int NTL = GJ_K2_NTL;
+#ifndef GJ_K2_TW
+#define GJ_K2_TW 1                 // trailing warps per matrix (2: T0 = look-ahead + a share, T1 = the rest)
+#endif
+constexpr int TW = GJ_K2_TW;
+constexpr int kThreads = 32 * (1 + TW);
+#ifndef GJ_K2_MINB
+#define GJ_K2_MINB (TW == 1 ? 6 : 5)
+#endif
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -196,7 +204,7 @@ __device__ __forceinline__ void tiles_update(double* M, const int (&nts)[NT], co
     for (int mt = 0; mt < 8; ++mt) *reinterpret_cast<double2*>(M + mix(8 * mt + g, 8 * nts[u] + 2 * t)) = c[u][mt];
 }
 
-__global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
+__global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(BatchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_e[];
   double* M = reinterpret_cast<double*>(smem_e + SmemE::M);
   unsigned char* rec = smem_e + SmemE::REC;
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
   const double* __restrict__ Ag = static_cast<const double*>(a.A);
   double* __restrict__ Xg = static_cast<double*>(a.Ainv);
   const int r0 = warp * 32;   // warps 0 and 1: their half of the rows for the load / store
-  const bool io = true;
+  const bool io = warp < 2;
 
   bool loaded = false;
   double rm_next = 0.0;
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
     // ---- a1: this warp's 32 rows -> shared memory, max |a_ij|
     double rm = rm_next;
 #pragma unroll 2
-    for (int i0 = r0; i0 < (loaded ? r0 : r0 + 32); i0 += 8) {
+    for (int i0 = r0; i0 < (loaded || !io ? r0 : r0 + 32); i0 += 8) {
       double2 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Ai + (i0 + u) * N64) + lane);
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
       const unsigned long long rb = (unsigned long long)__double_as_longlong(rm);
       const uint32_t mh = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32));
       const uint32_t ml = __reduce_max_sync(0xffffffffu, (uint32_t)(rb >> 32) == mh ? (uint32_t)rb : 0u);
-      if (lane == 0) rmx[warp] = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+      if (lane == 0 && io) rmx[warp] = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
     }
     __syncthreads();   // the whole matrix and both maxima are in shared memory
     const double tau = a.tol * fmax(rmx[0], rmx[1]);
@@ -245,7 +253,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
       // ------------------------------------------------------------ P: the panels
 #pragma unroll 1
       for (int kb = 0; kb < NB; ++kb) {
-        if (kb > 0) nbar_sync(BAR_TILE, 64);   // panel kb has block kb - 1's update
+        if (kb > 0) nbar_sync(BAR_TILE, 64);   // panel kb has block kb - 1's update (P + T0)
         double x[2][BS];
 #pragma unroll
         for (int r = 0; r < 2; ++r)
@@ -261,13 +269,14 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
 #pragma unroll
           for (int j = 0; j < BS; j += 2)
             *reinterpret_cast<double2*>(M + mix(lane + 32 * r, BS * kb + j)) = make_double2(x[r][j], x[r][j + 1]);
-        nbar_arrive(BAR_PANEL, 64);    // panel kb (W - S) and its record are stored
+        nbar_arrive(BAR_PANEL, kThreads);   // panel kb (W - S) and its record are stored
       }
     } else {
       // ------------------------------------------------------------ T: the block updates
+      const int tw = warp - 1;
 #pragma unroll 1
       for (int kb = 0; kb < NB; ++kb) {
-        nbar_sync(BAR_PANEL, 64);
+        nbar_sync(BAR_PANEL, kThreads);
         double af[8][KS];
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt)
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
 #pragma unroll
         for (int k = 0; k < KS; ++k) rk[k] = rowk[kb * BS + 4 * k + t];
         const int nt1 = (kb + 1) * TPB;   // first tile of panel kb + 1
-        if (kb + 1 < NB) {
+        if (tw == 0 && kb + 1 < NB) {
           // panel kb + 1 first, then release P to factor it
 #pragma unroll
           for (int u = 0; u < TPB; ++u) {
@@ -291,9 +300,12 @@ __global__ void __launch_bounds__(64, 6) gj_batched64f_kernel(BatchedArgs a) {
         // after them on, wrapping), or only those right of panel kb + 1 (determinant only)
         const int first = (kb + (Xg != nullptr && kb + 1 == NB ? 1 : 2)) * TPB;
         const int cnt = Xg != nullptr ? 8 - TPB * (kb + 1 < NB ? 2 : 1) : (first < 8 ? 8 - first : 0);
+        // with two trailing warps: T0 (which also took panel kb + 1) the first (cnt - 1) / 2
+        const int h = TW == 2 ? (cnt - 1) / 2 : cnt;
+        const int j0 = tw == 0 ? 0 : h, j1 = tw == 0 ? h : cnt;
 #pragma unroll 1
-        for (int j = 0; j < cnt; j += NTL) {
-          if (NTL == 2 && j + 1 < cnt) {
+        for (int j = j0; j < j1; j += NTL) {
+          if (NTL == 2 && j + 1 < j1) {
             const int pr[2] = {(first + j) & 7, (first + j + 1) & 7};
             tiles_update<2>(M, pr, af, rk, g, t);
           } else {
@@ -402,12 +414,12 @@ cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
     configured |= dbit;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_batched64f_kernel, 64, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_batched64f_kernel, kThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = (int64_t)device_sm_count() * per_sm;
   const int grid = (int)(a.batch < cap ? a.batch : cap);
-  gj_batched64f_kernel<<<grid, 64, smem, s>>>(a);
+  gj_batched64f_kernel<<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
