@@ -7,3 +7,6 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 cat gpurun_out/bench_ref.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_c4_launches.csv \
     python tools/profile_large_once.py 8192 > /dev/null 2>&1; echo ncu_c4_rc=$?
+timeout 900 python bench.py --workload c5 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo c5_rc=$?
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_c2_launches.csv \
+    python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline --no-c4 > /dev/null 2>&1; echo ncu_c2_rc=$?
