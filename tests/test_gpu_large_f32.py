@@ -93,3 +93,37 @@ def test_large_repeatable(gj, torch, dtype):
         assert torch.equal(X, runs[0][1])
         assert lg == runs[0][2]
     assert float(d.logabsdet) == runs[0][2]
+
+
+GOLD = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden")
+
+
+@pytest.mark.parametrize("fname", sorted(f for f in __import__("os").listdir(GOLD) if f.startswith("f1_oracle_ref"))
+                         or ["none"])
+def test_f1_full_vs_stored_oracle(gj, torch, fname):
+    """f1 at the size bench.py times (fp32 n = 8192) against the oracle's stored outputs on the
+    same fp32 input (tools/make_c4_reference.py 8192 3 f32: long-double GJ on [A | I]): the
+    pivot sequence (R3; a first divergence only at an oracle gap inside reading G26's
+    n u32 band), 64 sampled inverse rows within the kappa rule (R1), log|det| and sign, and
+    the residual of the sampled rows (R2)."""
+    import os
+    from tests.parity import TOL_RES, first_divergence_gap, tie_gap
+    if fname == "none":
+        pytest.skip("no stored f1 oracle reference")
+    ref = np.load(os.path.join(GOLD, fname))
+    n, seed = int(ref["n"]), int(ref["seed"])
+    A = synth.gen_gaussian(n, seed).astype(np.float32)
+    X, lg, sg, info, ipiv = run(gj, torch, A, tol=n * EPS32)
+    assert info == 0
+    ok, exempt = ipiv_match(ipiv, ref["ipiv"], ref["gap"], thr=tie_gap(np.float32, n))
+    print(f"f1 n={n}: first pivot divergence at oracle gap {first_divergence_gap(ipiv, ref['ipiv'], ref['gap'])}")
+    assert ok
+    kappa = float(ref["kappa_inf"])
+    Xr = ref["inv_rows"]
+    e = np.abs(X[ref["rows"]] - Xr).max() / np.abs(Xr).max()
+    print(f"f1 sampled-row rel err {e:.3e}, kappa_inf {kappa:.3e}, e/(kappa eps32) {e / (kappa * EPS32):.3e}")
+    assert e <= max(TOL_INV[np.float32], kappa * EPS32)
+    assert sg == int(ref["sign"])
+    assert abs(lg - float(ref["logabsdet"])) <= max(2e-4, kappa * EPS32)
+    res = oracle.residual(A.astype(np.float64), X.astype(np.float64), rows=ref["rows"])
+    assert res <= max(TOL_RES[np.float32], kappa * EPS32)
