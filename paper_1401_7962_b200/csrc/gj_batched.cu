@@ -49,7 +49,10 @@ namespace {
 using namespace ptx;
 using namespace rowops;
 
-constexpr int kWarpsPerBlock = 4;
+#ifndef GJ_K1_WPB
+#define GJ_K1_WPB 4
+#endif
+constexpr int kWarpsPerBlock = GJ_K1_WPB;   // warps per CTA of the batched kernels (A/B build option)
 #ifndef GJ_K1_FAST_PIVOT
 #define GJ_K1_FAST_PIVOT 0
 #endif
@@ -723,7 +726,7 @@ __device__ __forceinline__ void blk_trail_term(float (&T)[R][N], const float (&P
 // NST = TMA stages per warp: 2 = the next task streams in during this one; 1 = half the
 // shared memory (more resident warps), the next task is prefetched into L2 instead.
 template <int R, int BS, int NST>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, R == 4 ? 2 : (NST == 1 ? 4 : 3))
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, (R == 4 ? 8 : (NST == 1 ? 16 : 12)) / kWarpsPerBlock)
 gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
   using Geo = BlkGeo<R>;
   using M = BlkMisc<R, BS>;
@@ -1090,7 +1093,7 @@ __device__ __forceinline__ void slv_blocks(float (&x)[2][32], float (&b)[2][NR >
 template <int NR>
 // 3 CTAs per SM (168 registers) up to four right-hand sides; with eight the B registers
 // spill there, and 2 CTAs (255 registers, no spill) measure faster (tools/ab_solve.py)
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, NR >= 8 ? 2 : 3)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, (NR >= 8 ? 8 : 12) / kWarpsPerBlock)
 gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
   using S = SolveBlk<NR>;
   using Geo = BlkGeo<2>;
