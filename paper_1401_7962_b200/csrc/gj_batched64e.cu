@@ -180,7 +180,7 @@ constexpr int BAR_PANEL = 1, BAR_TILE = 2;
 // 8 x NT independent accumulator chains are in flight.
 template <int NT>
 __device__ __forceinline__ void tiles_update(double* M, const int (&nts)[NT], const double (&af)[8][KS],
-                                             const int (&rk)[KS], int g, int t) {
+                                             const int (&rk)[KS], int g, int gr, int t) {
   double b[NT][KS];
 #pragma unroll
   for (int u = 0; u < NT; ++u)
@@ -191,7 +191,7 @@ __device__ __forceinline__ void tiles_update(double* M, const int (&nts)[NT], co
 #pragma unroll
   for (int u = 0; u < NT; ++u)
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) c[u][mt] = *reinterpret_cast<const double2*>(M + mix(8 * mt + g, 8 * nts[u] + 2 * t));
+    for (int mt = 0; mt < 8; ++mt) c[u][mt] = *reinterpret_cast<const double2*>(M + mix(8 * mt + gr, 8 * nts[u] + 2 * t));
 #pragma unroll
   for (int k = 0; k < KS; ++k)
 #pragma unroll
@@ -201,7 +201,7 @@ __device__ __forceinline__ void tiles_update(double* M, const int (&nts)[NT], co
 #pragma unroll
   for (int u = 0; u < NT; ++u)
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) *reinterpret_cast<double2*>(M + mix(8 * mt + g, 8 * nts[u] + 2 * t)) = c[u][mt];
+    for (int mt = 0; mt < 8; ++mt) *reinterpret_cast<double2*>(M + mix(8 * mt + gr, 8 * nts[u] + 2 * t)) = c[u][mt];
 }
 
 __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(BatchedArgs a) {
@@ -215,6 +215,11 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
   double* rmx = rpm;   // [2] per-warp max |a_ij| (rpm is free until the epilogue)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
+  // T's fragment row of lane group g: 0, 1, 4, 5, 2, 3, 6, 7 (a row relabelling, free for A and
+  // C): the four rows of a half-warp's 8-byte A-fragment load then sit in different chunk
+  // pairs of the swizzled layout (ncu: these loads were 2-way bank-conflicted), while the
+  // accumulator pairs (2p, 2p + 1) of a quarter-warp's 16-byte C access stay together
+  const int gr = (g & 1) | ((g & 2) << 1) | ((g & 4) >> 1);
   const double* __restrict__ Ag = static_cast<const double*>(a.A);
   double* __restrict__ Xg = static_cast<double*>(a.Ainv);
   const int r0 = warp * 32;   // warps 0 and 1: their half of the rows for the load / store
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-          for (int k = 0; k < KS; ++k) af[mt][k] = M[mix(8 * mt + g, BS * kb + 4 * k + t)];   // A[g][4k + t]
+          for (int k = 0; k < KS; ++k) af[mt][k] = M[mix(8 * mt + gr, BS * kb + 4 * k + t)];   // A[gr][4k + t]
         int rk[KS];
 #pragma unroll
         for (int k = 0; k < KS; ++k) rk[k] = rowk[kb * BS + 4 * k + t];
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
 #pragma unroll
           for (int u = 0; u < TPB; ++u) {
             const int la[1] = {nt1 + u};
-            tiles_update<1>(M, la, af, rk, g, t);
+            tiles_update<1>(M, la, af, rk, g, gr, t);
           }
           wsync();
           nbar_arrive(BAR_TILE, 64);
@@ -307,10 +312,10 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
         for (int j = j0; j < j1; j += NTL) {
           if (NTL == 2 && j + 1 < j1) {
             const int pr[2] = {(first + j) & 7, (first + j + 1) & 7};
-            tiles_update<2>(M, pr, af, rk, g, t);
+            tiles_update<2>(M, pr, af, rk, g, gr, t);
           } else {
             const int one[1] = {(first + j) & 7};
-            tiles_update<1>(M, one, af, rk, g, t);
+            tiles_update<1>(M, one, af, rk, g, gr, t);
             if (NTL == 2) break;
           }
         }
