@@ -176,6 +176,11 @@ def _free_port():
 
 
 def test_c5_gaussian_distributed(gj, torch):
+    """C5 at full size (n = 32768, seed 4) through the column-block-cyclic schedule at P = 1:
+    what is unique against cuSOLVER getrf (sign, log|det|), a valid swap sequence, the
+    sampled residual on 64 rows (R2, kappa-scaled) and on 8 rows through the oracle's
+    long-double residual, and the library-driven gj_invert_dist (the bench path) bitwise
+    equal to the torch.distributed-driven schedule."""
     import torch.distributed as tdist
     from paper_1401_7962_b200.dist import invert_dist, local_columns
     n = 32768
@@ -210,7 +215,24 @@ def test_c5_gaussian_distributed(gj, torch):
         R[torch.arange(64, device="cuda"), rows] -= 1.0
         print(f"C5 kappa_inf {kappa:.3e}, sampled residual {float(R.abs().max()):.3e} (limit {lim:.3e})")
         assert float(R.abs().max()) <= lim
-        del A, LU
+        del LU, R
+        # the same residual through the oracle (long-double accumulation, G17) on 8 of the rows
+        Ah, Xh = A.cpu().numpy(), X.cpu().numpy()
+        rows8 = np.sort(np.random.default_rng(17).choice(n, 8, replace=False))
+        res8 = oracle.residual(Ah, Xh, rows=rows8)
+        print(f"C5 oracle residual on 8 rows {res8:.3e}")
+        assert res8 <= lim
+        del Ah
+        # the product path (bench.py --workload c5): the library-driven gj_invert_dist, bitwise
+        # equal to the torch.distributed-driven schedule above (same steps, same order)
+        from paper_1401_7962_b200.dist import DistContext
+        with DistContext() as ctx:
+            rl = ctx.invert(A[:, local_columns(n, 1, 0)].contiguous(), n)
+            torch.cuda.synchronize()
+        assert rl.info == 0 and rl.sign == res.sign and rl.logabsdet == res.logabsdet
+        assert bool(torch.equal(rl.ipiv, res.ipiv))
+        assert np.array_equal(rl.inverse_local.cpu().numpy(), Xh)
+        del A
     finally:
         tdist.destroy_process_group()
 
