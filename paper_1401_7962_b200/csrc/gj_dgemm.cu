@@ -305,23 +305,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) dgemm_tma_kernel(DgemmArgs g
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-}  // namespace
-
-bool dgemm_tma_supported(const DgemmArgs& g) {
-  return g.K == TK && (g.ldx % 2) == 0 && (g.ldc % 2) == 0 && (g.a_col0 % 2) == 0 &&
-         (reinterpret_cast<uintptr_t>(g.X) & 15) == 0 && (reinterpret_cast<uintptr_t>(g.RT) & 15) == 0 &&
-         (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (g.c_base % 2) == 0 && (g.skip_lo % 2) == 0 &&
-         (g.skip_hi % 2) == 0;
-}
-
-cudaError_t launch_dgemm_tma(const DgemmArgs& g, int grid_sms, bool pdl, cudaStream_t s) {
-  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
-  if (!dgemm_tma_supported(g)) return cudaErrorNotSupported;
-  CUtensorMap ma, mb;
-  if (!make_tma_map_2d(&ma, true, g.X, (uint64_t)g.x_cols, (uint64_t)g.x_rows, (uint64_t)g.ldx * 8, KB, TM, 128))
-    return cudaErrorNotSupported;
-  if (!make_tma_map_2d(&mb, true, g.RT, TK, (uint64_t)g.rt_rows, TK * 8, KB, 64, 128)) return cudaErrorNotSupported;
-  constexpr int CW = GJ_DGEMM_CW;
+template <int CW>
+cudaError_t launch_cw(const DgemmArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, int grid_sms, bool pdl,
+                      cudaStream_t s) {
   static_assert(CW % WMW == 0 && (TN / (CW / WMW)) % 8 == 0, "warp grid");
   auto kern = dgemm_tma_kernel<CW>;
   static unsigned long long configured = 0;
@@ -345,6 +331,29 @@ cudaError_t launch_dgemm_tma(const DgemmArgs& g, int grid_sms, bool pdl, cudaStr
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, g, ma, mb);
+}
+
+}  // namespace
+
+bool dgemm_tma_supported(const DgemmArgs& g) {
+  return g.K == TK && (g.ldx % 2) == 0 && (g.ldc % 2) == 0 && (g.a_col0 % 2) == 0 &&
+         (reinterpret_cast<uintptr_t>(g.X) & 15) == 0 && (reinterpret_cast<uintptr_t>(g.RT) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (g.c_base % 2) == 0 && (g.skip_lo % 2) == 0 &&
+         (g.skip_hi % 2) == 0;
+}
+
+cudaError_t launch_dgemm_tma(const DgemmArgs& g, int grid_sms, bool pdl, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  if (!dgemm_tma_supported(g)) return cudaErrorNotSupported;
+  CUtensorMap ma, mb;
+  if (!make_tma_map_2d(&ma, true, g.X, (uint64_t)g.x_cols, (uint64_t)g.x_rows, (uint64_t)g.ldx * 8, KB, TM, 128))
+    return cudaErrorNotSupported;
+  if (!make_tma_map_2d(&mb, true, g.RT, TK, (uint64_t)g.rt_rows, TK * 8, KB, 64, 128)) return cudaErrorNotSupported;
+  // 16 consumer warps (32 x 8 warp tiles: four warps per scheduler) for matrices up to
+  // ~12K rows, 8 (32 x 16) above: measured (tools/time_large_lib.py, bitwise-equal outputs)
+  // C4 n = 8192 38.1 -> 37.5 ms with 16, but n = 32768 2.23 -> 2.28 s with the weighted ranges
+  // (and n = 16384 alike), so the size decides
+  return g.M <= GJ_DGEMM_CW16_MAX_M ? launch_cw<16>(g, ma, mb, grid_sms, pdl, s) : launch_cw<8>(g, ma, mb, grid_sms, pdl, s);
 }
 
 }  // namespace gj

@@ -89,8 +89,8 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 #endif
-#ifndef GJ_DGEMM_CW
-#define GJ_DGEMM_CW 8
+#ifndef GJ_DGEMM_CW16_MAX_M
+#define GJ_DGEMM_CW16_MAX_M 12288   // K4b: 16 consumer warps up to this many rows, 8 above
 #endif
 
 // Large-n blocked path (gj_large.cu), fp64, one matrix; Ainv may be null (det only).
