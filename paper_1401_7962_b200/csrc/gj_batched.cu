@@ -90,9 +90,22 @@ struct Cfg {
 // redux.sync is only fast with a warp-uniform member mask: one matrix per warp uses it
 // directly, two matrices run one full-warp redux per group (the other group contributes
 // the identity), more groups use a shuffle butterfly over the group's lanes.
+// A/B build options (round 2 measurements, tools/time_c2_lib.py on C2, bitwise-equal
+// outputs): GJ_K1_GRPREDUX=1 reduces each 16-lane group with a non-uniform member mask instead
+// of two full-warp reductions (4.76 ms against 3.53: the masked redux's ~168-cycle latency sits
+// on the pivot chain); GJ_K1_RECPRED=1 (default) stores the per-step record with one predicated
+// st.shared instead of an `if (li == 0)` branch (3.485 against 3.531 ms).
+#ifndef GJ_K1_GRPREDUX
+#define GJ_K1_GRPREDUX 0
+#endif
+#ifndef GJ_K1_RECPRED
+#define GJ_K1_RECPRED 1
+#endif
 template <int MPW, int L>
 __device__ __forceinline__ uint32_t group_max_u32(uint32_t v, int g) {
-  if constexpr (MPW == 1) {
+  if constexpr (MPW == 2 && GJ_K1_GRPREDUX) {
+    return __reduce_max_sync(g ? 0xffff0000u : 0x0000ffffu, v);
+  } else if constexpr (MPW == 1) {
     return __reduce_max_sync(0xffffffffu, v);
   } else if constexpr (MPW == 2) {
     const uint32_t a = __reduce_max_sync(0xffffffffu, g == 0 ? v : 0u);
@@ -106,7 +119,9 @@ __device__ __forceinline__ uint32_t group_max_u32(uint32_t v, int g) {
 }
 template <int MPW, int L>
 __device__ __forceinline__ uint32_t group_min_u32(uint32_t v, int g) {
-  if constexpr (MPW == 1) {
+  if constexpr (MPW == 2 && GJ_K1_GRPREDUX) {
+    return __reduce_min_sync(g ? 0xffff0000u : 0x0000ffffu, v);
+  } else if constexpr (MPW == 1) {
     return __reduce_min_sync(0xffffffffu, v);
   } else if constexpr (MPW == 2) {
     const uint32_t a = __reduce_min_sync(0xffffffffu, g == 0 ? v : 0xffffffffu);
@@ -676,7 +691,13 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
     pos[r] = (pos[r] == k) ? q : pos[r];
     pos[r] = pv[r] ? k : pos[r];
   }
-  if (li == 0) rec_store(rec_g, k, p, q);
+  if constexpr (GJ_K1_RECPRED) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t@p st.shared.v2.u32 [%1], {%2, %3};\n}" ::"r"(li),
+                 "r"(smem_u32(rec_g) + 8u * k), "r"(__float_as_uint(p)), "r"(q)
+                 : "memory");
+  } else {
+    if (li == 0) rec_store(rec_g, k, p, q);
+  }
 }
 
 // Publish the block's pivot rows: their other RW values T (unchanged since the block began).
