@@ -50,7 +50,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=655360, help="oracle sample size (items, ~10 s of host work)")
-    p.add_argument("--no-c4", action="store_true", help="skip the secondary n=8192 fp64 measurement")
+    p.add_argument("--no-c4", action="store_true", help="skip the secondary measurements (C4, C3, C5, f1, f2, f4)")
+    p.add_argument("--no-c5", action="store_true", help="skip the secondary n=32768 fp64 measurement")
     p.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
                    help="c2: the headline batched line; c5: one fp64 32768^2 matrix, column-block-cyclic over the ranks")
     p.add_argument("--n", type=int, default=32768, help="order for --workload c5")
@@ -242,6 +243,56 @@ def c4_measure(dev, reps: int = 3):
                          "traffic": None, "peak_source": src,
                          "kernel": "whole gj_invert (leaf_kernel panels overlapped with the K4b DMMA trailing update)"},
             "roofline_dominant_kernel": k4b}
+
+
+def c5_measure(dev, reps: int = 2):
+    """BASELINE configs[4] at one GPU as a secondary key of the headline line: one fp64
+    32768 x 32768 N(0,1)/sqrt(n) matrix (seed 4) through gj_invert (at P = 1 gj_invert_dist runs
+    the same panels and kernels and is bitwise equal to it, tests/test_gpu_dist.py); the
+    multi-GPU line is bench.py --workload c5.  Host generation (~20 s) is outside the timing."""
+    import torch
+    import paper_1401_7962_b200 as gj
+    import synth
+    n = 32768
+    A = torch.from_numpy(synth.gen_c5(n)).to(dev)
+    X = torch.empty_like(A)
+    ws_bytes = gj.lib.gj_workspace_size(1, n, 1, 1)
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+    outs = [torch.empty(n, dtype=torch.int32, device=dev), torch.empty(1, dtype=torch.float64, device=dev),
+            torch.empty(1, dtype=torch.int8, device=dev), torch.empty(1, dtype=torch.int32, device=dev)]
+    s = torch.cuda.current_stream(dev)
+
+    def run():
+        st = gj.lib.gj_invert(1, n, A.data_ptr(), n, X.data_ptr(), n, outs[0].data_ptr(), outs[1].data_ptr(),
+                              outs[2].data_ptr(), outs[3].data_ptr(), -1.0, ws.data_ptr(), ws_bytes, s.cuda_stream)
+        if st != 0:
+            raise RuntimeError(gj.lib.gj_status_string(st).decode())
+
+    run()
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        run()
+        b.record(s)
+        torch.cuda.synchronize(dev)
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    fl = 2.0 * n ** 3 - n ** 2
+    peak, src = compute_peaks()
+    tf = fl / (ms / 1e3) / 1e12
+    res = {"workload": "C5 at 1 GPU: one fp64 32768x32768 N(0,1)/sqrt(n), seed 4 (BASELINE.json configs[4])",
+           "metric": "fp64 GFLOP/s at n=32768", "value": tf * 1e3, "unit": "GFLOP/s", "ms": ms, "reps": reps,
+           "ms_each": [round(t, 1) for t in ts],
+           "logabsdet": float(outs[1].item()), "sign": int(outs[2].item()), "info": int(outs[3].item()),
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                        "traffic": None, "peak_source": src,
+                        "kernel": "whole gj_invert (leaf_kernel panels overlapped with the K4b DMMA trailing update)"},
+           "multi_gpu": "bench.py --workload c5 --gpus N (gj_invert_dist, column-block-cyclic, NCCL)"}
+    del A, X, ws
+    torch.cuda.empty_cache()
+    return res
 
 
 def k4b_measure(dev, A, n, peak, src, reps: int = 5):
@@ -882,6 +933,8 @@ def main():
         if not args.no_c4 and world == 1:
             line["secondary"] = c4_measure(dev)
             line["secondary_c3"] = c3_measure(dev)
+            if not args.no_c5:
+                line["secondary_c5"] = c5_measure(dev)
             line["next_f1"] = f1_measure(dev)
             line["next_f2"] = f2
             line["next_f4"] = f4

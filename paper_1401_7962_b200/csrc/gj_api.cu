@@ -24,6 +24,40 @@ int device_sm_count() {
   return cached[dev];
 }
 
+void* pool_alloc_async(size_t bytes, cudaStream_t s) {
+  // one library-owned pool per device, keeping its memory between calls (release threshold
+  // = max), so that a per-call scratch buffer costs no device allocation after the first
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (pools[dev] == nullptr) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaMemPool_t p = nullptr;
+      if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev] = p;
+    }
+    pool = pools[dev];
+  }
+  void* ptr = nullptr;
+  if (cudaMallocFromPoolAsync(&ptr, bytes, pool, s) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return ptr;
+}
+
 static double resolve_tol(gj_dtype dt, int n, double tol) {
   if (tol >= 0.0) return tol;
   const double eps = dt == GJ_F32 ? 1.1920928955078125e-07 : 2.220446049250313e-16;

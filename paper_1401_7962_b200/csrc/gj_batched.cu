@@ -53,12 +53,6 @@ using namespace rowops;
 #define GJ_K1_WPB 4
 #endif
 constexpr int kWarpsPerBlock = GJ_K1_WPB;   // warps per CTA of the batched kernels (A/B build option)
-#ifndef GJ_K1_FAST_PIVOT
-#define GJ_K1_FAST_PIVOT 0
-#endif
-// K1b: ballot fast path for the (usual) unique maximum; measured no faster on C2 (kept
-// as a build-time option, -DGJ_K1_FAST_PIVOT=1)
-constexpr bool kFastPivot = GJ_K1_FAST_PIVOT != 0;
 // K1b block loop unrolling (build option -DGJ_K1B_UNROLL=n, A/B measurements)
 #ifndef GJ_K1B_LDS64
 #define GJ_K1B_LDS64 0
@@ -70,6 +64,9 @@ constexpr bool kFastPivot = GJ_K1_FAST_PIVOT != 0;
 #define K1B_SYNC() asm volatile("bar.warp.sync 0xffffffff;" ::: "memory")
 #else
 #define K1B_SYNC() __syncwarp()
+#endif
+#ifndef GJ_K1B_NST
+#define GJ_K1B_NST 2   // TMA stages per warp (A/B build option: 1 = 16 warps per SM at 128 registers)
 #endif
 #ifndef GJ_K1B_UNROLL
 #define GJ_K1B_UNROLL 1
@@ -597,11 +594,19 @@ __device__ __forceinline__ uint32_t blk_gmin(uint32_t v, int g) {
 // One panel step s (static) at global step k on the panel registers P (branch-free, so
 // that a whole block stays one basic block and the scheduler can interleave the previous
 // block's trailing update into the latency of this chain).
-template <int R, int BS>
+// FAST (K1f, the pass that assumes no exact ties): the pivot row of each matrix is the one
+// row whose key equals the group maximum, found from two ballots; no physical positions are
+// tracked (pos[] holds the step at which the row was pivoted) and the record keeps the row.
+// A step where some matrix of the warp has more than one row at its maximum (an exact tie,
+// or an all-zero column) sets `tie`; the task is then discarded and redone by the exact
+// kernel (the tie-break G3 needs the positions).  Without a tie both variants take the same
+// pivot and do the same arithmetic, so their outputs are bitwise equal.
+template <int R, int BS, bool FAST>
 __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (&P)[R][BS], uint32_t (&kmask)[R],
-                                               int (&pos)[R], int (&bs)[R], unsigned char* rec_g, int li, int g,
-                                               int lane) {
+                                               int (&pos)[R], int (&bs)[R], unsigned& tie, unsigned char* rec_g,
+                                               int li, int g, int lane) {
   constexpr int SB = R == 2 ? 1 : 2;   // slot bits in the winner code
+  constexpr int L = BlkGeo<R>::L;
   // a2: max |x_ik| over the un-pivoted rows (IEEE bit pattern of |x|, monotone)
   uint32_t key[R];
   uint32_t km = 0;
@@ -618,31 +623,26 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
   for (int r = 0; r < R; ++r) t[r] = P[r][s] * ra;
   int q, src, slot;
   bool pv[R];
-  // fast path: exactly one row per matrix attains the maximum (warp-uniform test on the
-  // ballots; an all-zero column makes every row tie and takes the slow path)
-  unsigned ball[R];
-  int tot = 0;
-  if constexpr (kFastPivot) {
+  if constexpr (FAST) {
+    // every matrix has at least one row at its maximum, so a total of M candidates over the
+    // warp means exactly one per matrix
+    unsigned ball[R], any = 0;
+    int tot = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       pv[r] = key[r] == m;
       ball[r] = __ballot_sync(0xffffffffu, pv[r]);
       tot += __popc(ball[r]);
+      any |= ball[r];
     }
-  }
-  if (kFastPivot && tot == BlkGeo<R>::M) {
-    unsigned any = 0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) any |= ball[r];
-    const unsigned gm = (BlkGeo<R>::L == 32 ? 0xffffffffu : ((1u << BlkGeo<R>::L) - 1u)) << (BlkGeo<R>::L * g);
-    src = __ffs(any & gm) - 1;
+    tie |= (unsigned)(tot != BlkGeo<R>::M);
+    const unsigned gm = (L == 32 ? 0xffffffffu : ((1u << L) - 1u)) << (L * g);
+    const unsigned su = 31u - (unsigned)__clz(any & gm);   // FLO: the candidate's lane
+    src = (int)su;
     slot = 0;
 #pragma unroll
-    for (int r = 1; r < R; ++r) slot = ((ball[r] >> src) & 1u) ? r : slot;
-    int ps = pos[0];
-#pragma unroll
-    for (int r = 1; r < R; ++r) ps = pv[r] ? pos[r] : ps;
-    q = __shfl_sync(0xffffffffu, ps, src);
+    for (int r = 1; r < R; ++r) slot = (ball[r] & gm) ? r : slot;
+    q = (int)((su & (unsigned)(L - 1)) + (unsigned)(L * slot));   // the pivot row (recorded instead of its position)
   } else {
     // ties -> smallest physical position (G3); the winner code carries (position, lane, slot)
     uint32_t cmin = 0xffffffu;
@@ -687,9 +687,13 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
     P[r][s] = nf;   // compact D entry; 0 on the pivot row (W - S: its 1 is held as 0)
     kmask[r] = pv[r] ? 0u : kmask[r];
     bs[r] = pv[r] ? s : bs[r];
-    // a3: the listing's swap of positions k and q (L156-L162), positions only
-    pos[r] = (pos[r] == k) ? q : pos[r];
-    pos[r] = pv[r] ? k : pos[r];
+    if constexpr (FAST) {
+      pos[r] = pv[r] ? k : pos[r];   // the step this row is pivoted at (= its final position)
+    } else {
+      // a3: the listing's swap of positions k and q (L156-L162), positions only
+      pos[r] = (pos[r] == k) ? q : pos[r];
+      pos[r] = pv[r] ? k : pos[r];
+    }
   }
   if constexpr (GJ_K1_RECPRED) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t@p st.shared.v2.u32 [%1], {%2, %3};\n}" ::"r"(li),
@@ -744,11 +748,48 @@ __device__ __forceinline__ void blk_trail_term(float (&T)[R][N], const float (&P
     }
 }
 
+// Number of cycles of the permutation sigma of a matrix's 32 rows (row li + L r -> sig[r]; L = 16
+// lanes x 2 rows): pointer jumping, 5 rounds, each row's label = the smallest row of its
+// cycle; a row is its cycle's representative iff its label is itself.  (lab, next) travel
+// packed in one word.
+template <int L>
+__device__ __forceinline__ int perm_cycles(const int (&sig)[2], int li, int g, unsigned gmask) {
+  static_assert(L == 16, "two rows per lane");
+  int lab[2] = {li, li + L}, nx[2] = {sig[0], sig[1]};
+#pragma unroll
+  for (int it = 0; it < 5; ++it) {
+    const int pk0 = (lab[0] << 8) | nx[0], pk1 = (lab[1] << 8) | nx[1];
+    int nl[2], nn[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int b = nx[r];
+      const int srcl = (g * L) | (b & (L - 1));
+      const int v0 = __shfl_sync(0xffffffffu, pk0, srcl), v1 = __shfl_sync(0xffffffffu, pk1, srcl);
+      const int v = b >= L ? v1 : v0;
+      nl[r] = min(lab[r], v >> 8);
+      nn[r] = v & 0xff;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      lab[r] = nl[r];
+      nx[r] = nn[r];
+    }
+  }
+  return __popc(__ballot_sync(0xffffffffu, lab[0] == li) & gmask) + __popc(__ballot_sync(0xffffffffu, lab[1] == li + L) & gmask);
+}
+
 // NST = TMA stages per warp: 2 = the next task streams in during this one; 1 = half the
 // shared memory (more resident warps), the next task is prefetched into L2 instead.
-template <int R, int BS, int NST>
+// MODE (the two-pass run of launch_blk32, used when no ipiv is requested):
+//   0  exact (G3 tie-break on physical positions) over every task;
+//   1  K1f: FAST panel steps over every task; a task in which a step found an exact tie
+//      writes nothing and is appended to tlist (tlist[0] = count, tlist[1..] = tasks);
+//   2  exact over the tasks of tlist only (the tasks MODE 1 gave up, read from A again —
+//      A is intact there even when the inverse aliases it).
+template <int R, int BS, int NST, int MODE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, (R == 4 ? 8 : (NST == 1 ? 16 : 12)) / kWarpsPerBlock)
-gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
+gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restrict__ tlist) {
+  constexpr bool FAST = MODE == 1;
   using Geo = BlkGeo<R>;
   using M = BlkMisc<R, BS>;
   constexpr int RW = M::RW, L = Geo::L, MT = Geo::M;
@@ -770,9 +811,11 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
   unsigned char* rec_g = rec + g * 32 * 8;
   int* perm_g = permS + g * 32;
 
-  const int64_t ntasks = (a.batch + MT - 1) / MT;
+  // task index ti -> task (MODE 2: the list of tasks the FAST pass gave up)
+  const int64_t ntasks = MODE == 2 ? (int64_t)tlist[0] : (a.batch + MT - 1) / MT;
+  auto task_of = [&](int64_t ti) -> int64_t { return MODE == 2 ? (int64_t)tlist[1 + ti] : ti; };
   const int64_t wstride = (int64_t)gridDim.x * kWarpsPerBlock;
-  const int64_t task0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+  const int64_t ti0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
 
   if (lane == 0) {
     mbar_init(&bars[0], 1);
@@ -780,28 +823,29 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     fence_mbar_init();
   }
   K1B_SYNC();
-  if (lane == 0 && task0 < ntasks) {
+  if (lane == 0 && ti0 < ntasks) {
     mbar_expect_tx(&bars[0], Geo::STAGE);
-    tma_load_2d(stage0, &tm.a, 0, (int)(task0 * Geo::ROWS), &bars[0]);
+    tma_load_2d(stage0, &tm.a, 0, (int)(task_of(ti0) * Geo::ROWS), &bars[0]);
   }
 
   int it = 0;
-  for (int64_t task = task0; task < ntasks; task += wstride, ++it) {
+  for (int64_t ti = ti0; ti < ntasks; ti += wstride, ++it) {
+    const int64_t task = task_of(ti);
     const int64_t item0 = task * MT;
     const bool item_ok = item0 + g < a.batch;
     unsigned char* stage = stage0 + (NST == 2 ? (it & 1) * Geo::STAGE : 0);
-    const int64_t nxt = task + wstride;
+    const int64_t nti = ti + wstride;
     if constexpr (NST == 2) {
-      if (lane == 0 && nxt < ntasks) {
+      if (lane == 0 && nti < ntasks) {
         unsigned char* ns = stage0 + ((it + 1) & 1) * Geo::STAGE;
         bulk_wait_read0();
         mbar_expect_tx(&bars[(it + 1) & 1], Geo::STAGE);
-        tma_load_2d(ns, &tm.a, 0, (int)(nxt * Geo::ROWS), &bars[(it + 1) & 1]);
+        tma_load_2d(ns, &tm.a, 0, (int)(task_of(nti) * Geo::ROWS), &bars[(it + 1) & 1]);
       }
       mbar_wait_warp(&bars[it & 1], (it >> 1) & 1);
     } else {
-      if (lane == 0 && nxt < ntasks)
-        bulk_prefetch_l2(static_cast<const float*>(a.A) + nxt * Geo::ROWS * 32, Geo::STAGE);
+      if (lane == 0 && nti < ntasks)
+        bulk_prefetch_l2(static_cast<const float*>(a.A) + task_of(nti) * Geo::ROWS * 32, Geo::STAGE);
       mbar_wait_warp(&bars[0], it & 1);
     }
     // ---- a1: rows li + L r of matrix g into registers ----
@@ -826,6 +870,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
 
     uint32_t kmask[R];
     int pos[R], bs[R];
+    unsigned tie = 0;
     // P: panel columns of the current block; T: the other 32 - BS columns, rotated so
     // that T[0..BS) is the next panel and the finished compact D columns sit at the end
     float P[R][BS], T[R][RW];
@@ -840,7 +885,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
       for (int j = 0; j < RW; ++j) T[r][j] = x[r][BS + j];
     }
 #pragma unroll
-    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS>(s, s, P, kmask, pos, bs, rec_g, li, g, lane);
+    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, FAST>(s, s, P, kmask, pos, bs, tie, rec_g, li, g, lane);
     // look-ahead: per iteration, publish block kb's pivot rows, apply its update to the
     // next panel first, then factor that panel while the rest of block kb's update runs
 #pragma unroll kK1bUnroll
@@ -858,7 +903,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
       for (int r = 0; r < R; ++r) bs[r] = -1;
 #pragma unroll
       for (int s = 0; s < BS; ++s) {
-        blk_panel_step<R, BS>(s, kb + BS + s, NP, kmask, pos, bs, rec_g, li, g, lane);
+        blk_panel_step<R, BS, FAST>(s, kb + BS + s, NP, kmask, pos, bs, tie, rec_g, li, g, lane);
         if (s + 1 < BS)
           blk_trail_term<R, BS, BS, RW, RW>(T, P, s, rbuf_g, BS);
         else
@@ -903,24 +948,32 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
       myrp[r] = rcp(p_own);
       const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau) & gmask;
       if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * L + r * L);
-      nswap += __popc(__ballot_sync(0xffffffffu, q_k != row) & gmask);
+      if constexpr (!FAST) nswap += __popc(__ballot_sync(0xffffffffu, q_k != row) & gmask);
       nneg += __popc(__ballot_sync(0xffffffffu, p_k < 0.0f) & gmask);
       lgl += log_abs(p_k);
-      if (a.ipiv && item_ok) a.ipiv[(item0 + g) * 32 + row] = q_k + 1;
+      if constexpr (!FAST) {
+        if (a.ipiv && item_ok) a.ipiv[(item0 + g) * 32 + row] = q_k + 1;
+      }
     }
+    // K1f keeps no positions: the swaps' parity is that of the permutation row -> pivot step
+    if constexpr (FAST) nswap = 32 - perm_cycles<L>(pos, li, g, gmask);
     const int info = (int)failb;
     const double lg = group_sum<L>(lgl);
     const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
-    if (item_ok && li == 0) {
+    if (item_ok && li == 0 && !tie) {
       const int64_t item = item0 + g;
       if (a.info) a.info[item] = info;
       if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
       if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
       if (a.det) static_cast<float*>(a.det)[item] = info ? 0.0f : (float)(sgn * exp(lg));
     }
+    if constexpr (FAST) {
+      // a task with an exact tie: nothing written; the exact pass redoes it (tie is warp-uniform)
+      if (tie && lane == 0) tlist[1 + atomicAdd(tlist, 1)] = (int)task;
+    }
 
     // ---- a7 + a8: un-permuted store through the staging buffer ----
-    if (a.Ainv != nullptr) {
+    if (a.Ainv != nullptr && !tie) {
 #pragma unroll
       for (int r = 0; r < R; ++r) perm_g[pos[r]] = (li + L * r) * 4;   // output column (bytes)
       K1B_SYNC();
@@ -947,20 +1000,20 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm) {
     }
     K1B_SYNC();
     if constexpr (NST == 1) {
-      if (lane == 0 && nxt < ntasks) {
+      if (lane == 0 && nti < ntasks) {
         bulk_wait_read0();   // the store has read the stage
         mbar_expect_tx(&bars[0], Geo::STAGE);
-        tma_load_2d(stage0, &tm.a, 0, (int)(nxt * Geo::ROWS), &bars[0]);
+        tma_load_2d(stage0, &tm.a, 0, (int)(task_of(nti) * Geo::ROWS), &bars[0]);
       }
     }
   }
   if (lane == 0) bulk_wait0();
 }
 
-template <int R, int BS, int NST>
-cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
+template <int R, int BS, int NST, int MODE>
+cudaError_t launch_blk32_mode(const BatchedArgs& a, const TmaMaps& maps, int* tlist, cudaStream_t s) {
   const size_t smem = BlkMisc<R, BS>::smem(NST);
-  auto kern = gj_blk32_kernel<R, BS, NST>;
+  auto kern = gj_blk32_kernel<R, BS, NST, MODE>;
   static unsigned long long configured = 0;
   const unsigned long long dbit = device_bit();
   if (!(configured & dbit)) {
@@ -976,8 +1029,32 @@ cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t
   const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int64_t cap = (int64_t)device_sm_count() * per_sm;
   const int grid = (int)(need < cap ? need : cap);
-  kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(a, maps);
+  kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(a, maps, tlist);
   return cudaGetLastError();
+}
+
+#ifndef GJ_K1F
+#define GJ_K1F 1   // two-pass K1f + exact redo when no ipiv is requested (A/B build option)
+#endif
+
+// K1b entry.  Without ipiv (C2's outputs) it runs two passes: K1f over every task (no
+// positions, no tie-break), then the exact kernel over the tasks in which K1f met an exact
+// tie; the task list comes from a stream-ordered allocation of the library's memory pool.
+// With ipiv (the LAPACK-style swap sequence needs the positions) it runs the exact kernel.
+template <int R, int BS, int NST>
+cudaError_t launch_blk32(const BatchedArgs& a, const TmaMaps& maps, cudaStream_t s) {
+  if (GJ_K1F && a.ipiv == nullptr) {
+    const int64_t ntasks = (a.batch + R - 1) / R;
+    int* tl = static_cast<int*>(pool_alloc_async((size_t)(ntasks + 1) * sizeof(int), s));
+    if (tl != nullptr) {
+      cudaError_t e = cudaMemsetAsync(tl, 0, sizeof(int), s);
+      if (e == cudaSuccess) e = launch_blk32_mode<R, BS, NST, 1>(a, maps, tl, s);
+      if (e == cudaSuccess) e = launch_blk32_mode<R, BS, NST, 2>(a, maps, tl, s);
+      const cudaError_t f = cudaFreeAsync(tl, s);
+      return e != cudaSuccess ? e : f;
+    }
+  }
+  return launch_blk32_mode<R, BS, NST, 0>(a, maps, nullptr, s);
 }
 
 // ------------------------------------------------------------------ K1s: blocked solve / det, fp32 n = 32
@@ -1094,9 +1171,10 @@ __device__ __forceinline__ void slv_blocks(float (&x)[2][32], float (&b)[2][NR >
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r) bs[r] = -1;
+    unsigned notie = 0;   // the exact panel step never sets it
 #pragma unroll
     for (int s = 0; s < BS; ++s) {
-      blk_panel_step<2, BS>(s, C1 + s, NP, kmask, pos, bs, rec_g, li, g, lane);
+      blk_panel_step<2, BS, false>(s, C1 + s, NP, kmask, pos, bs, notie, rec_g, li, g, lane);
       slv_trail<NR, C1 + BS>(x, b, P, s, rb);
     }
     __syncwarp();   // every lane has read rb before the next publish
@@ -1198,6 +1276,7 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
 
     uint32_t kmask[R];
     int pos[R], bs[R];
+    unsigned notie = 0;   // the exact panel step never sets it
     float P[R][BS];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1208,7 +1287,7 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
       for (int j = 0; j < BS; ++j) P[r][j] = x[r][j];
     }
 #pragma unroll
-    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS>(s, s, P, kmask, pos, bs, rec_g, li, g, lane);
+    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, false>(s, s, P, kmask, pos, bs, notie, rec_g, li, g, lane);
     slv_blocks<NR, 0>(x, b, P, kmask, pos, bs, rb, rec_g, li, g, lane);
     __syncwarp();
 
@@ -1348,7 +1427,7 @@ cudaError_t launch_np(const BatchedArgs& a, cudaStream_t s) {
         if (make_tma_map_2d(&maps.a, false, a.A, 32, rows, 128, 32, 64, 128) &&
             (a.Ainv == nullptr || make_tma_map_2d(&maps.x, false, a.Ainv, 32, rows, 128, 32, 64, 128))) {
           if (a.Ainv == nullptr) maps.x = maps.a;
-          return launch_blk32<2, 4, 2>(a, maps, s);
+          return launch_blk32<2, 4, GJ_K1B_NST>(a, maps, s);
         }
       }
     }

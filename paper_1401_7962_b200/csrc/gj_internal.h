@@ -137,6 +137,9 @@ cudaError_t dist_unpermute_unpack(int n, const double* recvbuf, const int* recv_
 
 // Number of SMs of the current device (cached per device).
 int device_sm_count();
+// Stream-ordered scratch allocation from a library-owned memory pool of the current device
+// (free with cudaFreeAsync on the same stream); nullptr if unavailable.
+void* pool_alloc_async(size_t bytes, cudaStream_t s);
 // Bit of the current device: launch-time function attributes (dynamic shared memory,
 // cluster size) are per device context, so "configured once" caches are per device.
 inline unsigned long long device_bit() {
