@@ -596,7 +596,7 @@ __device__ __forceinline__ uint32_t blk_gmin(uint32_t v, int g) {
 // block's trailing update into the latency of this chain).
 // FAST (K1f, the pass that assumes no exact ties): the pivot row of each matrix is the one
 // row whose key equals the group maximum, found from two ballots; no physical positions are
-// tracked (pos[] holds the step at which the row was pivoted) and the record keeps the row.
+// tracked (pos[] holds the step at which the row was pivoted) and the record keeps only p.
 // A step where some matrix of the warp has more than one row at its maximum (an exact tie,
 // or an all-zero column) sets `tie`; the task is then discarded and redone by the exact
 // kernel (the tie-break G3 needs the positions).  Without a tie both variants take the same
@@ -642,7 +642,7 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
     slot = 0;
 #pragma unroll
     for (int r = 1; r < R; ++r) slot = (ball[r] & gm) ? r : slot;
-    q = (int)((su & (unsigned)(L - 1)) + (unsigned)(L * slot));   // the pivot row (recorded instead of its position)
+    q = src;   // recorded in place of the position (K1f's epilogue reads only p from the record)
   } else {
     // ties -> smallest physical position (G3); the winner code carries (position, lane, slot)
     uint32_t cmin = 0xffffffu;
