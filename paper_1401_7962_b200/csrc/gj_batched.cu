@@ -68,6 +68,9 @@ constexpr int kWarpsPerBlock = GJ_K1_WPB;   // warps per CTA of the batched kern
 #ifndef GJ_K1B_NST
 #define GJ_K1B_NST 2   // TMA stages per warp (A/B build option: 1 = 16 warps per SM at 128 registers)
 #endif
+#ifndef GJ_K1B_PUB1
+#define GJ_K1B_PUB1 1   // the block publish as one asm block of predicated stores (A/B option)
+#endif
 #ifndef GJ_K1B_UNROLL
 #define GJ_K1B_UNROLL 1
 #endif
@@ -688,7 +691,8 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
     kmask[r] = pv[r] ? 0u : kmask[r];
     bs[r] = pv[r] ? s : bs[r];
     if constexpr (FAST) {
-      pos[r] = pv[r] ? k : pos[r];   // the step this row is pivoted at (= its final position)
+      // pos[] (the step this row is pivoted at = its final position) is set from bs[] once
+      // per block, where the block's pivot rows are published (k0_pos_from_bs)
     } else {
       // a3: the listing's swap of positions k and q (L156-L162), positions only
       pos[r] = (pos[r] == k) ? q : pos[r];
@@ -704,6 +708,13 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
   }
 }
 
+// K1f: the steps of block k0's pivot rows, from their block-step slots
+template <int R>
+__device__ __forceinline__ void k0_pos_from_bs(int (&pos)[R], const int (&bs)[R], int k0) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) pos[r] = bs[r] >= 0 ? k0 + bs[r] : pos[r];
+}
+
 // Publish the block's pivot rows: their other RW values T (unchanged since the block began).
 template <int R, int BS>
 __device__ __forceinline__ void blk_publish(const float (&T)[R][32 - BS], const int (&bs)[R], float* rbuf_g) {
@@ -711,9 +722,28 @@ __device__ __forceinline__ void blk_publish(const float (&T)[R][32 - BS], const 
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const uint32_t dst = smem_u32(rbuf_g) + (uint32_t)(bs[r] < 0 ? 0 : bs[r]) * (RW * 4);
+    if constexpr (RW == 28 && GJ_K1B_PUB1) {
+      // the seven predicated 16-byte stores in one asm block (one predicate)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %0, 0;\n\t"
+          "@p st.shared.v4.f32 [%1], {%2, %3, %4, %5};\n\t"
+          "@p st.shared.v4.f32 [%1+16], {%6, %7, %8, %9};\n\t"
+          "@p st.shared.v4.f32 [%1+32], {%10, %11, %12, %13};\n\t"
+          "@p st.shared.v4.f32 [%1+48], {%14, %15, %16, %17};\n\t"
+          "@p st.shared.v4.f32 [%1+64], {%18, %19, %20, %21};\n\t"
+          "@p st.shared.v4.f32 [%1+80], {%22, %23, %24, %25};\n\t"
+          "@p st.shared.v4.f32 [%1+96], {%26, %27, %28, %29};\n}" ::"r"(bs[r]), "r"(dst),
+          "f"(T[r][0]), "f"(T[r][1]), "f"(T[r][2]), "f"(T[r][3]), "f"(T[r][4]), "f"(T[r][5]), "f"(T[r][6]),
+          "f"(T[r][7]), "f"(T[r][8]), "f"(T[r][9]), "f"(T[r][10]), "f"(T[r][11]), "f"(T[r][12]), "f"(T[r][13]),
+          "f"(T[r][14]), "f"(T[r][15]), "f"(T[r][16]), "f"(T[r][17]), "f"(T[r][18]), "f"(T[r][19]),
+          "f"(T[r][20]), "f"(T[r][21]), "f"(T[r][22]), "f"(T[r][23]), "f"(T[r][24]), "f"(T[r][25]),
+          "f"(T[r][26]), "f"(T[r][27])
+          : "memory");
+    } else {
 #pragma unroll
-    for (int j = 0; j < RW; j += 4)
-      st_shared_v4_if(bs[r] >= 0, dst + 4u * j, T[r][j], T[r][j + 1], T[r][j + 2], T[r][j + 3]);
+      for (int j = 0; j < RW; j += 4)
+        st_shared_v4_if(bs[r] >= 0, dst + 4u * j, T[r][j], T[r][j + 1], T[r][j + 2], T[r][j + 3]);
+    }
   }
 }
 
@@ -891,6 +921,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restri
 #pragma unroll kK1bUnroll
     for (int kb = 0; kb + BS < 32; kb += BS) {
       blk_publish<R, BS>(T, bs, rbuf_g);
+      if constexpr (FAST) k0_pos_from_bs<R>(pos, bs, kb);
       K1B_SYNC();
       float NP[R][BS];
 #pragma unroll
@@ -921,6 +952,7 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restri
     }
     // last block: its whole update, then x = [T | P] (register j = compact column j)
     blk_publish<R, BS>(T, bs, rbuf_g);
+    if constexpr (FAST) k0_pos_from_bs<R>(pos, bs, 32 - BS);
     K1B_SYNC();
 #pragma unroll
     for (int s = 0; s < BS; ++s) blk_trail_term<R, BS, 0, RW, RW>(T, P, s, rbuf_g, 0);
