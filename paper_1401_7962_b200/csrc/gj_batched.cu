@@ -606,8 +606,8 @@ __device__ __forceinline__ uint32_t blk_gmin(uint32_t v, int g) {
 // pivot and do the same arithmetic, so their outputs are bitwise equal.
 template <int R, int BS, bool FAST>
 __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (&P)[R][BS], uint32_t (&kmask)[R],
-                                               int (&pos)[R], int (&bs)[R], unsigned& tie, unsigned char* rec_g,
-                                               int li, int g, int lane) {
+                                               int (&pos)[R], int (&bs)[R], unsigned& tie, float (&pblk)[BS],
+                                               unsigned char* rec_g, int li, int g, int lane) {
   constexpr int SB = R == 2 ? 1 : 2;   // slot bits in the winner code
   constexpr int L = BlkGeo<R>::L;
   // a2: max |x_ik| over the un-pivoted rows (IEEE bit pattern of |x|, monotone)
@@ -699,13 +699,24 @@ __device__ __forceinline__ void blk_panel_step(const int s, const int k, float (
       pos[r] = pv[r] ? k : pos[r];
     }
   }
-  if constexpr (GJ_K1_RECPRED) {
+  if constexpr (FAST) {
+    (void)q;
+    pblk[s] = p;   // K1f: the block's four pivots are recorded at once (rec_store_block)
+  } else if constexpr (GJ_K1_RECPRED) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t@p st.shared.v2.u32 [%1], {%2, %3};\n}" ::"r"(li),
                  "r"(smem_u32(rec_g) + 8u * k), "r"(__float_as_uint(p)), "r"(q)
                  : "memory");
   } else {
     if (li == 0) rec_store(rec_g, k, p, q);
   }
+}
+
+// K1f's record: p of steps k0 .. k0 + 3 as one 16-byte store by the group's lane 0 (the
+// record is then p only, 4 bytes per step; one store per block instead of one per step)
+__device__ __forceinline__ void rec_store_block(unsigned char* rec_g, int k0, const float (&pb)[4], int li) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t@p st.shared.v4.f32 [%1], {%2, %3, %4, %5};\n}" ::"r"(li),
+               "r"(smem_u32(rec_g) + 4u * k0), "f"(pb[0]), "f"(pb[1]), "f"(pb[2]), "f"(pb[3])
+               : "memory");
 }
 
 // K1f: the steps of block k0's pivot rows, from their block-step slots
@@ -914,8 +925,10 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restri
 #pragma unroll
       for (int j = 0; j < RW; ++j) T[r][j] = x[r][BS + j];
     }
+    float pb[BS];
 #pragma unroll
-    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, FAST>(s, s, P, kmask, pos, bs, tie, rec_g, li, g, lane);
+    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, FAST>(s, s, P, kmask, pos, bs, tie, pb, rec_g, li, g, lane);
+    if constexpr (FAST) rec_store_block(rec_g, 0, pb, li);
     // look-ahead: per iteration, publish block kb's pivot rows, apply its update to the
     // next panel first, then factor that panel while the rest of block kb's update runs
 #pragma unroll kK1bUnroll
@@ -934,12 +947,13 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restri
       for (int r = 0; r < R; ++r) bs[r] = -1;
 #pragma unroll
       for (int s = 0; s < BS; ++s) {
-        blk_panel_step<R, BS, FAST>(s, kb + BS + s, NP, kmask, pos, bs, tie, rec_g, li, g, lane);
+        blk_panel_step<R, BS, FAST>(s, kb + BS + s, NP, kmask, pos, bs, tie, pb, rec_g, li, g, lane);
         if (s + 1 < BS)
           blk_trail_term<R, BS, BS, RW, RW>(T, P, s, rbuf_g, BS);
         else
           blk_trail_term<R, BS, BS, RW, RW, true>(T, P, s, rbuf_g, BS);   // + the rotation
       }
+      if constexpr (FAST) rec_store_block(rec_g, kb + BS, pb, li);
       K1B_SYNC();   // every lane has read rbuf before the next publish
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -973,10 +987,15 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restri
     for (int r = 0; r < R; ++r) {
       const int row = li + L * r;
       float p_own, p_k;
-      int q_own, q_k;
-      rec_load(rec_g, pos[r], p_own, q_own);
-      rec_load(rec_g, row, p_k, q_k);
-      (void)q_own;
+      int q_own, q_k = 0;
+      if constexpr (FAST) {
+        p_own = reinterpret_cast<const float*>(rec_g)[pos[r]];
+        p_k = reinterpret_cast<const float*>(rec_g)[row];
+      } else {
+        rec_load(rec_g, pos[r], p_own, q_own);
+        rec_load(rec_g, row, p_k, q_k);
+        (void)q_own;
+      }
       myrp[r] = rcp(p_own);
       const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau) & gmask;
       if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * L + r * L);
@@ -1204,9 +1223,10 @@ __device__ __forceinline__ void slv_blocks(float (&x)[2][32], float (&b)[2][NR >
 #pragma unroll
     for (int r = 0; r < 2; ++r) bs[r] = -1;
     unsigned notie = 0;   // the exact panel step never sets it
+    float nopb[BS];      // nor records into it
 #pragma unroll
     for (int s = 0; s < BS; ++s) {
-      blk_panel_step<2, BS, false>(s, C1 + s, NP, kmask, pos, bs, notie, rec_g, li, g, lane);
+      blk_panel_step<2, BS, false>(s, C1 + s, NP, kmask, pos, bs, notie, nopb, rec_g, li, g, lane);
       slv_trail<NR, C1 + BS>(x, b, P, s, rb);
     }
     __syncwarp();   // every lane has read rb before the next publish
@@ -1309,6 +1329,7 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
     uint32_t kmask[R];
     int pos[R], bs[R];
     unsigned notie = 0;   // the exact panel step never sets it
+    float nopb[BS];       // nor records into it
     float P[R][BS];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1319,7 +1340,7 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
       for (int j = 0; j < BS; ++j) P[r][j] = x[r][j];
     }
 #pragma unroll
-    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, false>(s, s, P, kmask, pos, bs, notie, rec_g, li, g, lane);
+    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, false>(s, s, P, kmask, pos, bs, notie, nopb, rec_g, li, g, lane);
     slv_blocks<NR, 0>(x, b, P, kmask, pos, bs, rb, rec_g, li, g, lane);
     __syncwarp();
 
