@@ -913,7 +913,9 @@ def main():
         achieved = B * BYTES_PER_MATRIX / (avg_launch_ms / 1e3) / 1e9
         traffic = profile_traffic() if B == BATCH else None
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "gj_blk32_kernel<2,4,2> (K1b)",
+                "traffic": traffic,
+                "kernel": "gj_blk32_kernel<2,4,2,1> (K1f) + gj_blk32_kernel<2,4,2,2> (the exact pass over K1f's "
+                          "tie list; empty on C2), timed together as the one gj_invert_batched call",
                 "algorithmic_bytes_per_launch": B * BYTES_PER_MATRIX, "peak_source": peak_src,
                 "per_unit_bytes": BYTES_PER_MATRIX, "units_per_launch": B,
                 "fp32_flops_per_launch": B * FLOPS_PER_MATRIX,
@@ -926,7 +928,9 @@ def main():
                            "parallelism": f"dp{world} (contiguous shards of the one seed-1 batch, no collective)",
                            "l2": "inputs (4 GiB total) larger than L2 (126 MB); no flush needed",
                            "outputs": "inverse, logabsdet, sign"},
-                "roofline": roof, "gpu_launches": args.steps, "clocks": clk.summary(), "e2e": e2e}
+                "roofline": roof, "gpu_launches": 2 * args.steps,
+                "gpu_launches_note": "per step: K1f and the exact pass over its tie list (plus one 4-byte cudaMemsetAsync)",
+                "clocks": clk.summary(), "e2e": e2e}
         if weak is not None:
             line["weak_scaling"] = weak
         line["parity"] = c2_parity_report()

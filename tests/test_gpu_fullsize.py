@@ -3,7 +3,8 @@ outputs the oracle can compute item by item (sampled) or on properties that hold
 size (exact pins, library cross-checks of det / pivots, residual rows).
 
 * C2 (configs[1]): the whole 1,048,576-item fp32 batch in one gj_invert_batched call
-  (the bench's K1b kernel), oracle on a sample spread over the batch incl. its ragged end.
+  (with ipiv: the exact K1b kernel; the bench's call without ipiv runs K1f and is asserted
+  bitwise equal to it), oracle on a sample spread over the batch incl. its ragged end.
 * C2 and C3 also EVERY item against the oracle (chunked; SURVEY §8d's oracle plan: "every
   report run, all items").
 * C3 (configs[2]): the whole 262,144-item fp64 batch (K2f), every singular flag against the
@@ -68,9 +69,20 @@ def test_c2_every_item(gj, torch):
     ipiv (near-tie rule), R4 sign, R5 log|det|, R7 singular flag."""
     A = synth.gen_c2()
     tol = 32 * 2.0 ** -23
-    r = gj.invert_batched(torch.from_numpy(A).cuda(), tol=tol)
+    At = torch.from_numpy(A).cuda()
+    r = gj.invert_batched(At, tol=tol)
     torch.cuda.synchronize()
     gall = {k: v.cpu().numpy() for k, v in r._asdict().items() if v is not None}
+    # the bench requests no ipiv, which runs K1f (+ the exact redo of its tie tasks): every
+    # output of that call bitwise equal to this one, so the oracle comparison below covers it
+    rf = gj.invert_batched(At, tol=tol, ipiv=False)
+    torch.cuda.synchronize()
+    for k in ("inverse", "logabsdet", "sign", "det", "info"):
+        a, b = getattr(r, k), getattr(rf, k)
+        if a.dtype == torch.float32:
+            a, b = a.view(torch.int32), b.view(torch.int32)
+        assert torch.equal(a, b), k
+    del rf
     worst = 0.0
     ch = 65536
     tot = {"items": 0, "ipiv_exempt_gap_le_1e-6": 0, "ipiv_exempt_g26_band": 0, "g26_items": [],

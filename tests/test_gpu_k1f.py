@@ -1,0 +1,70 @@
+"""K1f — the two-pass fp32 n = 32 batched inversion used when no ipiv is requested (the
+bench's C2 call): a FAST pass that picks each pivot row from two ballots (no physical
+positions, no tie-break) and gives up any task in which a step meets an exact tie, then the
+exact kernel (G3 tie-break) over those tasks only.  Its outputs must be BITWISE the exact
+kernel's (the same call with ipiv), on batches that do and do not tie, with singular items,
+a ragged batch and an in-place inverse (the redo reads A, which the FAST pass must leave
+intact for its given-up tasks).  Method: Eqs. (14)-(15); tie rule G3."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def gj():
+    import paper_1401_7962_b200 as g
+    return g
+
+
+def _batch(kind, B, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "gauss":
+        return rng.standard_normal((B, 32, 32)).astype(np.float32)
+    if kind == "int":          # small integers: exact ties at many steps
+        return rng.integers(-3, 4, (B, 32, 32)).astype(np.float32)
+    A = rng.standard_normal((B, 32, 32)).astype(np.float32)   # mixed
+    idx = rng.choice(B, B // 50, replace=False)
+    A[idx] = rng.integers(-2, 3, (len(idx), 32, 32)).astype(np.float32)
+    A[idx[:5], :, 7] = 0.0                                      # a zero column: singular
+    A[idx[5:8]] = np.stack([synth.hadamard_pd(32, seed=s)[0] for s in range(3)]).astype(np.float32)
+    return A
+
+
+def _run(gj, torch, A, ipiv, alias=False):
+    X = A.clone() if alias else torch.empty_like(A)
+    r = gj.invert_batched(X if alias else A, out=X, ipiv=ipiv)
+    torch.cuda.synchronize()
+    return [t.cpu() for t in (r.inverse, r.logabsdet, r.sign, r.det, r.info)]
+
+
+@pytest.mark.parametrize("kind,B", [("gauss", 100001), ("int", 4097), ("mixed", 65537), ("gauss", 1), ("int", 3)])
+@pytest.mark.parametrize("alias", [False, True])
+def test_k1f_bitwise_exact_kernel(gj, torch, kind, B, alias):
+    A = torch.from_numpy(_batch(kind, B, 11 + B)).cuda()
+    ref = _run(gj, torch, A, True)
+    got = _run(gj, torch, A, False, alias)
+    for a, b, name in zip(ref, got, ("inverse", "logabsdet", "sign", "det", "info")):
+        if a.dtype == torch.float32:
+            a, b = a.view(torch.int32), b.view(torch.int32)
+        assert torch.equal(a, b), name
+
+
+def test_k1f_all_ties_hadamard(gj, torch):
+    """Every step an exact tie: every task goes to the exact pass; the result is still the
+    exact inverse A^T / n of the Hadamard pin P6."""
+    H = np.stack([synth.hadamard_pd(32, seed=5 + s)[0] for s in range(40)]).astype(np.float32)
+    A = torch.from_numpy(H).cuda()
+    r = gj.invert_batched(A, ipiv=False)
+    torch.cuda.synchronize()
+    want = np.transpose(H, (0, 2, 1)) / 32.0
+    assert np.array_equal(r.inverse.cpu().numpy(), want)
