@@ -414,10 +414,9 @@ def f4_measure(A, stream, nrhs: int = 1, reps: int = 3):
     g.manual_seed(5)
     R = torch.randn((Bn, N, nrhs), dtype=A.dtype, device=A.device, generator=g)
     X = torch.empty_like(R)
-    ip = torch.empty((Bn, N), dtype=torch.int32, device=A.device)
 
     def run():
-        st = gj.lib.gj_solve_batched(0, N, nrhs, Bn, A.data_ptr(), R.data_ptr(), X.data_ptr(), ip.data_ptr(),
+        st = gj.lib.gj_solve_batched(0, N, nrhs, Bn, A.data_ptr(), R.data_ptr(), X.data_ptr(), None,
                                      None, None, None, N * 2.0 ** -23, stream.cuda_stream)
         if st != 0:
             raise RuntimeError(gj.lib.gj_status_string(st).decode())
@@ -459,7 +458,7 @@ def f4_measure(A, stream, nrhs: int = 1, reps: int = 3):
     return {"workload": f"f4: C2 batch (1,048,576 x 32 x 32 fp32) solved for {nrhs} right-hand side(s) (SURVEY §8f f4)",
             "metric": "systems/s", "value": Bn / (ms / 1e3), "unit": "systems/s", "ms": ms, "reps": reps,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                         "peak_source": src, "kernel": f"gj_blk32s_kernel<{nrhs}> (K1s)",
+                         "peak_source": src, "kernel": f"gj_blk32s_kernel<{nrhs},1> (K1s, two-pass as K1f: no ipiv requested)",
                          "note": "K1b's blocked elimination without the D half; pivot-chain bound like K1b"},
             "det_only": {"api": "gj_det (K1s without right-hand sides)", "ms": ms_det,
                          "value": Bn / (ms_det / 1e3), "unit": "matrices/s",

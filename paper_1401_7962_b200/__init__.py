@@ -174,9 +174,11 @@ def invert_batched(A, tol: Optional[float] = None, *, out=None, inverse: bool = 
 SolveResult = namedtuple("SolveResult", ["X", "logabsdet", "sign", "ipiv", "info"])
 
 
-def solve_batched(A, B, tol: Optional[float] = None, *, out=None, stream=None) -> "SolveResult":
+def solve_batched(A, B, tol: Optional[float] = None, *, out=None, ipiv: bool = True, stream=None) -> "SolveResult":
     """``gj_solve_batched``: X = A^-1 B by Gauss–Jordan on [A | B] (n, nrhs ≤ 32).
-    A [batch, n, n], B [batch, n, nrhs] (or [n, n], [n, nrhs]); ``out`` may be B."""
+    A [batch, n, n], B [batch, n, nrhs] (or [n, n], [n, nrhs]); ``out`` may be B.
+    ``ipiv=False`` requests no pivot sequence (fp32 n = 32 then runs the two-pass K1f
+    scheme; the result's ipiv is None)."""
     torch = _torch()
     if not (A.is_cuda and B.is_cuda):
         raise ValueError("A and B must be CUDA tensors")
@@ -195,17 +197,17 @@ def solve_batched(A, B, tol: Optional[float] = None, *, out=None, stream=None) -
         out = out.unsqueeze(0)
     _check_out(out, B.shape, B.dtype, dev)
     X = out if out is not None else torch.empty_like(B)
-    o_ipiv = torch.empty((bt, n), dtype=torch.int32, device=dev)
+    o_ipiv = torch.empty((bt, n), dtype=torch.int32, device=dev) if ipiv else None
     o_lg = torch.empty((bt,), dtype=torch.float64, device=dev)
     o_sg = torch.empty((bt,), dtype=torch.int8, device=dev)
     o_info = torch.empty((bt,), dtype=torch.int32, device=dev)
     with torch.cuda.device(dev):
-        st = lib.gj_solve_batched(_dt(A), n, m, bt, A.data_ptr(), B.data_ptr(), X.data_ptr(), o_ipiv.data_ptr(),
+        st = lib.gj_solve_batched(_dt(A), n, m, bt, A.data_ptr(), B.data_ptr(), X.data_ptr(), _ptr(o_ipiv),
                                   o_lg.data_ptr(), o_sg.data_ptr(), o_info.data_ptr(),
                                   TOL_DEFAULT if tol is None else float(tol), _stream_ptr(stream))
     _check(st)
     if squeeze:
-        return SolveResult(X[0], o_lg[0], o_sg[0], o_ipiv[0], o_info[0])
+        return SolveResult(X[0], o_lg[0], o_sg[0], None if o_ipiv is None else o_ipiv[0], o_info[0])
     return SolveResult(X, o_lg, o_sg, o_ipiv, o_info)
 
 
@@ -285,8 +287,9 @@ def invert_batched_full(A, tol: Optional[float] = None, *, out=None, inverse: bo
     return invert_batched_pivoting(A, "full", tol, out=out, inverse=inverse, stream=stream)
 
 
-def det(A, tol: Optional[float] = None, *, stream=None) -> Result:
-    """Determinants only (``gj_det``): logabsdet, sign, det, ipiv, info; inverse is None."""
+def det(A, tol: Optional[float] = None, *, ipiv: bool = True, stream=None) -> Result:
+    """Determinants only (``gj_det``): logabsdet, sign, det, ipiv, info; inverse is None.
+    ``ipiv=False`` requests no pivot sequence (its field is then None)."""
     torch = _torch()
     squeeze = A.dim() == 2
     if squeeze:
@@ -294,7 +297,7 @@ def det(A, tol: Optional[float] = None, *, stream=None) -> Result:
     _check_square_batch(A)
     B, n = A.shape[0], A.shape[1]
     dev = A.device
-    o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev)
+    o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev) if ipiv else None
     o_lg = torch.empty((B,), dtype=torch.float64, device=dev)
     o_sg = torch.empty((B,), dtype=torch.int8, device=dev)
     o_det = torch.empty((B,), dtype=A.dtype, device=dev)
@@ -303,11 +306,11 @@ def det(A, tol: Optional[float] = None, *, stream=None) -> Result:
     ws = torch.empty((max(ws_bytes, 1),), dtype=torch.uint8, device=dev)
     with torch.cuda.device(dev):
         st = lib.gj_det(_dt(A), n, B, A.data_ptr(), o_lg.data_ptr(), o_sg.data_ptr(), o_det.data_ptr(),
-                        o_ipiv.data_ptr(), o_info.data_ptr(), TOL_DEFAULT if tol is None else float(tol),
+                        _ptr(o_ipiv), o_info.data_ptr(), TOL_DEFAULT if tol is None else float(tol),
                         ws.data_ptr(), ws_bytes, _stream_ptr(stream))
     _check(st)
     if squeeze:
-        return Result(None, o_lg[0], o_sg[0], o_det[0], o_ipiv[0], o_info[0])
+        return Result(None, o_lg[0], o_sg[0], o_det[0], None if o_ipiv is None else o_ipiv[0], o_info[0])
     return Result(None, o_lg, o_sg, o_det, o_ipiv, o_info)
 
 

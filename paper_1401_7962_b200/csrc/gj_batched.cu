@@ -1196,12 +1196,13 @@ __device__ __forceinline__ void slv_trail(float (&x)[2][32], float (&b)[2][NR > 
 
 // block KB has been factored (panel values P = W - S); apply its update, factoring block
 // KB + 1 under it (look-ahead), then recurse
-template <int NR, int KB>
+template <int NR, int KB, bool FAST>
 __device__ __forceinline__ void slv_blocks(float (&x)[2][32], float (&b)[2][NR > 0 ? NR : 1], float (&P)[2][4],
                                            uint32_t (&kmask)[2], int (&pos)[2], int (&bs)[2], float* rb,
-                                           unsigned char* rec_g, int li, int g, int lane) {
+                                           unsigned& tie, unsigned char* rec_g, int li, int g, int lane) {
   constexpr int BS = 4;
   slv_publish<NR, KB>(x, b, bs, rb);
+  if constexpr (FAST) k0_pos_from_bs<2>(pos, bs, KB * BS);
   __syncwarp();
   if constexpr (KB + 1 < 32 / BS) {
     constexpr int C1 = (KB + 1) * BS;   // the next panel
@@ -1222,30 +1223,31 @@ __device__ __forceinline__ void slv_blocks(float (&x)[2][32], float (&b)[2][NR >
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r) bs[r] = -1;
-    unsigned notie = 0;   // the exact panel step never sets it
-    float nopb[BS];      // nor records into it
+    float pb[BS];
 #pragma unroll
     for (int s = 0; s < BS; ++s) {
-      blk_panel_step<2, BS, false>(s, C1 + s, NP, kmask, pos, bs, notie, nopb, rec_g, li, g, lane);
+      blk_panel_step<2, BS, FAST>(s, C1 + s, NP, kmask, pos, bs, tie, pb, rec_g, li, g, lane);
       slv_trail<NR, C1 + BS>(x, b, P, s, rb);
     }
+    if constexpr (FAST) rec_store_block(rec_g, C1, pb, li);
     __syncwarp();   // every lane has read rb before the next publish
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int j = 0; j < BS; ++j) P[r][j] = NP[r][j];
-    slv_blocks<NR, KB + 1>(x, b, P, kmask, pos, bs, rb, rec_g, li, g, lane);
+    slv_blocks<NR, KB + 1, FAST>(x, b, P, kmask, pos, bs, rb, tie, rec_g, li, g, lane);
   } else {
 #pragma unroll
     for (int s = 0; s < BS; ++s) slv_trail<NR, 32>(x, b, P, s, rb);
   }
 }
 
-template <int NR>
+template <int NR, int MODE>
 // 3 CTAs per SM (168 registers) up to four right-hand sides; with eight the B registers
 // spill there, and 2 CTAs (255 registers, no spill) measure faster (tools/ab_solve.py)
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, (NR >= 8 ? 8 : 12) / kWarpsPerBlock)
-gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
+gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm, int* __restrict__ tlist) {
+  constexpr bool FAST = MODE == 1;   // MODE as in gj_blk32_kernel (K1f's two passes)
   using S = SolveBlk<NR>;
   using Geo = BlkGeo<2>;
   constexpr int R = 2, BS = 4, L = Geo::L, MT = Geo::M, NB = NR > 0 ? NR : 1;
@@ -1265,9 +1267,10 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
   float* rb = rbuf + g * BS * S::RS;
   unsigned char* rec_g = rec + g * 32 * 8;
 
-  const int64_t ntasks = (a.batch + MT - 1) / MT;
+  const int64_t ntasks = MODE == 2 ? (int64_t)tlist[0] : (a.batch + MT - 1) / MT;
+  auto task_of = [&](int64_t ti) -> int64_t { return MODE == 2 ? (int64_t)tlist[1 + ti] : ti; };
   const int64_t wstride = (int64_t)gridDim.x * kWarpsPerBlock;
-  const int64_t task0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+  const int64_t ti0 = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
   const int m = a.m;
 
   if (lane == 0) {
@@ -1276,18 +1279,20 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
     fence_mbar_init();
   }
   __syncwarp();
-  if (lane == 0 && task0 < ntasks) {
+  if (lane == 0 && ti0 < ntasks) {
     mbar_expect_tx(&bars[0], Geo::STAGE);
-    tma_load_2d(stage0, &tm.a, 0, (int)(task0 * Geo::ROWS), &bars[0]);
+    tma_load_2d(stage0, &tm.a, 0, (int)(task_of(ti0) * Geo::ROWS), &bars[0]);
   }
 
   int it = 0;
-  for (int64_t task = task0; task < ntasks; task += wstride, ++it) {
+  for (int64_t ti = ti0; ti < ntasks; ti += wstride, ++it) {
+    const int64_t task = task_of(ti);
     const int64_t item0 = task * MT;
     const bool item_ok = item0 + g < a.batch;
     unsigned char* stage = stage0 + (it & 1) * Geo::STAGE;
-    const int64_t nxt = task + wstride;
-    if (lane == 0 && nxt < ntasks) {
+    const int64_t nti = ti + wstride;
+    const int64_t nxt = nti < ntasks ? task_of(nti) : 0;
+    if (lane == 0 && nti < ntasks) {
       mbar_expect_tx(&bars[(it + 1) & 1], Geo::STAGE);
       tma_load_2d(stage0 + ((it + 1) & 1) * Geo::STAGE, &tm.a, 0, (int)(nxt * Geo::ROWS), &bars[(it + 1) & 1]);
       if constexpr (NR > 0) {
@@ -1328,8 +1333,8 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
 
     uint32_t kmask[R];
     int pos[R], bs[R];
-    unsigned notie = 0;   // the exact panel step never sets it
-    float nopb[BS];       // nor records into it
+    unsigned tie = 0;
+    float pb[BS];
     float P[R][BS];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1340,8 +1345,9 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
       for (int j = 0; j < BS; ++j) P[r][j] = x[r][j];
     }
 #pragma unroll
-    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, false>(s, s, P, kmask, pos, bs, notie, nopb, rec_g, li, g, lane);
-    slv_blocks<NR, 0>(x, b, P, kmask, pos, bs, rb, rec_g, li, g, lane);
+    for (int s = 0; s < BS; ++s) blk_panel_step<R, BS, FAST>(s, s, P, kmask, pos, bs, tie, pb, rec_g, li, g, lane);
+    if constexpr (FAST) rec_store_block(rec_g, 0, pb, li);
+    slv_blocks<NR, 0, FAST>(x, b, P, kmask, pos, bs, rb, tie, rec_g, li, g, lane);
     __syncwarp();
 
     // ---- a6: det / ipiv / singular flag from the per-step record (K1b's epilogue)
@@ -1353,22 +1359,33 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
     for (int r = 0; r < R; ++r) {
       const int row = li + L * r;
       float p_own, p_k;
-      int q_own, q_k;
-      rec_load(rec_g, pos[r], p_own, q_own);
-      rec_load(rec_g, row, p_k, q_k);
-      (void)q_own;
+      int q_own, q_k = 0;
+      if constexpr (FAST) {
+        p_own = reinterpret_cast<const float*>(rec_g)[pos[r]];
+        p_k = reinterpret_cast<const float*>(rec_g)[row];
+      } else {
+        rec_load(rec_g, pos[r], p_own, q_own);
+        rec_load(rec_g, row, p_k, q_k);
+        (void)q_own;
+      }
       myrp[r] = rcp(p_own);
       const unsigned fb = __ballot_sync(0xffffffffu, fabsf(p_k) <= tau) & gmask;
       if (failb == 0 && fb != 0) failb = (unsigned)(__ffs(fb) - g * L + r * L);
-      nswap += __popc(__ballot_sync(0xffffffffu, q_k != row) & gmask);
+      if constexpr (!FAST) nswap += __popc(__ballot_sync(0xffffffffu, q_k != row) & gmask);
       nneg += __popc(__ballot_sync(0xffffffffu, p_k < 0.0f) & gmask);
       lgl += log_abs(p_k);
-      if (a.ipiv && item_ok) a.ipiv[(item0 + g) * 32 + row] = q_k + 1;
+      if constexpr (!FAST) {
+        if (a.ipiv && item_ok) a.ipiv[(item0 + g) * 32 + row] = q_k + 1;
+      }
     }
+    if constexpr (FAST) nswap = 32 - perm_cycles<L>(pos, li, g, gmask);
     const int info = (int)failb;
     const double lg = group_sum<L>(lgl);
     const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
-    if (item_ok && li == 0) {
+    if constexpr (FAST) {
+      if (tie && lane == 0) tlist[1 + atomicAdd(tlist, 1)] = (int)task;   // redone by the exact pass
+    }
+    if (item_ok && li == 0 && !tie) {
       const int64_t item = item0 + g;
       if (a.info) a.info[item] = info;
       if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
@@ -1377,7 +1394,7 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
     }
     // ---- a7 + a8: X[k][:] = (row pivoted at step k)[B part] / p_k
     if constexpr (NR > 0) {
-      if (item_ok) {
+      if (item_ok && !tie) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -1389,10 +1406,10 @@ gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm) {
   }
 }
 
-template <int NR>
-cudaError_t launch_blk32s(const BlkSolveArgs& a, const TmaMaps& maps, cudaStream_t s) {
+template <int NR, int MODE>
+cudaError_t launch_blk32s_mode(const BlkSolveArgs& a, const TmaMaps& maps, int* tlist, cudaStream_t s) {
   const size_t smem = SolveBlk<NR>::smem();
-  auto kern = gj_blk32s_kernel<NR>;
+  auto kern = gj_blk32s_kernel<NR, MODE>;
   static unsigned long long configured = 0;
   const unsigned long long dbit = device_bit();
   if (!(configured & dbit)) {
@@ -1408,8 +1425,26 @@ cudaError_t launch_blk32s(const BlkSolveArgs& a, const TmaMaps& maps, cudaStream
   const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int64_t cap = (int64_t)device_sm_count() * per_sm;
   const int grid = (int)(need < cap ? need : cap);
-  kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(a, maps);
+  kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(a, maps, tlist);
   return cudaGetLastError();
+}
+
+// K1s entry: without ipiv the two passes of K1f (FAST pass, then the exact kernel over the
+// tasks it gave up), with ipiv the exact kernel (launch_blk32 explains why)
+template <int NR>
+cudaError_t launch_blk32s(const BlkSolveArgs& a, const TmaMaps& maps, cudaStream_t s) {
+  if (GJ_K1F && a.ipiv == nullptr) {
+    const int64_t ntasks = (a.batch + 1) / 2;
+    int* tl = static_cast<int*>(pool_alloc_async((size_t)(ntasks + 1) * sizeof(int), s));
+    if (tl != nullptr) {
+      cudaError_t e = cudaMemsetAsync(tl, 0, sizeof(int), s);
+      if (e == cudaSuccess) e = launch_blk32s_mode<NR, 1>(a, maps, tl, s);
+      if (e == cudaSuccess) e = launch_blk32s_mode<NR, 2>(a, maps, tl, s);
+      const cudaError_t f = cudaFreeAsync(tl, s);
+      return e != cudaSuccess ? e : f;
+    }
+  }
+  return launch_blk32s_mode<NR, 0>(a, maps, nullptr, s);
 }
 
 // K1s applicability: fp32, n = 32, m <= 8, 16-byte aligned A, rows indexable by the TMA map

@@ -68,3 +68,31 @@ def test_k1f_all_ties_hadamard(gj, torch):
     torch.cuda.synchronize()
     want = np.transpose(H, (0, 2, 1)) / 32.0
     assert np.array_equal(r.inverse.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("kind,B", [("gauss", 20001), ("mixed", 16385), ("int", 1025)])
+@pytest.mark.parametrize("nrhs", [0, 1, 3, 8])
+def test_k1s_two_pass_bitwise_exact(gj, torch, kind, B, nrhs):
+    """The same two-pass scheme in K1s (fp32 n = 32 solve on [A | B], and the determinant-only
+    run when nrhs = 0): without ipiv bitwise the exact kernel's outputs (with ipiv), also with
+    X aliasing B (the exact pass reads B again for the tasks the FAST pass gave up)."""
+    A = torch.from_numpy(_batch(kind, B, 7 + B + nrhs)).cuda()
+    if nrhs == 0:
+        ref = gj.det(A)
+        got = gj.det(A, ipiv=False)
+        torch.cuda.synchronize()
+        pairs = [(ref.logabsdet, got.logabsdet), (ref.sign, got.sign), (ref.det, got.det), (ref.info, got.info)]
+    else:
+        g = torch.Generator(device="cuda").manual_seed(B + nrhs)
+        Bm = torch.randn((B, 32, nrhs), generator=g, device="cuda", dtype=torch.float32)
+        ref = gj.solve_batched(A, Bm)
+        got = gj.solve_batched(A, Bm, ipiv=False)
+        Bc = Bm.clone()
+        ali = gj.solve_batched(A, Bc, out=Bc, ipiv=False)
+        torch.cuda.synchronize()
+        pairs = [(ref.X, got.X), (ref.X, ali.X), (ref.logabsdet, got.logabsdet), (ref.sign, got.sign),
+                 (ref.info, got.info)]
+    for a, b in pairs:
+        if a.dtype == torch.float32:
+            a, b = a.view(torch.int32), b.view(torch.int32)
+        assert torch.equal(a, b)
