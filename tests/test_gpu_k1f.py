@@ -97,36 +97,3 @@ def test_k1s_two_pass_bitwise_exact(gj, torch, kind, B, nrhs):
             a, b = a.view(torch.int32), b.view(torch.int32)
         assert torch.equal(a, b)
 
-
-def _batch64(kind, B, seed):
-    rng = np.random.default_rng(seed)
-    if kind == "gauss":
-        return rng.standard_normal((B, 64, 64))
-    if kind == "int":
-        return rng.integers(-3, 4, (B, 64, 64)).astype(np.float64)
-    # C3-like: P L diag(u) with some duplicated rows (singular, ending on a zero column)
-    L = np.tril(rng.normal(0, 0.5, (B, 64, 64)), -1) + np.eye(64)
-    A = L * rng.uniform(0.5, 2, (B, 1, 64))
-    A = np.stack([a[rng.permutation(64)] for a in A])
-    for b in rng.choice(B, B // 20, replace=False):
-        i, j = rng.choice(64, 2, replace=False)
-        A[b, j] = A[b, i]
-    return A
-
-
-@pytest.mark.parametrize("kind,B", [("gauss", 3001), ("c3like", 4099), ("int", 257), ("gauss", 1)])
-@pytest.mark.parametrize("alias", [False, True])
-def test_k2f_two_pass_bitwise_exact(gj, torch, kind, B, alias):
-    """K2f (fp64 n = 64, the C3 kernel) without ipiv: the FAST pass + the exact redo of its
-    tie matrices, bitwise the exact kernel's outputs (with ipiv), also in place."""
-    A = torch.from_numpy(_batch64(kind, B, 3 + B)).cuda()
-    tol = 1e-10
-    r = gj.invert_batched(A, tol=tol)
-    X = A.clone() if alias else torch.empty_like(A)
-    f = gj.invert_batched(X if alias else A, tol=tol, out=X, ipiv=False)
-    torch.cuda.synchronize()
-    for k in ("inverse", "logabsdet", "sign", "det", "info"):
-        a, b = getattr(r, k), getattr(f, k)
-        if a.dtype == torch.float64:
-            a, b = a.view(torch.int64), b.view(torch.int64)
-        assert torch.equal(a, b), k
