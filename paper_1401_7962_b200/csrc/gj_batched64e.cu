@@ -87,14 +87,9 @@ __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.syn
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // P's pivot step S (static) at global step k on the panel rows lane and lane + 32.
-// FAST (the first pass of the two-pass run, as K1f in gj_batched.cu): the pivot row is the one
-// row whose key equals the maximum (two ballots); no physical positions (pos[] = the step the
-// row is pivoted at); a step with more than one row at the maximum sets `tie` and the matrix
-// is redone by the exact kernel.  Without a tie both variants take the same pivot and do the
-// same arithmetic: bitwise equal outputs.
-template <int S, bool FAST>
+template <int S>
 __device__ __forceinline__ void panel_step(const int k, double (&x)[2][BS], uint32_t (&kmask)[2], int (&pos)[2],
-                                           unsigned char* rec, int* rowk, int lane, double* prow, unsigned& tie) {
+                                           unsigned char* rec, int* rowk, int lane, double* prow) {
   uint32_t hi[2], lo[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -107,27 +102,15 @@ __device__ __forceinline__ void panel_step(const int k, double (&x)[2][BS], uint
   const uint32_t ml = __reduce_max_sync(0xffffffffu, lm);
   // |p| is the winning key itself: 1/|p| starts before the winner is known
   const double rap = rcp64d(__longlong_as_double((long long)(((unsigned long long)mh << 32) | ml)));
-  int q, src, slot;
-  bool cand[2];
-  if constexpr (FAST) {
+  uint32_t c = 0xffffffu;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) cand[r] = hi[r] == mh && lo[r] == ml;
-    const unsigned b0 = __ballot_sync(0xffffffffu, cand[0]), b1 = __ballot_sync(0xffffffffu, cand[1]);
-    tie |= (unsigned)(__popc(b0) + __popc(b1) != 1);
-    src = (int)(31u - (unsigned)__clz(b0 | b1));
-    slot = b1 != 0u ? 1 : 0;
-    q = 0;   // not recorded: K2f's FAST epilogue reads only p from the record
-  } else {
-    uint32_t c = 0xffffffu;
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-      c = min(c, (hi[r] == mh && lo[r] == ml && kmask[r] != 0u) ? ((uint32_t)pos[r] << 6 | (uint32_t)lane << 1 | (uint32_t)r)
-                                                                 : 0xffffffu);
-    const uint32_t win = __reduce_min_sync(0xffffffffu, c);
-    q = (int)(win >> 6);
-    src = (int)((win >> 1) & 31u);
-    slot = (int)(win & 1u);
-  }
+  for (int r = 0; r < 2; ++r)
+    c = min(c, (hi[r] == mh && lo[r] == ml && kmask[r] != 0u) ? ((uint32_t)pos[r] << 6 | (uint32_t)lane << 1 | (uint32_t)r)
+                                                               : 0xffffffu);
+  const uint32_t win = __reduce_min_sync(0xffffffffu, c);
+  const int q = (int)(win >> 6);
+  const int src = (int)((win >> 1) & 31u);
+  const int slot = (int)(win & 1u);
   // the pivot row's panel values: one writer (predicated stores), broadcast reads
   double* pr = prow + (S & 1) * BS;
 #pragma unroll
@@ -148,14 +131,14 @@ __device__ __forceinline__ void panel_step(const int k, double (&x)[2][BS], uint
   const double rp = p < 0.0 ? -rap : rap;   // rcp64d is odd: bit-identical to rcp64d(p)
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const bool pv = FAST ? cand[r] : (pos[r] == q && kmask[r] != 0u);
+    const bool pv = pos[r] == q && kmask[r] != 0u;
     const double nf = pv ? 0.0 : -(x[r][S] * rp);
 #pragma unroll
     for (int j = 0; j < BS; ++j)
       if (j != S) x[r][j] = fma(nf, z[j], x[r][j]);
     x[r][S] = nf;   // compact D entry; 0 on the pivot row (W - S)
     kmask[r] = pv ? 0u : kmask[r];
-    if constexpr (!FAST) pos[r] = (pos[r] == k) ? q : pos[r];   // a3: the listing's swap of positions k and q (L156-L162)
+    pos[r] = (pos[r] == k) ? q : pos[r];   // a3: the listing's swap of positions k and q (L156-L162)
     pos[r] = pv ? k : pos[r];
   }
   if (lane == 0) {
@@ -163,38 +146,13 @@ __device__ __forceinline__ void panel_step(const int k, double (&x)[2][BS], uint
     rowk[k] = src + 32 * slot;
   }
 }
-template <int S, bool FAST>
+template <int S>
 __device__ __forceinline__ void panel_steps(const int kb, double (&x)[2][BS], uint32_t (&kmask)[2], int (&pos)[2],
-                                            unsigned char* rec, int* rowk, int lane, double* prow, unsigned& tie) {
+                                            unsigned char* rec, int* rowk, int lane, double* prow) {
   if constexpr (S < BS) {
-    panel_step<S, FAST>(kb + S, x, kmask, pos, rec, rowk, lane, prow, tie);
-    panel_steps<S + 1, FAST>(kb, x, kmask, pos, rec, rowk, lane, prow, tie);
+    panel_step<S>(kb + S, x, kmask, pos, rec, rowk, lane, prow);
+    panel_steps<S + 1>(kb, x, kmask, pos, rec, rowk, lane, prow);
   }
-}
-
-// Cycles of the permutation sigma of the 64 rows (row lane + 32 r -> sig[r]): pointer jumping,
-// 6 rounds; the swap parity of K2f's FAST pass is (64 - cycles) mod 2 (see perm_cycles, K1f).
-__device__ __forceinline__ int perm_cycles64(const int (&sig)[2], int lane) {
-  int lab[2] = {lane, lane + 32}, nx[2] = {sig[0], sig[1]};
-#pragma unroll
-  for (int it = 0; it < 6; ++it) {
-    const int pk0 = (lab[0] << 8) | nx[0], pk1 = (lab[1] << 8) | nx[1];
-    int nl[2], nn[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int b = nx[r];
-      const int v0 = __shfl_sync(0xffffffffu, pk0, b & 31), v1 = __shfl_sync(0xffffffffu, pk1, b & 31);
-      const int v = b >= 32 ? v1 : v0;
-      nl[r] = min(lab[r], v >> 8);
-      nn[r] = v & 0xff;
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      lab[r] = nl[r];
-      nx[r] = nn[r];
-    }
-  }
-  return __popc(__ballot_sync(0xffffffffu, lab[0] == lane)) + __popc(__ballot_sync(0xffffffffu, lab[1] == lane + 32));
 }
 
 // Element (row, col) of the shared working array: row stride 64 doubles and the 16-byte
@@ -213,8 +171,7 @@ struct SmemE {
   static constexpr int POS = ROW + N64 * 4;                // [64] final position of row i
   static constexpr int RP = POS + N64 * 4;                 // [64] 1 / p of step k
   static constexpr int PROW = RP + N64 * 8;                // [2][BS] pivot-row broadcast
-  static constexpr int TIE = PROW + 2 * BS * 8;            // FAST pass: this matrix is given up
-  static constexpr int BYTES = TIE + 16;
+  static constexpr int BYTES = PROW + 2 * BS * 8;
 };
 constexpr int BAR_PANEL = 1, BAR_TILE = 2;
 
@@ -247,11 +204,7 @@ __device__ __forceinline__ void tiles_update(double* M, const int (&nts)[NT], co
     for (int mt = 0; mt < 8; ++mt) *reinterpret_cast<double2*>(M + mix(8 * mt + gr, 8 * nts[u] + 2 * t)) = c[u][mt];
 }
 
-// MODE (as gj_blk32_kernel): 0 exact over every matrix; 1 FAST panel steps, a matrix with an
-// exact tie writes nothing and is appended to tlist (tlist[0] = count); 2 exact over tlist.
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(BatchedArgs a, int* __restrict__ tlist) {
-  constexpr bool FAST = MODE == 1;
+__global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(BatchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_e[];
   double* M = reinterpret_cast<double*>(smem_e + SmemE::M);
   unsigned char* rec = smem_e + SmemE::REC;
@@ -260,7 +213,6 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
   double* rpm = reinterpret_cast<double*>(smem_e + SmemE::RP);
   double* prow = reinterpret_cast<double*>(smem_e + SmemE::PROW);
   double* rmx = rpm;   // [2] per-warp max |a_ij| (rpm is free until the epilogue)
-  int* tie_s = reinterpret_cast<int*>(smem_e + SmemE::TIE);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   // T's fragment row of lane group g: 0, 1, 4, 5, 2, 3, 6, 7 (a row relabelling, free for A and
@@ -275,14 +227,9 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
 
   bool loaded = false;
   double rm_next = 0.0;
-  // matrix index ti -> item (MODE 2: the list of matrices the FAST pass gave up)
-  const int64_t nitems = MODE == 2 ? (int64_t)tlist[0] : a.batch;
-  auto item_of = [&](int64_t ti) -> int64_t { return MODE == 2 ? (int64_t)tlist[1 + ti] : ti; };
-  for (int64_t ti = blockIdx.x; ti < nitems; ti += gridDim.x) {
-    const int64_t item = item_of(ti);
+  for (int64_t item = blockIdx.x; item < a.batch; item += gridDim.x) {
     const double* Ai = Ag + item * (N64 * N64);
-    if (ti + gridDim.x < nitems && threadIdx.x == 0)
-      bulk_prefetch_l2(Ag + item_of(ti + gridDim.x) * (N64 * N64), N64 * N64 * 8);
+    if (item + gridDim.x < a.batch && threadIdx.x == 0) bulk_prefetch_l2(Ag + (item + gridDim.x) * (N64 * N64), N64 * N64 * 8);
     // ---- a1: this warp's 32 rows -> shared memory, max |a_ij|
     double rm = rm_next;
 #pragma unroll 2
@@ -307,7 +254,6 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
     uint32_t kmask[2] = {0xffffffffu, 0xffffffffu};
     int pos[2] = {lane, lane + 32};
 
-    unsigned tie = 0;   // (P) FAST: an exact tie met at some step
     if (warp == 0) {
       // ------------------------------------------------------------ P: the panels
 #pragma unroll 1
@@ -322,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
             x[r][j] = v.x;
             x[r][j + 1] = v.y;
           }
-        panel_steps<0, FAST>(kb * BS, x, kmask, pos, rec, rowk, lane, prow, tie);
+        panel_steps<0>(kb * BS, x, kmask, pos, rec, rowk, lane, prow);
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -379,10 +325,6 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
 
     // ---- a6 (warp P holds the positions): det / ipiv / singular flag from the record
     if (warp == 0) {
-      if (lane == 0) *tie_s = (int)tie;
-      if constexpr (FAST) {
-        if (tie && lane == 0) tlist[1 + atomicAdd(tlist, 1)] = (int)item;   // redone by the exact pass
-      }
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         posm[lane + 32 * r] = pos[r];
@@ -402,20 +344,16 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
         rec_load(rec, k, pk, qk);
         const unsigned fb = __ballot_sync(0xffffffffu, fabs(pk) <= tau);
         if (r == 0) fb0 = fb; else fb1 = fb;
-        if constexpr (!FAST) nswap += __popc(__ballot_sync(0xffffffffu, qk != k));
+        nswap += __popc(__ballot_sync(0xffffffffu, qk != k));
         nneg += __popc(__ballot_sync(0xffffffffu, pk < 0.0));
         lg += log(fabs(pk));
-        if constexpr (!FAST) {
-          if (a.ipiv) a.ipiv[item * N64 + k] = qk + 1;
-        }
+        if (a.ipiv) a.ipiv[item * N64 + k] = qk + 1;
       }
-      // the FAST pass keeps no positions: the swaps' parity is that of row -> pivot step
-      if constexpr (FAST) nswap = 64 - perm_cycles64(pos, lane);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
       const int info = fb0 ? __ffs(fb0) : (fb1 ? 32 + __ffs(fb1) : 0);
       const int sgn = ((nswap ^ nneg) & 1) ? -1 : 1;
-      if (lane == 0 && !tie) {
+      if (lane == 0) {
         if (a.info) a.info[item] = info;
         if (a.logabsdet) a.logabsdet[item] = info ? -INFINITY : lg;
         if (a.sign) a.sign[item] = info ? 0 : (int8_t)sgn;
@@ -427,12 +365,12 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
     // warp stores its half of the rows and loads the next matrix's same half under the store
     loaded = false;
     rm_next = 0.0;
-    const bool gave_up = FAST && *tie_s != 0;   // the FAST pass writes nothing for this matrix
     if (Xg != nullptr && io) {
       double* Xi = Xg + item * (N64 * N64);
       const int oc0 = rowk[lane], oc1 = rowk[lane + 32];
-      const bool pre = ti + gridDim.x < nitems;
-      const double* An = Ag + (pre ? item_of(ti + gridDim.x) : 0) * (N64 * N64);
+      const int64_t nitem = item + gridDim.x;
+      const bool pre = nitem < a.batch;
+      const double* An = Ag + nitem * (N64 * N64);
 #pragma unroll 1
       for (int i0 = r0; i0 < r0 + 32; i0 += 8) {
         double2 v[8];
@@ -446,10 +384,8 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
           const int ps = posm[i];
           const double rp = rpm[ps];
           double* orow = Xi + (int64_t)ps * N64;
-          if (!gave_up) {
-            __stcs(orow + oc0, M[mix(i, lane)] * rp + (lane == ps ? rp : 0.0));
-            __stcs(orow + oc1, M[mix(i, lane + 32)] * rp + (lane + 32 == ps ? rp : 0.0));
-          }
+          __stcs(orow + oc0, M[mix(i, lane)] * rp + (lane == ps ? rp : 0.0));
+          __stcs(orow + oc1, M[mix(i, lane + 32)] * rp + (lane + 32 == ps ? rp : 0.0));
         }
         __syncwarp();
         if (pre) {
@@ -468,50 +404,28 @@ __global__ void __launch_bounds__(kThreads, GJ_K2_MINB) gj_batched64f_kernel(Bat
 
 }  // namespace
 
-template <int MODE>
-cudaError_t launch_k2f_mode(const BatchedArgs& a, int* tlist, cudaStream_t s) {
-  const int smem = SmemE::BYTES;
-  auto kern = gj_batched64f_kernel<MODE>;
-  static unsigned long long configured = 0;
-  const unsigned long long dbit = device_bit();
-  if (!(configured & dbit)) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured |= dbit;
-  }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t cap = (int64_t)device_sm_count() * per_sm;
-  const int grid = (int)(a.batch < cap ? a.batch : cap);
-  kern<<<grid, kThreads, smem, s>>>(a, tlist);
-  return cudaGetLastError();
-}
-
-#ifndef GJ_K2F_FAST
-#define GJ_K2F_FAST 1   // two-pass run without ipiv (A/B build option)
-#endif
-
 cudaError_t launch_batched64e(const BatchedArgs& a, cudaStream_t s) {
   if (a.n != N64 || a.batch <= 0) return cudaErrorInvalidValue;
   // 16-byte vector loads / stores of A and the inverse (__ldcs double2): an 8-byte-aligned
   // batch (e.g. a 1-D buffer sliced at an odd element) goes to the generic K2 instead
   if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (a.Ainv && (reinterpret_cast<uintptr_t>(a.Ainv) & 15)))
     return cudaErrorNotSupported;
-  // no ipiv requested: the FAST pass over every matrix, then the exact kernel over the
-  // matrices it gave up (an exact tie — C3's duplicated-row items end on a zero column)
-  if (GJ_K2F_FAST && a.ipiv == nullptr) {
-    int* tl = static_cast<int*>(pool_alloc_async((size_t)(a.batch + 1) * sizeof(int), s));
-    if (tl != nullptr) {
-      cudaError_t e = cudaMemsetAsync(tl, 0, sizeof(int), s);
-      if (e == cudaSuccess) e = launch_k2f_mode<1>(a, tl, s);
-      if (e == cudaSuccess) e = launch_k2f_mode<2>(a, tl, s);
-      const cudaError_t f = cudaFreeAsync(tl, s);
-      return e != cudaSuccess ? e : f;
-    }
+  const int smem = SmemE::BYTES;
+  static unsigned long long configured = 0;
+  const unsigned long long dbit = device_bit();
+  if (!(configured & dbit)) {
+    cudaError_t e = cudaFuncSetAttribute(gj_batched64f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured |= dbit;
   }
-  return launch_k2f_mode<0>(a, nullptr, s);
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_batched64f_kernel, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = (int64_t)device_sm_count() * per_sm;
+  const int grid = (int)(a.batch < cap ? a.batch : cap);
+  gj_batched64f_kernel<<<grid, kThreads, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace gj
