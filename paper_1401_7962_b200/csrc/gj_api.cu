@@ -26,7 +26,14 @@ int device_sm_count() {
 
 void* pool_alloc_async(size_t bytes, cudaStream_t s) {
   // one library-owned pool per device, keeping its memory between calls (release threshold
-  // = max), so that a per-call scratch buffer costs no device allocation after the first
+  // = max), so that a per-call scratch buffer costs no device allocation after the first.
+  // Not under stream capture: an allocation from a user pool there may fail and invalidate
+  // the caller's capture, so a captured call takes the single-pass path instead.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
   int dev = 0;

@@ -97,3 +97,38 @@ def test_k1s_two_pass_bitwise_exact(gj, torch, kind, B, nrhs):
             a, b = a.view(torch.int32), b.view(torch.int32)
         assert torch.equal(a, b)
 
+
+
+def test_two_pass_concurrent_streams_and_graph_capture(gj, torch):
+    """Two calls in flight on two streams (each call's task list is its own stream-ordered
+    allocation), and a call captured into a CUDA graph (the capture takes the exact single
+    pass): all bitwise the exact kernel's results."""
+    A1 = torch.from_numpy(_batch("mixed", 30001, 21)).cuda()
+    A2 = torch.from_numpy(_batch("int", 20001, 22)).cuda()
+    ref1, ref2 = _run(gj, torch, A1, True), _run(gj, torch, A2, True)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    X1, X2 = torch.empty_like(A1), torch.empty_like(A2)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            r1 = gj.invert_batched(A1, out=X1, ipiv=False, stream=s1)
+        with torch.cuda.stream(s2):
+            r2 = gj.invert_batched(A2, out=X2, ipiv=False, stream=s2)
+        torch.cuda.synchronize()
+        for ref, r in ((ref1, r1), (ref2, r2)):
+            assert torch.equal(ref[0].view(torch.int32), r.inverse.cpu().view(torch.int32))
+            assert torch.equal(ref[1], r.logabsdet.cpu()) and torch.equal(ref[2], r.sign.cpu())
+    # graph capture
+    Xg = torch.empty_like(A1)
+    g = torch.cuda.CUDAGraph()
+    sc = torch.cuda.Stream()
+    sc.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(sc):
+        gj.invert_batched(A1, out=Xg, ipiv=False, stream=sc)   # warm-up outside the capture
+        torch.cuda.synchronize()
+        Xg.zero_()
+        with torch.cuda.graph(g, stream=sc):
+            gj.invert_batched(A1, out=Xg, ipiv=False, logabsdet=False, sign=False, det=False, info=False, stream=sc)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ref1[0].view(torch.int32), Xg.cpu().view(torch.int32))
