@@ -38,6 +38,13 @@
  *   Inputs containing NaN/Inf give unspecified results (not validated).
  *   Optional outputs: any output pointer documented "or NULL" may be NULL and is
  *     then not computed / written.
+ *   Scratch memory: the fp32 n = 32 batched paths (gj_invert_batched, gj_solve_batched,
+ *     gj_det) called with ipiv == NULL run two passes (K1f): a pass without
+ *     the tie-break, then the exact kernel over the matrices in which it met an exact
+ *     tie; the list of those (4 bytes per two matrices) is a stream-ordered allocation
+ *     from a memory pool the library owns, freed on the same stream.  Outputs are
+ *     bitwise those of the single exact pass.  Under stream capture, or if the pool
+ *     allocation fails, the call runs the single exact pass instead.
  */
 #ifndef GJINV_H
 #define GJINV_H
