@@ -71,6 +71,9 @@ constexpr int kWarpsPerBlock = GJ_K1_WPB;   // warps per CTA of the batched kern
 #ifndef GJ_K1B_PUB1
 #define GJ_K1B_PUB1 1   // the block publish as one asm block of predicated stores (A/B option)
 #endif
+#ifndef GJ_K1B_PUBM
+#define GJ_K1B_PUBM 1   // block publish with the two register slots merged (A/B option)
+#endif
 #ifndef GJ_K1B_UNROLL
 #define GJ_K1B_UNROLL 1
 #endif
@@ -726,10 +729,41 @@ __device__ __forceinline__ void k0_pos_from_bs(int (&pos)[R], const int (&bs)[R]
   for (int r = 0; r < R; ++r) pos[r] = bs[r] >= 0 ? k0 + bs[r] : pos[r];
 }
 
+// Seven predicated 16-byte shared stores of v[0..27] at dst (one asm block: ptxas keeps them
+// predicated instead of turning the run into a branch ladder).
+__device__ __forceinline__ void st7_if(bool pred, uint32_t dst, const float (&v)[28]) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+      "@p st.shared.v4.f32 [%1], {%2, %3, %4, %5};\n\t"
+      "@p st.shared.v4.f32 [%1+16], {%6, %7, %8, %9};\n\t"
+      "@p st.shared.v4.f32 [%1+32], {%10, %11, %12, %13};\n\t"
+      "@p st.shared.v4.f32 [%1+48], {%14, %15, %16, %17};\n\t"
+      "@p st.shared.v4.f32 [%1+64], {%18, %19, %20, %21};\n\t"
+      "@p st.shared.v4.f32 [%1+80], {%22, %23, %24, %25};\n\t"
+      "@p st.shared.v4.f32 [%1+96], {%26, %27, %28, %29};\n}" ::"r"(pred ? 1u : 0u), "r"(dst),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27])
+      : "memory");
+}
+
 // Publish the block's pivot rows: their other RW values T (unchanged since the block began).
 template <int R, int BS>
 __device__ __forceinline__ void blk_publish(const float (&T)[R][32 - BS], const int (&bs)[R], float* rbuf_g) {
   constexpr int RW = 32 - BS;
+  if constexpr (R == 2 && RW == 28 && GJ_K1B_PUBM) {
+    // merged slots: one store sequence carries the lane's (first) pivot row of the block, so
+    // that the active lanes of both slots share each wavefront; the rare lane whose two rows
+    // both pivot in the block stores its second one in a sequence that is predicated off
+    // (no wavefront) everywhere else
+    const bool p0 = bs[0] >= 0;
+    const int sb = p0 ? bs[0] : bs[1];
+    float D[28];
+#pragma unroll
+    for (int j = 0; j < 28; ++j) D[j] = p0 ? T[0][j] : T[1][j];
+    st7_if(sb >= 0, smem_u32(rbuf_g) + (uint32_t)(sb < 0 ? 0 : sb) * (RW * 4), D);
+    st7_if(p0 && bs[1] >= 0, smem_u32(rbuf_g) + (uint32_t)(bs[1] < 0 ? 0 : bs[1]) * (RW * 4), T[1]);
+  } else {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const uint32_t dst = smem_u32(rbuf_g) + (uint32_t)(bs[r] < 0 ? 0 : bs[r]) * (RW * 4);
@@ -755,6 +789,7 @@ __device__ __forceinline__ void blk_publish(const float (&T)[R][32 - BS], const 
       for (int j = 0; j < RW; j += 4)
         st_shared_v4_if(bs[r] >= 0, dst + 4u * j, T[r][j], T[r][j + 1], T[r][j + 2], T[r][j + 3]);
     }
+  }
   }
 }
 
