@@ -998,6 +998,9 @@ gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restri
           P[r][j] = NP[r][j];
         }
       }
+      // K1f gives a task up at the end of the block that met its first tie (warp-uniform):
+      // the rest is not worth computing, the exact pass redoes the task
+      if (FAST && tie) break;
     }
     // last block: its whole update, then x = [T | P] (register j = compact column j)
     blk_publish<R, BS>(T, bs, rbuf_g);
