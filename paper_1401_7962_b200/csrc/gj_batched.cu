@@ -1239,6 +1239,9 @@ __device__ __forceinline__ void slv_blocks(float (&x)[2][32], float (&b)[2][NR >
                                            uint32_t (&kmask)[2], int (&pos)[2], int (&bs)[2], float* rb,
                                            unsigned& tie, unsigned char* rec_g, int li, int g, int lane) {
   constexpr int BS = 4;
+  if constexpr (FAST) {
+    if (tie) return;   // given up at an exact tie (warp-uniform): the exact pass redoes the task
+  }
   slv_publish<NR, KB>(x, b, bs, rb);
   if constexpr (FAST) k0_pos_from_bs<2>(pos, bs, KB * BS);
   __syncwarp();
