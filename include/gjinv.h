@@ -45,7 +45,7 @@
  *     from a memory pool the library owns, freed on the same stream.  Outputs are
  *     bitwise those of the single exact pass.  Under stream capture, or if the pool
  *     allocation fails, the call runs the single exact pass instead.  A batch in which
- *     exact ties are common (e.g. small-integer matrices) runs up to ~1.8x slower this
+ *     exact ties are common (e.g. small-integer matrices) runs up to ~1.3x slower this
  *     way; passing an ipiv buffer selects the single exact pass.
  */
 #ifndef GJINV_H
