@@ -243,10 +243,12 @@ PIVOTING = {"none": 0, "partial": 1, "full": 2}
 
 
 def invert_batched_pivoting(A, strategy: str = "full", tol: Optional[float] = None, *, out=None,
-                            inverse: bool = True, stream=None) -> "FullResult":
+                            inverse: bool = True, pivots: bool = True, stream=None) -> "FullResult":
     """``gj_invert_batched_pivoting`` (n ≤ 32): the K6 kernel with ``strategy`` "none"
     (pivot a_kk, Eqs. (3)–(10)), "partial" (the listing's row search) or "full"
-    (Obs. 2–3); as :func:`invert_batched` plus ``jpiv``, the column swap sequence."""
+    (Obs. 2–3); as :func:`invert_batched` plus ``jpiv``, the column swap sequence.
+    ``pivots=False`` requests neither ipiv nor jpiv (their fields are None; full pivoting
+    at fp32 n = 32 then runs the two-pass K6f scheme)."""
     torch = _torch()
     if not A.is_cuda:
         raise ValueError("A must be a CUDA tensor")
@@ -262,29 +264,29 @@ def invert_batched_pivoting(A, strategy: str = "full", tol: Optional[float] = No
     if inverse:
         _check_out(out, A.shape, A.dtype, dev)
     X = (out if out is not None else torch.empty_like(A)) if inverse else None
-    o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev)
-    o_jpiv = torch.empty((B, n), dtype=torch.int32, device=dev)
+    o_ipiv = torch.empty((B, n), dtype=torch.int32, device=dev) if pivots else None
+    o_jpiv = torch.empty((B, n), dtype=torch.int32, device=dev) if pivots else None
     o_lg = torch.empty((B,), dtype=torch.float64, device=dev)
     o_sg = torch.empty((B,), dtype=torch.int8, device=dev)
     o_det = torch.empty((B,), dtype=A.dtype, device=dev)
     o_info = torch.empty((B,), dtype=torch.int32, device=dev)
     with torch.cuda.device(dev):
-        st = lib.gj_invert_batched_pivoting(_dt(A), n, B, A.data_ptr(), _ptr(X), o_ipiv.data_ptr(),
-                                            o_jpiv.data_ptr(), o_lg.data_ptr(), o_sg.data_ptr(), o_det.data_ptr(),
+        st = lib.gj_invert_batched_pivoting(_dt(A), n, B, A.data_ptr(), _ptr(X), _ptr(o_ipiv),
+                                            _ptr(o_jpiv), o_lg.data_ptr(), o_sg.data_ptr(), o_det.data_ptr(),
                                             o_info.data_ptr(), TOL_DEFAULT if tol is None else float(tol),
                                             PIVOTING[strategy], _stream_ptr(stream))
     _check(st)
     if squeeze:
         sq = lambda t: None if t is None else t[0]
-        return FullResult(sq(X), o_lg[0], o_sg[0], o_det[0], o_ipiv[0], o_jpiv[0], o_info[0])
+        return FullResult(sq(X), o_lg[0], o_sg[0], o_det[0], sq(o_ipiv), sq(o_jpiv), o_info[0])
     return FullResult(X, o_lg, o_sg, o_det, o_ipiv, o_jpiv, o_info)
 
 
 def invert_batched_full(A, tol: Optional[float] = None, *, out=None, inverse: bool = True,
-                        stream=None) -> "FullResult":
+                        pivots: bool = True, stream=None) -> "FullResult":
     """Full pivoting (``gj_invert_batched_full``, Obs. 2–3; n ≤ 32): as
     :func:`invert_batched` plus ``jpiv``, the 1-based column swap sequence."""
-    return invert_batched_pivoting(A, "full", tol, out=out, inverse=inverse, stream=stream)
+    return invert_batched_pivoting(A, "full", tol, out=out, inverse=inverse, pivots=pivots, stream=stream)
 
 
 def det(A, tol: Optional[float] = None, *, ipiv: bool = True, stream=None) -> Result:
