@@ -866,6 +866,9 @@ template <int R, int BS, int NST, int MODE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, (R == 4 ? 8 : (NST == 1 ? 16 : 12)) / kWarpsPerBlock)
 gj_blk32_kernel(BatchedArgs a, const __grid_constant__ TmaMaps tm, int* __restrict__ tlist) {
   constexpr bool FAST = MODE == 1;
+  if constexpr (MODE == 2) {
+    if (tlist[0] == 0) return;   // the usual case: K1f met no tie
+  }
   using Geo = BlkGeo<R>;
   using M = BlkMisc<R, BS>;
   constexpr int RW = M::RW, L = Geo::L, MT = Geo::M;
@@ -1289,6 +1292,9 @@ template <int NR, int MODE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, (NR >= 8 ? 8 : 12) / kWarpsPerBlock)
 gj_blk32s_kernel(BlkSolveArgs a, const __grid_constant__ TmaMaps tm, int* __restrict__ tlist) {
   constexpr bool FAST = MODE == 1;   // MODE as in gj_blk32_kernel (K1f's two passes)
+  if constexpr (MODE == 2) {
+    if (tlist[0] == 0) return;
+  }
   using S = SolveBlk<NR>;
   using Geo = BlkGeo<2>;
   constexpr int R = 2, BS = 4, L = Geo::L, MT = Geo::M, NB = NR > 0 ? NR : 1;
