@@ -28,6 +28,10 @@
 //   a6  log|det| = sum log|p_k| (fp64), sign = (-1)^swaps prod sign(p_k) (Eq. (13), G4).
 //   a7  un-permutation on store: Ainv[k][perm[k']] = (1/p_{perm[k]}) X[perm[k]][k'] (the
 //       listing's reverse-order column swaps, L179-L198, as one gather/scatter).
+// fp32 n = 32 runs the blocked K1b (blk_panel_step, BS = 4); a call without ipiv runs it in
+// two passes (K1f, launch_blk32): first with the pivot row taken from ballots when it is
+// unique — no positions, no tie-break — giving a task up at its first exact tie, then the
+// exact kernel over the tasks given up (bitwise the same outputs).
 // I/O: for n = NP and 16-byte aligned buffers each warp streams its 32 rows per task with
 // TMA (cp.async.bulk.tensor; 128/64/32-byte swizzle so every lane's row read and the
 // scatter are bank-conflict free), double-buffered against the compute; the output is
